@@ -1,0 +1,166 @@
+/*
+ * tkv.h — C ABI of the B200-native exact top-k decode-attention library (libtkv.so).
+ *
+ * This is the drop-in boundary for the hot path of the reference package `topk_kv`
+ * (arXiv 2502.06766 desk realisation, /root/reference/pkg/src/topk_kv). Every entry point
+ * below replaces one reference interface; the citation is given per function.
+ *
+ * Conventions
+ *   - Plain C types only: device pointers, sizes, an opaque CUDA stream (cudaStream_t passed
+ *     as void*). No torch / C++ types cross this boundary.
+ *   - All compute entry points are stream-ordered and asynchronous: they enqueue kernels on
+ *     `stream` and return without a host synchronisation (CUDA-graph capturable).
+ *   - The caller owns every buffer (q, caches, outputs, workspace). Nothing is allocated
+ *     inside a compute call. Size the scratch with tkv_workspace_bytes() and zero it once
+ *     with tkv_workspace_init(); kernels leave its control words zeroed again on exit.
+ *     One workspace per stream (calls sharing a workspace must be stream-ordered).
+ *   - Return value: TKV_OK (0) or a negative TKV_E* code; tkv_last_error() gives a
+ *     thread-local message for the last failing call on the calling thread.
+ *
+ * Data layout (HBM)
+ *   q        [B, Hq, d]            bf16   (query of the current decode token, post-RoPE)
+ *   k_cache  [B, Hkv, cache_rows, d] bf16  (rows [0, n_ctx[b]) = context: the top-k domain;
+ *   v_cache  [B, Hkv, cache_rows, d] bf16   rows [n_ctx[b], n_ctx[b]+n_win[b]) = generation
+ *                                            window, always attended, never retrieved —
+ *                                            reference GenWindow, attention.py:76-104)
+ *   n_ctx, n_win [B]               int32  device arrays
+ *   out      [B, Hq, d]            f32
+ *   idx      [B, Hq, k]            int32  global row ids (row_offset + local row); -1 pads
+ *                                          when k > n_ctx[b] (reference clamps, attention.py:147-149)
+ *   scores   [B, Hq, k]            f32    raw (unscaled) dot products q·K[idx]
+ *                                          (TopKResult.vals, ann.py:47-55); -inf pads
+ *   GQA: q head h reads kv head h / (Hq/Hkv) (contiguous-group convention; the reference is
+ *   MHA, SPEC.md:13 — with Hq == Hkv this is exactly the reference mapping).
+ */
+#ifndef TKV_H_
+#define TKV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TKV_VERSION 1
+
+/* status codes (reference error taxonomy, errors.py:4-42, mapped by the Python shim) */
+#define TKV_OK 0
+#define TKV_EBADSHAPE (-1)  /* -> ShapeError  (ann.py:210-211, tensor.py:33-36)          */
+#define TKV_EBADK (-2)      /* -> InputError  (attention.py:144-145, ann.py:212-213)     */
+#define TKV_ECONFIG (-3)    /* -> ConfigError (attention.py:122)                          */
+#define TKV_ECUDA (-4)      /* CUDA runtime failure (launch, bad pointer, no device)      */
+#define TKV_EWORKSPACE (-5) /* workspace too small / misaligned                           */
+
+/* combine modes (reference _joint_attend, attention.py:107-122) */
+#define TKV_COMBINE_JOINT 0
+#define TKV_COMBINE_ADDITIVE 1
+
+/* flags */
+#define TKV_F_SORTED 1u    /* idx/scores ordered score-desc, id-asc (TopKResult order, ann.py:166) */
+#define TKV_F_NO_FILTER 2u /* disable the sampled-threshold pre-filter (emit every score)       */
+
+typedef struct tkv_problem {
+  int32_t batch;         /* B                                                                  */
+  int32_t n_q_heads;     /* Hq                                                                 */
+  int32_t n_kv_heads;    /* Hkv; Hq % Hkv == 0 and Hq / Hkv in {1, 2, 4, 8}                     */
+  int32_t head_dim;      /* d; this build supports d == 128 (Llama-3 head shape)               */
+  int64_t cache_rows;    /* row stride between kv heads in k_cache / v_cache                   */
+  int64_t max_ctx;       /* host-side upper bound on n_ctx[b] (grid and workspace sizing)      */
+  int32_t k;             /* rows retrieved per q head (clamped per batch entry to n_ctx[b])    */
+  int32_t pinned_prefix; /* rows [0, p) always attended (attention.py:152-154); 0 = off        */
+  float scale;           /* softmax scale; reference uses 1/sqrt(d) (attention.py:159)         */
+  int32_t combine;       /* TKV_COMBINE_*                                                      */
+  uint32_t flags;        /* TKV_F_*                                                            */
+  int64_t row_offset;    /* global id of local row 0 (token-range shard); 0 when unsharded     */
+} tkv_problem;
+
+/* Library / device identification. */
+int tkv_version(void);
+const char* tkv_last_error(void);
+/* Checks that a CUDA device of compute capability 10.0 is current. */
+int tkv_device_check(void);
+
+/* Scratch sizing and one-time zeroing of the workspace control words. */
+int tkv_workspace_bytes(const tkv_problem* p, size_t* bytes);
+int tkv_workspace_init(const tkv_problem* p, void* workspace, size_t bytes, void* stream);
+
+/*
+ * One layer's top-k decode attention for all (b, q head): key scan, exact top-k selection
+ * (ties to the lower row id), V gather + numerically stable softmax jointly with the
+ * window rows.
+ * Replaces: topk_attend            attention.py:125-167 (batched over heads and batch)
+ *           knn_search (flat)      ann.py:203-218 → _flat_topk ann.py:154-167
+ *           ip_scores_all          ann_kernels.py:40-47
+ *           _joint_attend          attention.py:107-122
+ *           the per-head loop of decode_step, attention.py:213-230
+ * `scores` may be NULL (kept in the workspace).
+ */
+int tkv_topk_decode_attention(const tkv_problem* p, const void* q, const void* k_cache,
+                              const void* v_cache, const int32_t* n_ctx, const int32_t* n_win,
+                              float* out, int32_t* idx, float* scores, void* workspace,
+                              size_t workspace_bytes, void* stream);
+
+/*
+ * Exact top-k search only (no attention): knn_search flat, ann.py:203-218 / _flat_topk
+ * ann.py:154-167. With TKV_F_SORTED the result is TopKResult-ordered.
+ */
+int tkv_topk_search(const tkv_problem* p, const void* q, const void* k_cache,
+                    const int32_t* n_ctx, int32_t* idx, float* scores, void* workspace,
+                    size_t workspace_bytes, void* stream);
+
+/*
+ * Append this token's post-RoPE k/v rows ([B, Hkv, d] bf16) at row base[b] + count[b] of
+ * every kv head (base may be NULL → row count[b]). Replaces GenWindow.append,
+ * attention.py:94-100 (with base = n_ctx, count = n_win: the window grows after the context).
+ * With advance != 0, count[b] += 1 on device, so a decode loop needs no host sync.
+ * Rows >= cache_rows are not written (capacity is the caller's, as GenWindow's, :96-97).
+ */
+int tkv_kv_append(int32_t batch, int32_t n_kv_heads, int32_t head_dim, int64_t cache_rows,
+                  void* k_cache, void* v_cache, const void* k_new, const void* v_new,
+                  const int32_t* base, int32_t* count, int32_t advance, void* stream);
+
+/*
+ * Token-range sharded stages (decode-time context parallelism; the reference is
+ * single-process). Shard g holds global rows [row_offset, row_offset+n_ctx[b]).
+ *   1. tkv_shard_candidates: local exact top-k → packed candidates cand[B*Hq*k] (uint64,
+ *      (order-preserving score key << 32) | ~global_id; 0 = empty slot).
+ *   2. caller all-gathers cand from every shard → gathered[n_shards][B*Hq*k].
+ *   3. tkv_shard_merge: exact global top-k over the gathered candidates (ties → lower
+ *      global id ⇔ lower shard), writes idx/scores (global ids) and the softmax reference max.
+ *   4. tkv_shard_partial: V rows this shard owns → partial[B*Hq*(d+1)] = (l, o[d]) against
+ *      the global max (no rescale needed on combine).
+ *   5. caller all-reduces partial with SUM.
+ *   6. tkv_shard_finalize: window rows + normalisation → out.
+ */
+int tkv_shard_candidates(const tkv_problem* p, const void* q, const void* k_cache,
+                         const int32_t* n_ctx, uint64_t* cand, void* workspace,
+                         size_t workspace_bytes, void* stream);
+int tkv_shard_merge(const tkv_problem* p, const uint64_t* gathered, int32_t n_shards,
+                    int32_t* idx, float* scores, void* workspace, size_t workspace_bytes,
+                    void* stream);
+int tkv_shard_partial(const tkv_problem* p, const void* q, const void* k_cache,
+                      const void* v_cache, const int32_t* n_ctx, const int32_t* idx,
+                      const float* scores, float* partial, void* workspace,
+                      size_t workspace_bytes, void* stream);
+int tkv_shard_finalize(const tkv_problem* p, const void* q, const void* k_cache,
+                       const void* v_cache, const int32_t* n_ctx, const int32_t* n_win,
+                       const float* partial, float* out, void* workspace,
+                       size_t workspace_bytes, void* stream);
+
+/* Number of kernels the last compute call on this thread enqueued (for launch accounting). */
+int tkv_last_launch_count(void);
+
+/*
+ * Measurement hook: when both events are non-NULL (cudaEvent_t as void*), subsequent compute
+ * calls on this thread record `start` / `stop` on their stream immediately before / after the
+ * main key-scan kernel launch, so a caller can time the dominant kernel with CUDA events on
+ * the stream it runs on. Pass NULLs to disable.
+ */
+int tkv_profile_scan_events(void* start, void* stop);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TKV_H_ */

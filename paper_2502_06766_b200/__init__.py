@@ -1,0 +1,37 @@
+"""B200-native exact top-k decode attention (hot path of arXiv 2502.06766, `topk_kv`).
+
+Drop-in surface (same names as the reference's `topk_kv/__init__.py:19-31`):
+    topk_attend, TierAccounting, build_index, knn_search, TopKResult, MipsIndex,
+    recall_at_k, and the error taxonomy.
+Batched device API (the fast path):
+    topk_decode_attention, topk_search, kv_append, TopkDecoder,
+    sharded_topk_attention / CudaStages (token-range sharding over torch.distributed).
+The compute runs in libtkv.so (sm_100a CUDA kernels behind the C ABI in include/tkv.h).
+"""
+
+from .ann import DeviceValues, MipsIndex, TopKResult, build_index, knn_search, recall_at_k
+from .attention import VALUE_ROW_BYTES, TierAccounting, topk_attend
+from .decoder import TopkDecoder
+from .errors import (
+    ConfigError,
+    DegenerateError,
+    DeviceError,
+    DomainError,
+    FormatError,
+    InfeasibleBudgetError,
+    InputError,
+    ShapeError,
+    TopkKvError,
+)
+from .ops import Workspace, kv_append, topk_decode_attention, topk_search
+from .sharded import CudaStages, shard_range, sharded_topk_attention
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "ConfigError", "CudaStages", "DegenerateError", "DeviceError", "DeviceValues", "DomainError",
+    "FormatError", "InfeasibleBudgetError", "InputError", "MipsIndex", "ShapeError",
+    "TierAccounting", "TopKResult", "TopkDecoder", "TopkKvError", "VALUE_ROW_BYTES", "Workspace",
+    "build_index", "knn_search", "kv_append", "recall_at_k", "shard_range",
+    "sharded_topk_attention", "topk_attend", "topk_decode_attention", "topk_search",
+]

@@ -1,0 +1,459 @@
+// api.cu — extern "C" boundary of libtkv.so (declared in include/tkv.h).
+//
+// Host-side validation mirrors the reference's error behaviour where it can be checked
+// without touching device data (errors.py:4-42; attention.py:144-145; ann.py:210-213;
+// attention.py:122); the Python shim maps the status codes back onto the reference's
+// exception classes. Device-resident values (n_ctx, n_win, finiteness of q/K) are not
+// inspected here — that would cost a host synchronisation or a full scan.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/tkv.h"
+#include "common.cuh"
+#include "internal.h"
+
+using namespace tkv;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_launches = 0;
+thread_local cudaEvent_t g_scan_start = nullptr, g_scan_stop = nullptr;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define TKV_LAUNCH(expr)                                                            \
+  do {                                                                              \
+    cudaError_t e__ = (expr);                                                       \
+    ++g_launches;                                                                   \
+    if (e__ != cudaSuccess) return fail(TKV_ECUDA, "%s: %s", #expr, cudaGetErrorString(e__)); \
+  } while (0)
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct Layout {
+  size_t ticket_s, ticket_g, flag, gflag, ctrl_end;
+  size_t cnt, thr, mmax, mkth, mkb, samp, cand, sidx, sscore, pl, po, total;
+  int64_t cap;
+  int nchunks;
+};
+
+Layout make_layout(const tkv_problem* p) {
+  Layout L{};
+  const size_t BH = static_cast<size_t>(p->batch) * p->n_q_heads;
+  const size_t BK = static_cast<size_t>(p->batch) * p->n_kv_heads;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off = align_up(off + (bytes ? bytes : 1), 256);
+    return o;
+  };
+  L.ticket_s = take(BK * 4);
+  L.ticket_g = take(BH * 4);
+  L.flag = take(BH * 4);
+  L.gflag = take(BK * 4);
+  L.ctrl_end = off;
+  L.cnt = take(BH * 4);
+  L.thr = take(BH * 4);
+  L.mmax = take(BH * 4);
+  L.mkth = take(BH * 8);
+  L.mkb = take(BH * 4);
+  L.samp = take(BH * kSamples * 4);
+  L.cap = p->max_ctx > 0 ? p->max_ctx : 1;
+  L.cand = take(BH * static_cast<size_t>(L.cap) * 8);
+  L.sidx = take(BH * static_cast<size_t>(p->k) * 4);
+  L.sscore = take(BH * static_cast<size_t>(p->k) * 4);
+  L.nchunks = static_cast<int>((p->k + kAttendChunk - 1) / kAttendChunk);
+  L.pl = take(BH * L.nchunks * 4);
+  L.po = take(BH * L.nchunks * kD * 4);
+  L.total = off;
+  return L;
+}
+
+int validate(const tkv_problem* p) {
+  if (!p) return fail(TKV_EBADSHAPE, "problem is NULL");
+  if (p->batch < 1 || p->n_q_heads < 1 || p->n_kv_heads < 1)
+    return fail(TKV_EBADSHAPE, "batch/heads must be >= 1 (got B=%d Hq=%d Hkv=%d)", p->batch,
+                p->n_q_heads, p->n_kv_heads);
+  if (p->n_q_heads % p->n_kv_heads != 0)
+    return fail(TKV_EBADSHAPE, "Hq=%d not a multiple of Hkv=%d", p->n_q_heads, p->n_kv_heads);
+  const int G = p->n_q_heads / p->n_kv_heads;
+  if (G != 1 && G != 2 && G != 4 && G != 8)
+    return fail(TKV_EBADSHAPE, "GQA group size Hq/Hkv=%d must be 1, 2, 4 or 8", G);
+  if (p->head_dim != kD) return fail(TKV_EBADSHAPE, "head_dim=%d unsupported (this build: %d)", p->head_dim, kD);
+  if (p->k < 1) return fail(TKV_EBADK, "k must be >= 1 (got %d)", p->k);
+  if (p->max_ctx < 0 || p->max_ctx > 0x7fffffffLL)
+    return fail(TKV_EBADSHAPE, "max_ctx=%lld out of range", static_cast<long long>(p->max_ctx));
+  if (p->cache_rows < p->max_ctx)
+    return fail(TKV_EBADSHAPE, "cache_rows=%lld < max_ctx=%lld", static_cast<long long>(p->cache_rows),
+                static_cast<long long>(p->max_ctx));
+  if (p->row_offset < 0 || p->row_offset + p->max_ctx > 0x7fffffffLL)
+    return fail(TKV_EBADSHAPE, "row_offset=%lld out of range", static_cast<long long>(p->row_offset));
+  if (p->combine != TKV_COMBINE_JOINT && p->combine != TKV_COMBINE_ADDITIVE)
+    return fail(TKV_ECONFIG, "unknown combine mode %d", p->combine);
+  if ((p->flags & TKV_F_SORTED) && p->k > kSortMax)
+    return fail(TKV_ECONFIG, "sorted output supports k <= %d (got %d)", kSortMax, p->k);
+  if (p->pinned_prefix < 0) return fail(TKV_EBADK, "pinned_prefix must be >= 0");
+  return TKV_OK;
+}
+
+int check_ptr(const void* ptr, const char* name, size_t align) {
+  if (!ptr) return fail(TKV_EBADSHAPE, "%s is NULL", name);
+  if (reinterpret_cast<uintptr_t>(ptr) % align)
+    return fail(TKV_EBADSHAPE, "%s must be %zu-byte aligned", name, align);
+  return TKV_OK;
+}
+
+int check_ws(const tkv_problem* p, void* ws, size_t bytes, Layout* L) {
+  *L = make_layout(p);
+  if (!ws) return fail(TKV_EWORKSPACE, "workspace is NULL");
+  if (reinterpret_cast<uintptr_t>(ws) % 256) return fail(TKV_EWORKSPACE, "workspace must be 256-byte aligned");
+  if (bytes < L->total)
+    return fail(TKV_EWORKSPACE, "workspace too small: %zu < %zu bytes", bytes, L->total);
+  return TKV_OK;
+}
+
+template <typename T>
+T* at(void* ws, size_t off) {
+  return reinterpret_cast<T*>(static_cast<char*>(ws) + off);
+}
+
+#define TRY(x)                 \
+  do {                         \
+    const int r__ = (x);       \
+    if (r__ != TKV_OK) return r__; \
+  } while (0)
+
+// sample → scan → select (+ fallback scan/select) [→ sort]; results in idx/scores
+int run_select(const tkv_problem* p, const void* q, const void* k_cache, const int32_t* n_ctx,
+               int32_t* idx, float* scores, void* ws, const Layout& L, cudaStream_t st,
+               uint64_t* packed_out) {
+  const int G = p->n_q_heads / p->n_kv_heads;
+  SampleParams sp{};
+  sp.q = static_cast<const __nv_bfloat16*>(q);
+  sp.kc = static_cast<const __nv_bfloat16*>(k_cache);
+  sp.cache_rows = p->cache_rows;
+  sp.B = p->batch;
+  sp.Hq = p->n_q_heads;
+  sp.Hkv = p->n_kv_heads;
+  sp.G = G;
+  sp.k = p->k;
+  sp.n_ctx = n_ctx;
+  sp.no_filter = (p->flags & TKV_F_NO_FILTER) ? 1 : 0;
+  sp.samp = at<uint32_t>(ws, L.samp);
+  sp.thr = at<uint32_t>(ws, L.thr);
+  sp.cand_cnt = at<uint32_t>(ws, L.cnt);
+  sp.ticket = at<uint32_t>(ws, L.ticket_s);
+  TKV_LAUNCH(launch_sample(sp, st));
+
+  ScanParams cp{};
+  cp.q = sp.q;
+  cp.kc = sp.kc;
+  cp.cache_rows = p->cache_rows;
+  cp.B = p->batch;
+  cp.Hq = p->n_q_heads;
+  cp.Hkv = p->n_kv_heads;
+  cp.G = G;
+  cp.max_ctx = p->max_ctx;
+  cp.n_ctx = n_ctx;
+  cp.row_offset = static_cast<uint32_t>(p->row_offset);
+  cp.thr = sp.thr;
+  cp.cand = at<uint64_t>(ws, L.cand);
+  cp.cap = L.cap;
+  cp.cand_cnt = sp.cand_cnt;
+  cp.flag_fail = at<uint32_t>(ws, L.flag);
+  cp.group_fail = at<uint32_t>(ws, L.gflag);
+  cp.fallback = 0;
+  if (g_scan_start && g_scan_stop) cudaEventRecord(g_scan_start, st);
+  TKV_LAUNCH(launch_scan(cp, st));
+  if (g_scan_start && g_scan_stop) cudaEventRecord(g_scan_stop, st);
+
+  SelectParams sl{};
+  sl.src = cp.cand;
+  sl.src_stride = L.cap;
+  sl.src_cnt = cp.cand_cnt;
+  sl.B = p->batch;
+  sl.Hq = p->n_q_heads;
+  sl.Hkv = p->n_kv_heads;
+  sl.G = G;
+  sl.k = p->k;
+  sl.n_ctx = n_ctx;
+  sl.idx = idx;
+  sl.scores = scores;
+  sl.meta_max = at<float>(ws, L.mmax);
+  sl.meta_kth = at<uint64_t>(ws, L.mkth);
+  sl.meta_kb = at<int32_t>(ws, L.mkb);
+  sl.flag_fail = at<uint32_t>(ws, L.flag);
+  sl.group_fail = at<uint32_t>(ws, L.gflag);
+  sl.cand_cnt = cp.cand_cnt;
+  sl.packed_out = packed_out;
+  sl.pass = kPassMain;
+  TKV_LAUNCH(launch_select(sl, st));
+
+  // exactness fallback: heads whose sampled threshold let fewer than k rows through
+  cp.fallback = 1;
+  TKV_LAUNCH(launch_scan(cp, st));
+  sl.pass = kPassFallback;
+  TKV_LAUNCH(launch_select(sl, st));
+
+  if (p->flags & TKV_F_SORTED) {
+    SortParams so{idx, scores, sl.meta_kb, p->k};
+    TKV_LAUNCH(launch_sort(so, p->batch * p->n_q_heads, st));
+  }
+  return TKV_OK;
+}
+
+AttendParams make_attend(const tkv_problem* p, const void* q, const void* k_cache, const void* v_cache,
+                         const int32_t* n_ctx, const int32_t* n_win, const int32_t* idx,
+                         const float* scores, void* ws, const Layout& L) {
+  AttendParams a{};
+  a.q = static_cast<const __nv_bfloat16*>(q);
+  a.kc = static_cast<const __nv_bfloat16*>(k_cache);
+  a.vc = static_cast<const __nv_bfloat16*>(v_cache);
+  a.cache_rows = p->cache_rows;
+  a.B = p->batch;
+  a.Hq = p->n_q_heads;
+  a.Hkv = p->n_kv_heads;
+  a.G = p->n_q_heads / p->n_kv_heads;
+  a.k = p->k;
+  a.n_ctx = n_ctx;
+  a.n_win = n_win;
+  a.row_offset = p->row_offset;
+  a.pinned = p->pinned_prefix;
+  a.scale = p->scale;
+  a.combine = p->combine;
+  a.idx = idx;
+  a.scores = scores;
+  a.meta_max = at<float>(ws, L.mmax);
+  a.meta_kth = at<uint64_t>(ws, L.mkth);
+  a.meta_kb = at<int32_t>(ws, L.mkb);
+  a.part_l = at<float>(ws, L.pl);
+  a.part_o = at<float>(ws, L.po);
+  a.ticket = at<uint32_t>(ws, L.ticket_g);
+  a.nchunks = L.nchunks;
+  return a;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tkv_version(void) { return TKV_VERSION; }
+
+const char* tkv_last_error(void) { return g_err.c_str(); }
+
+int tkv_last_launch_count(void) { return g_launches; }
+
+int tkv_profile_scan_events(void* start, void* stop) {
+  g_scan_start = static_cast<cudaEvent_t>(start);
+  g_scan_stop = static_cast<cudaEvent_t>(stop);
+  return TKV_OK;
+}
+
+int tkv_device_check(void) {
+  int dev = 0, n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    return fail(TKV_ECUDA, "no CUDA device: %s", e == cudaSuccess ? "count is 0" : cudaGetErrorString(e));
+  cudaGetDevice(&dev);
+  int major = 0, minor = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  if (major != 10 || minor != 0)
+    return fail(TKV_ECUDA, "device %d is sm_%d%d; libtkv is built for sm_100a only", dev, major, minor);
+  return TKV_OK;
+}
+
+int tkv_workspace_bytes(const tkv_problem* p, size_t* bytes) {
+  TRY(validate(p));
+  if (!bytes) return fail(TKV_EBADSHAPE, "bytes is NULL");
+  *bytes = make_layout(p).total;
+  return TKV_OK;
+}
+
+int tkv_workspace_init(const tkv_problem* p, void* ws, size_t bytes, void* stream) {
+  g_launches = 0;
+  TRY(validate(p));
+  Layout L;
+  TRY(check_ws(p, ws, bytes, &L));
+  cudaError_t e = cudaMemsetAsync(ws, 0, L.ctrl_end, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(TKV_ECUDA, "cudaMemsetAsync: %s", cudaGetErrorString(e));
+  return TKV_OK;
+}
+
+int tkv_topk_decode_attention(const tkv_problem* p, const void* q, const void* k_cache,
+                              const void* v_cache, const int32_t* n_ctx, const int32_t* n_win,
+                              float* out, int32_t* idx, float* scores, void* ws, size_t ws_bytes,
+                              void* stream) {
+  g_launches = 0;
+  TRY(validate(p));
+  Layout L;
+  TRY(check_ws(p, ws, ws_bytes, &L));
+  TRY(check_ptr(q, "q", 16));
+  TRY(check_ptr(k_cache, "k_cache", 16));
+  TRY(check_ptr(v_cache, "v_cache", 16));
+  TRY(check_ptr(n_ctx, "n_ctx", 4));
+  TRY(check_ptr(out, "out", 4));
+  TRY(check_ptr(idx, "idx", 4));
+  if (n_win) TRY(check_ptr(n_win, "n_win", 4));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float* sc = scores ? scores : at<float>(ws, L.sscore);
+  TRY(run_select(p, q, k_cache, n_ctx, idx, sc, ws, L, st, nullptr));
+  AttendParams a = make_attend(p, q, k_cache, v_cache, n_ctx, n_win, idx, sc, ws, L);
+  a.partial_only = 0;
+  a.out = out;
+  TKV_LAUNCH(launch_attend(a, st));
+  return TKV_OK;
+}
+
+int tkv_topk_search(const tkv_problem* p, const void* q, const void* k_cache, const int32_t* n_ctx,
+                    int32_t* idx, float* scores, void* ws, size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  TRY(validate(p));
+  Layout L;
+  TRY(check_ws(p, ws, ws_bytes, &L));
+  TRY(check_ptr(q, "q", 16));
+  TRY(check_ptr(k_cache, "k_cache", 16));
+  TRY(check_ptr(n_ctx, "n_ctx", 4));
+  TRY(check_ptr(idx, "idx", 4));
+  float* sc = scores ? scores : at<float>(ws, L.sscore);
+  return run_select(p, q, k_cache, n_ctx, idx, sc, ws, L, static_cast<cudaStream_t>(stream), nullptr);
+}
+
+int tkv_kv_append(int32_t batch, int32_t n_kv_heads, int32_t head_dim, int64_t cache_rows,
+                  void* k_cache, void* v_cache, const void* k_new, const void* v_new,
+                  const int32_t* base, int32_t* count, int32_t advance, void* stream) {
+  g_launches = 0;
+  if (batch < 1 || n_kv_heads < 1) return fail(TKV_EBADSHAPE, "batch/heads must be >= 1");
+  if (head_dim != kD) return fail(TKV_EBADSHAPE, "head_dim=%d unsupported (this build: %d)", head_dim, kD);
+  if (cache_rows < 1) return fail(TKV_EBADSHAPE, "cache_rows must be >= 1");
+  TRY(check_ptr(k_cache, "k_cache", 16));
+  TRY(check_ptr(v_cache, "v_cache", 16));
+  TRY(check_ptr(k_new, "k_new", 16));
+  TRY(check_ptr(v_new, "v_new", 16));
+  TRY(check_ptr(count, "count", 4));
+  if (base) TRY(check_ptr(base, "base", 4));
+  AppendParams a{};
+  a.B = batch;
+  a.Hkv = n_kv_heads;
+  a.cache_rows = cache_rows;
+  a.kc = static_cast<__nv_bfloat16*>(k_cache);
+  a.vc = static_cast<__nv_bfloat16*>(v_cache);
+  a.k_new = static_cast<const __nv_bfloat16*>(k_new);
+  a.v_new = static_cast<const __nv_bfloat16*>(v_new);
+  a.base = base;
+  a.count = count;
+  a.advance = advance;
+  TKV_LAUNCH(launch_append(a, static_cast<cudaStream_t>(stream)));
+  return TKV_OK;
+}
+
+int tkv_shard_candidates(const tkv_problem* p, const void* q, const void* k_cache, const int32_t* n_ctx,
+                         uint64_t* cand, void* ws, size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  TRY(validate(p));
+  Layout L;
+  TRY(check_ws(p, ws, ws_bytes, &L));
+  TRY(check_ptr(q, "q", 16));
+  TRY(check_ptr(k_cache, "k_cache", 16));
+  TRY(check_ptr(n_ctx, "n_ctx", 4));
+  TRY(check_ptr(cand, "cand", 8));
+  return run_select(p, q, k_cache, n_ctx, at<int32_t>(ws, L.sidx), at<float>(ws, L.sscore), ws, L,
+                    static_cast<cudaStream_t>(stream), cand);
+}
+
+int tkv_shard_merge(const tkv_problem* p, const uint64_t* gathered, int32_t n_shards, int32_t* idx,
+                    float* scores, void* ws, size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  TRY(validate(p));
+  Layout L;
+  TRY(check_ws(p, ws, ws_bytes, &L));
+  TRY(check_ptr(gathered, "gathered", 8));
+  TRY(check_ptr(idx, "idx", 4));
+  TRY(check_ptr(scores, "scores", 4));
+  if (n_shards < 1) return fail(TKV_EBADSHAPE, "n_shards must be >= 1");
+  // gathered is [n_shards][B*Hq*k] (all_gather_into_tensor layout), read in place.
+  const int G = p->n_q_heads / p->n_kv_heads;
+  SelectParams sl{};
+  sl.src = gathered;
+  sl.src_stride = static_cast<int64_t>(n_shards) * p->k;
+  sl.shard_stride = static_cast<int64_t>(p->batch) * p->n_q_heads * p->k;
+  sl.src_cnt = nullptr;
+  sl.src_fixed = static_cast<int64_t>(n_shards) * p->k;
+  sl.B = p->batch;
+  sl.Hq = p->n_q_heads;
+  sl.Hkv = p->n_kv_heads;
+  sl.G = G;
+  sl.k = p->k;
+  sl.n_ctx = nullptr;
+  sl.idx = idx;
+  sl.scores = scores;
+  sl.meta_max = at<float>(ws, L.mmax);
+  sl.meta_kth = at<uint64_t>(ws, L.mkth);
+  sl.meta_kb = at<int32_t>(ws, L.mkb);
+  sl.flag_fail = at<uint32_t>(ws, L.flag);
+  sl.group_fail = at<uint32_t>(ws, L.gflag);
+  sl.cand_cnt = at<uint32_t>(ws, L.cnt);
+  sl.packed_out = nullptr;
+  sl.pass = kPassMerge;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  TKV_LAUNCH(launch_select(sl, st));
+  if (p->flags & TKV_F_SORTED) {
+    SortParams so{idx, scores, sl.meta_kb, p->k};
+    TKV_LAUNCH(launch_sort(so, p->batch * p->n_q_heads, st));
+  }
+  return TKV_OK;
+}
+
+int tkv_shard_partial(const tkv_problem* p, const void* q, const void* k_cache, const void* v_cache,
+                      const int32_t* n_ctx, const int32_t* idx, const float* scores, float* partial,
+                      void* ws, size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  TRY(validate(p));
+  Layout L;
+  TRY(check_ws(p, ws, ws_bytes, &L));
+  TRY(check_ptr(q, "q", 16));
+  TRY(check_ptr(k_cache, "k_cache", 16));
+  TRY(check_ptr(v_cache, "v_cache", 16));
+  TRY(check_ptr(n_ctx, "n_ctx", 4));
+  TRY(check_ptr(idx, "idx", 4));
+  TRY(check_ptr(scores, "scores", 4));
+  TRY(check_ptr(partial, "partial", 4));
+  AttendParams a = make_attend(p, q, k_cache, v_cache, n_ctx, nullptr, idx, scores, ws, L);
+  a.partial_only = 1;
+  a.partial_out = partial;
+  TKV_LAUNCH(launch_attend(a, static_cast<cudaStream_t>(stream)));
+  return TKV_OK;
+}
+
+int tkv_shard_finalize(const tkv_problem* p, const void* q, const void* k_cache, const void* v_cache,
+                       const int32_t* n_ctx, const int32_t* n_win, const float* partial, float* out,
+                       void* ws, size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  TRY(validate(p));
+  Layout L;
+  TRY(check_ws(p, ws, ws_bytes, &L));
+  TRY(check_ptr(q, "q", 16));
+  TRY(check_ptr(k_cache, "k_cache", 16));
+  TRY(check_ptr(v_cache, "v_cache", 16));
+  TRY(check_ptr(n_ctx, "n_ctx", 4));
+  TRY(check_ptr(partial, "partial", 4));
+  TRY(check_ptr(out, "out", 4));
+  AttendParams a = make_attend(p, q, k_cache, v_cache, n_ctx, n_win, nullptr, nullptr, ws, L);
+  a.partial_in = partial;
+  a.out = out;
+  TKV_LAUNCH(launch_finalize(a, static_cast<cudaStream_t>(stream)));
+  return TKV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,218 @@
+// common.cuh — shared device helpers for the sm_100a top-k decode-attention kernels.
+//
+// Numerics contract (reference: ann_kernels.py:31-47, ann.py:154-167, attention.py:107-167):
+//   * scores are raw dot products q·K[row] of bf16 inputs; products are exact in fp32 and the
+//     128-term sum is accumulated in fp32 on the tensor cores (HMMA, fp32 accumulate). The
+//     reference accumulates in f64; the difference (~1e-6 relative) is far inside the
+//     near-tie exemption of the parity contract (|Δs| < 1e-3·|s_k|).
+//   * selection order is the reference's: larger score first, ties to the LOWER row id
+//     (ann.py:162-166). It is realised as one 64-bit composite per row:
+//        comp = (order-preserving key of the f32 score) << 32 | ~global_row_id
+//     so "top-k by composite, descending" == reference order, and composites are unique.
+//   * -0.0 is canonicalised to +0.0 before keying (the reference compares f64 values, where
+//     -0.0 == +0.0 and the lower id wins).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tkv {
+
+constexpr int kD = 128;                 // head dim this build supports
+constexpr unsigned kFull = 0xffffffffu;
+constexpr float kLog2e = 1.4426950408889634f;
+
+// ---------------------------------------------------------------- score keys / composites
+__device__ __forceinline__ uint32_t score_key(float f) {
+  uint32_t b = __float_as_uint(f);
+  if (b == 0x80000000u) b = 0u;  // -0.0 -> +0.0
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float key_score(uint32_t k) {
+  uint32_t b = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+  return __uint_as_float(b);
+}
+__device__ __forceinline__ uint64_t make_comp(uint32_t key, uint32_t gid) {
+  return (static_cast<uint64_t>(key) << 32) | static_cast<uint32_t>(~gid);
+}
+__device__ __forceinline__ uint32_t comp_gid(uint64_t c) { return ~static_cast<uint32_t>(c); }
+__device__ __forceinline__ uint32_t comp_key(uint64_t c) { return static_cast<uint32_t>(c >> 32); }
+
+// ---------------------------------------------------------------- memory
+// Streaming 128-bit load: read-only path, no L1 allocation, 256B L2 prefetch (K is read once).
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+// Gather load (V rows): read-only path, no L1 allocation.
+__device__ __forceinline__ uint4 ldg_nc(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t u4_word(const uint4& v, int i) {
+  return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
+}
+
+__device__ __forceinline__ float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+
+// ---------------------------------------------------------------- HMMA key-scan tile
+// One warp scores a 16-row × 128 tile of K against up to 8 q heads of one GQA group with
+// 8 × mma.m16n8k16 (bf16 in, fp32 accumulate). The k-dimension is permuted so that every
+// thread's A/B fragments come straight from 16-byte contiguous global loads (no shared
+// memory, no ldmatrix):
+//   thread (g = lane/4, c = lane%4) loads, for its rows g and g+8, the 16-byte chunks
+//   j = 0..3 at element offset 32*j + 8*c  (a warp instruction covers 64 contiguous bytes of
+//   each of 8 rows = whole 32-byte sectors);
+//   mma step s = 2*j + h consumes elements 32*j + 8*c + 4*h + {0,1,2,3} of that chunk as the
+//   A slots {2c, 2c+1, 2c+8, 2c+9}; the B fragment (q head n = g) uses the same map.
+// The accumulator layout is the standard one:
+//   acc[0] = S[row g][head 2c], acc[1] = S[row g][head 2c+1],
+//   acc[2] = S[row g+8][head 2c], acc[3] = S[row g+8][head 2c+1].
+// A row's score depends only on that row and q (fixed step order 0..7), so any kernel that
+// scores a row with this function gets bit-identical values (used for pinned-row membership).
+struct QFrag {
+  uint32_t w[8][2];
+};
+
+__device__ __forceinline__ void load_qfrag(QFrag& f, const __nv_bfloat16* qgroup, int G, int lane) {
+  const int g = lane >> 2, c = lane & 3;
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    if (g < G) {
+      const uint2 v = *reinterpret_cast<const uint2*>(qgroup + g * kD + 32 * (s >> 1) + 8 * c +
+                                                      4 * (s & 1));
+      f.w[s][0] = v.x;
+      f.w[s][1] = v.y;
+    } else {
+      f.w[s][0] = 0u;
+      f.w[s][1] = 0u;
+    }
+  }
+}
+
+__device__ __forceinline__ void mma_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                          uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// rowA / rowB: pointers to the two rows this thread loads (row g and row g+8 of the tile);
+// invalid rows are zero-filled (never dereferenced).
+__device__ __forceinline__ void load_tile(uint4 (&a)[2][4], const __nv_bfloat16* rowA, bool okA,
+                                          const __nv_bfloat16* rowB, bool okB, int c) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    a[0][j] = okA ? ldg_stream(rowA + 32 * j + 8 * c) : make_uint4(0, 0, 0, 0);
+    a[1][j] = okB ? ldg_stream(rowB + 32 * j + 8 * c) : make_uint4(0, 0, 0, 0);
+  }
+}
+
+__device__ __forceinline__ void score_tile(float (&acc)[4], const uint4 (&a)[2][4], const QFrag& f) {
+  acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int s = 2 * j + h;
+      mma_16816(acc, u4_word(a[0][j], 2 * h), u4_word(a[1][j], 2 * h), u4_word(a[0][j], 2 * h + 1),
+                u4_word(a[1][j], 2 * h + 1), f.w[s][0], f.w[s][1]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- block helpers
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+__device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t t = __shfl_xor_sync(kFull, v, o);
+    v = t > v ? t : v;
+  }
+  return v;
+}
+__device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t t = __shfl_xor_sync(kFull, v, o);
+    v = t < v ? t : v;
+  }
+  return v;
+}
+
+// Given a histogram hist[NB] (shared memory), find the bucket d* in LARGEST-first order such
+// that above(d*) < need <= above(d*) + hist[d*], where above(d) = sum of hist over buckets > d.
+// Requires 1 <= need <= sum(hist). Result in out[0] = d*, out[1] = above(d*). Block-wide;
+// every thread must call it. scratch: >= NT/32 words.
+template <int NT, int NB>
+__device__ __forceinline__ void find_bucket(const uint32_t* hist, uint32_t need, uint32_t* out,
+                                            uint32_t* scratch) {
+  constexpr int PER = (NB + NT - 1) / NT;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t local[PER];
+  uint32_t sum = 0;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const int pos = tid * PER + j;  // descending position
+    local[j] = pos < NB ? hist[NB - 1 - pos] : 0u;
+    sum += local[j];
+  }
+  // block exclusive scan of `sum`
+  uint32_t incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) scratch[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    constexpr int NW = NT / 32;
+    uint32_t w = lane < NW ? scratch[lane] : 0u;
+    uint32_t wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(kFull, wi, o);
+      if (lane >= o) wi += t;
+    }
+    if (lane < NW) scratch[lane] = wi - w;  // exclusive warp offsets
+  }
+  __syncthreads();
+  const uint32_t excl = scratch[warp] + incl - sum;
+  if (excl < need && need <= excl + sum) {
+    uint32_t cum = excl;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      if (cum + local[j] >= need) {
+        out[0] = NB - 1 - (tid * PER + j);
+        out[1] = cum;
+        break;
+      }
+      cum += local[j];
+    }
+  }
+  __syncthreads();
+}
+
+}  // namespace tkv

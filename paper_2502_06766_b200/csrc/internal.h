@@ -1,0 +1,128 @@
+// internal.h — kernel parameter blocks and launchers shared by the .cu translation units.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tkv {
+
+constexpr int kSamples = 4096;       // sampled rows per (b, kv head) for the threshold estimate
+constexpr int kSampleThreads = 256;  // sample kernel CTA
+constexpr int kScanWarps = 8;        // scan kernel CTA = 8 warps
+constexpr int kScanU = 2;            // 16-row tiles per warp per iteration
+constexpr int kScanRows = kScanWarps * 16 * kScanU;  // rows per CTA iteration
+constexpr int kScanFlushEvery = 4;                   // iterations between staging flushes
+constexpr int kScanStage = kScanRows * kScanFlushEvery;  // staged candidates per head
+constexpr int kSelectThreads = 1024;
+constexpr int kAttendThreads = 256;
+constexpr int kAttendChunk = 512;  // selected rows per gather CTA
+constexpr int kSortMax = 16384;    // sorted output supported up to this k
+
+struct SampleParams {
+  const __nv_bfloat16* q;
+  const __nv_bfloat16* kc;
+  int64_t cache_rows;
+  int B, Hq, Hkv, G, k;
+  const int32_t* n_ctx;
+  int no_filter;
+  uint32_t* samp;      // [B*Hq*kSamples]
+  uint32_t* thr;       // [B*Hq]
+  uint32_t* cand_cnt;  // [B*Hq] (reset here)
+  uint32_t* ticket;    // [B*Hkv]
+};
+
+struct ScanParams {
+  const __nv_bfloat16* q;
+  const __nv_bfloat16* kc;
+  int64_t cache_rows;
+  int B, Hq, Hkv, G;
+  int64_t max_ctx;
+  const int32_t* n_ctx;
+  uint32_t row_offset;
+  const uint32_t* thr;
+  uint64_t* cand;  // [B*Hq][cap]
+  int64_t cap;
+  uint32_t* cand_cnt;
+  const uint32_t* flag_fail;   // [B*Hq]
+  const uint32_t* group_fail;  // [B*Hkv]
+  int fallback;
+};
+
+enum SelectPass { kPassMain = 0, kPassFallback = 1, kPassMerge = 2 };
+
+struct SelectParams {
+  const uint64_t* src;     // candidates: src + bh*src_stride (main/fallback)
+  int64_t src_stride;      // merge: element i of head bh is
+  int64_t shard_stride;    //   src[(i / k) * shard_stride + bh * k + i % k]
+  const uint32_t* src_cnt;  // per-bh count (main/fallback); nullptr → src_fixed (merge)
+  int64_t src_fixed;
+  int B, Hq, Hkv, G, k;
+  const int32_t* n_ctx;  // kb = min(k, n_ctx[b]) (main/fallback); merge: min(k, #valid)
+  int32_t* idx;          // [B*Hq*k]
+  float* scores;         // [B*Hq*k]
+  float* meta_max;       // [B*Hq]
+  uint64_t* meta_kth;    // [B*Hq]
+  int32_t* meta_kb;      // [B*Hq]
+  uint32_t* flag_fail;
+  uint32_t* group_fail;
+  uint32_t* cand_cnt;
+  uint64_t* packed_out;  // optional [B*Hq*k] composites (shard candidates)
+  int pass;
+};
+
+struct SortParams {
+  int32_t* idx;
+  float* scores;
+  const int32_t* meta_kb;
+  int k;
+};
+
+struct AttendParams {
+  const __nv_bfloat16* q;
+  const __nv_bfloat16* kc;
+  const __nv_bfloat16* vc;
+  int64_t cache_rows;
+  int B, Hq, Hkv, G, k;
+  const int32_t* n_ctx;
+  const int32_t* n_win;
+  int64_t row_offset;
+  int pinned;
+  float scale;
+  int combine;
+  const int32_t* idx;
+  const float* scores;
+  const float* meta_max;
+  const uint64_t* meta_kth;
+  const int32_t* meta_kb;
+  float* part_l;  // [B*Hq*nchunks]
+  float* part_o;  // [B*Hq*nchunks*D]
+  uint32_t* ticket;
+  int nchunks;
+  int partial_only;  // 1: write (l, o) to partial_out; 0: finalize into out
+  float* partial_out;
+  const float* partial_in;  // finalize kernel input
+  float* out;
+};
+
+struct AppendParams {
+  int B, Hkv;
+  int64_t cache_rows;
+  __nv_bfloat16* kc;
+  __nv_bfloat16* vc;
+  const __nv_bfloat16* k_new;
+  const __nv_bfloat16* v_new;
+  const int32_t* base;  // nullable
+  int32_t* count;
+  int advance;
+};
+
+cudaError_t launch_sample(const SampleParams& p, cudaStream_t s);
+cudaError_t launch_scan(const ScanParams& p, cudaStream_t s);
+cudaError_t launch_select(const SelectParams& p, cudaStream_t s);
+cudaError_t launch_sort(const SortParams& p, int nbh, cudaStream_t s);
+cudaError_t launch_attend(const AttendParams& p, cudaStream_t s);
+cudaError_t launch_finalize(const AttendParams& p, cudaStream_t s);
+cudaError_t launch_append(const AppendParams& p, cudaStream_t s);
+
+}  // namespace tkv

@@ -1,0 +1,99 @@
+"""Decode-loop session over one layer's device-resident KV cache.
+
+`TopkDecoder` is the user-facing object for the paper's decode step on B200: it owns the
+layer's bf16 K/V cache in HBM (context rows [0, n_ctx) followed by the generation window,
+the reference's GenWindow, attention.py:76-104), the libtkv workspace, and pinned host
+staging buffers. `step(q, k_new, v_new)` mirrors one layer of `decode_step`
+(attention.py:203-230): append the token's k/v to the window (attention.py:210), then top-k
+attention for every q head. With host tensors it is the end-to-end path: q/k/v are copied
+host→device, results device→host, all stream-ordered without extra synchronisation.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import ops
+from .errors import InputError, ShapeError
+
+
+class TopkDecoder:
+    def __init__(self, k_cache: torch.Tensor, v_cache: torch.Tensor, n_ctx, k: int, *,
+                 n_win=0, scale: float | None = None, combine: str = "joint",
+                 pinned_prefix: int = 0, sorted: bool = False, max_ctx: int | None = None):
+        if k < 1:
+            raise InputError("k must be >= 1")
+        ops._check_cuda_bf16("k_cache", k_cache, 4)
+        ops._check_cuda_bf16("v_cache", v_cache, 4)
+        if v_cache.shape != k_cache.shape:
+            raise ShapeError("v_cache shape must equal k_cache shape")
+        self.k_cache, self.v_cache = k_cache, v_cache
+        self.B, self.Hkv, self.rows, d = k_cache.shape
+        self.device = k_cache.device
+        self.n_ctx = ops._as_counts("n_ctx", n_ctx, self.B, self.device)
+        self.n_win = ops._as_counts("n_win", n_win, self.B, self.device)
+        self.max_ctx = int(max_ctx if max_ctx is not None else self.rows)
+        self.k = k
+        self.kw = dict(scale=scale, combine=combine, pinned_prefix=pinned_prefix, sorted=sorted,
+                       max_ctx=self.max_ctx)
+        ops.combine_code(combine)
+        self.Hq = None
+        self._bufs = None
+        self.ws = None
+
+    def _ensure(self, Hq: int) -> None:
+        if self.Hq == Hq:
+            return
+        if Hq % self.Hkv:
+            raise ShapeError(f"Hq={Hq} is not a multiple of Hkv={self.Hkv}")
+        self.Hq = Hq
+        dev = self.device
+        prob = ops.make_problem(self.B, Hq, self.Hkv, self.rows, self.max_ctx, self.k,
+                                pinned_prefix=self.kw["pinned_prefix"], scale=self.kw["scale"],
+                                combine=self.kw["combine"], sorted=self.kw["sorted"])
+        self.ws = ops.Workspace(prob, dev)
+        D = ops.HEAD_DIM
+        self._bufs = dict(
+            q=torch.empty((self.B, Hq, D), dtype=torch.bfloat16, device=dev),
+            k_new=torch.empty((self.B, self.Hkv, D), dtype=torch.bfloat16, device=dev),
+            v_new=torch.empty((self.B, self.Hkv, D), dtype=torch.bfloat16, device=dev),
+            out=torch.empty((self.B, Hq, D), dtype=torch.float32, device=dev),
+            idx=torch.empty((self.B, Hq, self.k), dtype=torch.int32, device=dev),
+            scores=torch.empty((self.B, Hq, self.k), dtype=torch.float32, device=dev),
+            out_h=torch.empty((self.B, Hq, D), dtype=torch.float32, pin_memory=True),
+            idx_h=torch.empty((self.B, Hq, self.k), dtype=torch.int32, pin_memory=True),
+        )
+
+    def append(self, k_new: torch.Tensor, v_new: torch.Tensor) -> None:
+        """GenWindow.append (attention.py:94-100) on device: rows n_ctx + n_win, n_win += 1."""
+        if self._bufs is None:
+            raise InputError("call step() (or attend()) once before append-only use")
+        kd, vd = self._bufs["k_new"], self._bufs["v_new"]
+        kd.copy_(k_new, non_blocking=True)
+        vd.copy_(v_new, non_blocking=True)
+        ops.kv_append(self.k_cache, self.v_cache, kd, vd, self.n_win, base=self.n_ctx, advance=True)
+
+    def attend(self, q: torch.Tensor):
+        """Top-k attention of q [B, Hq, 128] over context + window. Device tensors out."""
+        self._ensure(q.shape[1])
+        b = self._bufs
+        qd = q if (q.is_cuda and q.dtype == torch.bfloat16 and q.is_contiguous()) else b["q"].copy_(q, non_blocking=True)
+        ops.topk_decode_attention(qd, self.k_cache, self.v_cache, self.n_ctx, self.k, n_win=self.n_win,
+                                  out=b["out"], idx=b["idx"], scores=b["scores"], workspace=self.ws,
+                                  **self.kw)
+        return b["out"], b["idx"], b["scores"]
+
+    def step(self, q: torch.Tensor, k_new: torch.Tensor | None = None, v_new: torch.Tensor | None = None):
+        """One decode step for this layer. Host inputs → host outputs (out f32, idx int32);
+        device inputs → device outputs."""
+        self._ensure(q.shape[1])
+        if k_new is not None:
+            self.append(k_new, v_new)
+        out, idx, _ = self.attend(q)
+        if q.is_cuda:
+            return out, idx
+        b = self._bufs
+        b["out_h"].copy_(out, non_blocking=True)
+        b["idx_h"].copy_(idx, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        return b["out_h"], b["idx_h"]

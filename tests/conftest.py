@@ -1,0 +1,34 @@
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+if str(ROOT) not in sys.path:
+    sys.path.insert(0, str(ROOT))
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) GPU")
+    config.addinivalue_line("markers", "slow: long-running")
+
+
+@pytest.fixture(scope="session")
+def cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test ran without a CUDA device")
+    from paper_2502_06766_b200 import _lib
+
+    _lib.load()
+    _lib.check(_lib.load().tkv_device_check())
+    return torch.device("cuda", 0)
+
+
+def bf16_normal(rng: np.random.Generator, shape) -> np.ndarray:
+    from oracle.oracle import to_bf16_f32
+
+    return to_bf16_f32(rng.standard_normal(shape, dtype=np.float32))
