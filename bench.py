@@ -140,34 +140,32 @@ def make_inputs(cfg, rows, seed, device, rank_lo=0, rank_hi=None):
 
 
 def cpu_baseline(cfg, seconds_budget=20.0, threads=None):
-    """Oracle port timed on the host: one KV group (4 q heads) of batch entry 0 at the
-    workload's N and k, scaled to a full layer-step (×Hq/4 heads, ×B)."""
+    """The reference algorithm's CPU port (oracle/tkv_oracle.c: strict left-to-right f64 scan,
+    _flat_topk selection, f64 joint softmax — test infrastructure, timed here as the baseline)
+    on the host cores, on a bounded sample: one KV group (Hq/Hkv = 4 q heads) of one batch
+    entry at the workload's N and k, scaled to a full layer-step (x Hkv groups x B)."""
     import numpy as np
 
     from oracle import oracle as O
 
     N, k, B = cfg["N"], cfg["k"], cfg["B"]
+    G = HQ // HKV
     rng = np.random.default_rng(1234)
-    keys = O.to_bf16_f32(rng.standard_normal((N, D), dtype=np.float32))
-    vals = O.to_bf16_f32(rng.standard_normal((N, D), dtype=np.float32))
-    qs = O.to_bf16_f32(rng.standard_normal((HQ // HKV, D), dtype=np.float32))
-    keys64 = keys.astype(np.float64)
+    K = O.to_bf16_f32(rng.standard_normal((1, 1, N, D), dtype=np.float32))
+    V = O.to_bf16_f32(rng.standard_normal((1, 1, N, D), dtype=np.float32))
+    q = O.to_bf16_f32(rng.standard_normal((1, G, D), dtype=np.float32))
+    t = threads or O.c_lib().tkv_oracle_max_threads()
     times = []
     t_end = time.perf_counter() + seconds_budget
     while not times or (time.perf_counter() < t_end and len(times) < 3):
         t0 = time.perf_counter()
-        for h in range(qs.shape[0]):
-            q64 = qs[h].astype(np.float64)
-            s = keys64 @ q64                                   # ann_kernels.py:40-47
-            _, ids = O.flat_topk_from_scores(s, k)             # ann.py:154-167
-            s_ctx = (keys64[ids] @ q64) / math.sqrt(D)         # attention.py:158-160
-            O.joint_attend(s_ctx, vals[ids].astype(np.float64), np.zeros(0), np.zeros((0, D)), "joint")
+        O.c_decode_layer(q, K, V, [N], k, threads=t)
         times.append(time.perf_counter() - t0)
-    per_group = min(times)
-    us = per_group * (HQ // (HQ // HKV)) * B * 1e6
-    return {"value": us, "unit": "us", "cores": threads or os.cpu_count(), "kind": "port",
-            "sample": f"1 KV group (4 q heads) of 1 batch entry at N={N}, k={k}, numpy/BLAS f64 oracle port "
-                      f"(oracle/oracle.py), best of {len(times)}, scaled x{HKV * B} to a layer-step"}
+    us = min(times) * HKV * B * 1e6
+    return {"value": round(us, 1), "unit": "us", "cores": t, "kind": "port",
+            "sample": f"1 KV group ({G} q heads) of 1 batch entry at N={N}, k={k}: oracle/tkv_oracle.c "
+                      f"(C port of ann_kernels.py:31-47, ann.py:154-167, attention.py:107-167), {t} OpenMP "
+                      f"threads, best of {len(times)}, scaled x{HKV * B} to one layer-step"}
 
 
 def run_reference(args, cfg):

@@ -191,3 +191,55 @@ def topk_by_composite(comp: np.ndarray, k: int) -> np.ndarray:
     comp = np.asarray(comp, dtype=np.uint64)
     order = np.argsort(comp)[::-1]
     return order[:k]
+
+
+# ------------------------------------------------------------------------------ C port (ctypes)
+_C = None
+
+
+def c_lib():
+    """oracle/build/libtkv_oracle.so (oracle/tkv_oracle.c, built by oracle/Makefile)."""
+    global _C
+    if _C is None:
+        import ctypes
+        from pathlib import Path
+
+        path = Path(__file__).resolve().parent / "build" / "libtkv_oracle.so"
+        if not path.exists():
+            import subprocess
+
+            subprocess.run(["make", "-C", str(path.parent.parent)], check=True, capture_output=True)
+        lib = ctypes.CDLL(str(path))
+        P = ctypes.c_void_p
+        lib.tkv_oracle_layer.argtypes = [P, P, P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64,
+                                         ctypes.c_int, P, P, ctypes.c_int64, ctypes.c_int, ctypes.c_int64,
+                                         ctypes.c_int, P, P, P]
+        lib.tkv_oracle_layer.restype = ctypes.c_int
+        lib.tkv_oracle_max_threads.restype = ctypes.c_int
+        _C = lib
+    return _C
+
+
+def c_decode_layer(q, k_cache, v_cache, n_ctx, k: int, n_win=None, combine: str = "joint",
+                   pinned_prefix: int = 0, threads: int | None = None):
+    """decode_layer() through the C port (strict left-to-right f64 scan, OpenMP)."""
+    import ctypes
+
+    lib = c_lib()
+    q = np.ascontiguousarray(q, dtype=np.float32)
+    kc = np.ascontiguousarray(k_cache, dtype=np.float32)
+    vc = np.ascontiguousarray(v_cache, dtype=np.float32)
+    B, Hq, d = q.shape
+    Hkv, rows = kc.shape[1], kc.shape[2]
+    nc = np.ascontiguousarray(n_ctx, dtype=np.int32)
+    nw = np.ascontiguousarray(n_win if n_win is not None else np.zeros(B), dtype=np.int32)
+    stride = k + max(0, pinned_prefix)
+    out = np.zeros((B, Hq, d), dtype=np.float32)
+    ids = np.zeros((B * Hq, stride), dtype=np.int64)
+    cnt = np.zeros(B * Hq, dtype=np.int64)
+    t = threads if threads is not None else lib.tkv_oracle_max_threads()
+    vp = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
+    lib.tkv_oracle_layer(vp(q), vp(kc), vp(vc), B, Hq, Hkv, rows, d, vp(nc), vp(nw), k,
+                         0 if combine == "joint" else 1, pinned_prefix, t, vp(out), vp(ids), vp(cnt))
+    ids_all = [[ids[b * Hq + h, : cnt[b * Hq + h]].copy() for h in range(Hq)] for b in range(B)]
+    return out, ids_all

@@ -42,8 +42,8 @@ int fail(int code, const char* fmt, ...) {
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct Layout {
-  size_t ticket_s, ticket_g, flag, gflag, ctrl_end;
-  size_t cnt, thr, mmax, mkth, mkb, samp, cand, sidx, sscore, pl, po, total;
+  size_t ticket_g, flag, gflag, ctrl_end;
+  size_t cnt, thr, hshift, hist, mmax, mkth, mkb, samp, cand, sidx, sscore, pl, po, total;
   int64_t cap;
   int nchunks;
 };
@@ -58,13 +58,14 @@ Layout make_layout(const tkv_problem* p) {
     off = align_up(off + (bytes ? bytes : 1), 256);
     return o;
   };
-  L.ticket_s = take(BK * 4);
   L.ticket_g = take(BH * 4);
   L.flag = take(BH * 4);
   L.gflag = take(BK * 4);
   L.ctrl_end = off;
   L.cnt = take(BH * 4);
   L.thr = take(BH * 4);
+  L.hshift = take(BH * 4);
+  L.hist = take(BH * kHistBins * 4);
   L.mmax = take(BH * 4);
   L.mkth = take(BH * 8);
   L.mkb = take(BH * 4);
@@ -134,11 +135,23 @@ T* at(void* ws, size_t off) {
     if (r__ != TKV_OK) return r__; \
   } while (0)
 
-// sample → scan → select (+ fallback scan/select) [→ sort]; results in idx/scores
+HeadState head_state(void* ws, const Layout& L) {
+  HeadState hs{};
+  hs.thr = at<uint32_t>(ws, L.thr);
+  hs.hshift = at<uint32_t>(ws, L.hshift);
+  hs.cand_cnt = at<uint32_t>(ws, L.cnt);
+  hs.hist = at<uint32_t>(ws, L.hist);
+  hs.flag_fail = at<uint32_t>(ws, L.flag);
+  hs.group_fail = at<uint32_t>(ws, L.gflag);
+  return hs;
+}
+
+// sample → threshold → scan → select (+ fallback scan/select) [→ sort]; results in idx/scores
 int run_select(const tkv_problem* p, const void* q, const void* k_cache, const int32_t* n_ctx,
                int32_t* idx, float* scores, void* ws, const Layout& L, cudaStream_t st,
                uint64_t* packed_out) {
   const int G = p->n_q_heads / p->n_kv_heads;
+  const HeadState hs = head_state(ws, L);
   SampleParams sp{};
   sp.q = static_cast<const __nv_bfloat16*>(q);
   sp.kc = static_cast<const __nv_bfloat16*>(k_cache);
@@ -151,10 +164,9 @@ int run_select(const tkv_problem* p, const void* q, const void* k_cache, const i
   sp.n_ctx = n_ctx;
   sp.no_filter = (p->flags & TKV_F_NO_FILTER) ? 1 : 0;
   sp.samp = at<uint32_t>(ws, L.samp);
-  sp.thr = at<uint32_t>(ws, L.thr);
-  sp.cand_cnt = at<uint32_t>(ws, L.cnt);
-  sp.ticket = at<uint32_t>(ws, L.ticket_s);
+  sp.hs = hs;
   TKV_LAUNCH(launch_sample(sp, st));
+  if (!sp.no_filter) ++g_launches;  // sample + threshold kernels
 
   ScanParams cp{};
   cp.q = sp.q;
@@ -167,12 +179,9 @@ int run_select(const tkv_problem* p, const void* q, const void* k_cache, const i
   cp.max_ctx = p->max_ctx;
   cp.n_ctx = n_ctx;
   cp.row_offset = static_cast<uint32_t>(p->row_offset);
-  cp.thr = sp.thr;
   cp.cand = at<uint64_t>(ws, L.cand);
   cp.cap = L.cap;
-  cp.cand_cnt = sp.cand_cnt;
-  cp.flag_fail = at<uint32_t>(ws, L.flag);
-  cp.group_fail = at<uint32_t>(ws, L.gflag);
+  cp.hs = hs;
   cp.fallback = 0;
   if (g_scan_start && g_scan_stop) cudaEventRecord(g_scan_start, st);
   TKV_LAUNCH(launch_scan(cp, st));
@@ -181,7 +190,6 @@ int run_select(const tkv_problem* p, const void* q, const void* k_cache, const i
   SelectParams sl{};
   sl.src = cp.cand;
   sl.src_stride = L.cap;
-  sl.src_cnt = cp.cand_cnt;
   sl.B = p->batch;
   sl.Hq = p->n_q_heads;
   sl.Hkv = p->n_kv_heads;
@@ -193,9 +201,7 @@ int run_select(const tkv_problem* p, const void* q, const void* k_cache, const i
   sl.meta_max = at<float>(ws, L.mmax);
   sl.meta_kth = at<uint64_t>(ws, L.mkth);
   sl.meta_kb = at<int32_t>(ws, L.mkb);
-  sl.flag_fail = at<uint32_t>(ws, L.flag);
-  sl.group_fail = at<uint32_t>(ws, L.gflag);
-  sl.cand_cnt = cp.cand_cnt;
+  sl.hs = hs;
   sl.packed_out = packed_out;
   sl.pass = kPassMain;
   TKV_LAUNCH(launch_select(sl, st));
@@ -388,7 +394,6 @@ int tkv_shard_merge(const tkv_problem* p, const uint64_t* gathered, int32_t n_sh
   sl.src = gathered;
   sl.src_stride = static_cast<int64_t>(n_shards) * p->k;
   sl.shard_stride = static_cast<int64_t>(p->batch) * p->n_q_heads * p->k;
-  sl.src_cnt = nullptr;
   sl.src_fixed = static_cast<int64_t>(n_shards) * p->k;
   sl.B = p->batch;
   sl.Hq = p->n_q_heads;
@@ -401,9 +406,7 @@ int tkv_shard_merge(const tkv_problem* p, const uint64_t* gathered, int32_t n_sh
   sl.meta_max = at<float>(ws, L.mmax);
   sl.meta_kth = at<uint64_t>(ws, L.mkth);
   sl.meta_kb = at<int32_t>(ws, L.mkb);
-  sl.flag_fail = at<uint32_t>(ws, L.flag);
-  sl.group_fail = at<uint32_t>(ws, L.gflag);
-  sl.cand_cnt = at<uint32_t>(ws, L.cnt);
+  sl.hs = head_state(ws, L);
   sl.packed_out = nullptr;
   sl.pass = kPassMerge;
   cudaStream_t st = static_cast<cudaStream_t>(stream);

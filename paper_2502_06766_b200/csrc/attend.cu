@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(NT) attend_kernel(AttendParams p) {
   float acc[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) acc[j] = 0.f;
-  constexpr int UNR = 4;
+  constexpr int UNR = 8;
   for (int r0 = warp * 2 + half; r0 < nrows; r0 += 2 * NW * UNR) {
     uint4 v[UNR];
     float w[UNR];

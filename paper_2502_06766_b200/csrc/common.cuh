@@ -132,6 +132,24 @@ __device__ __forceinline__ void score_tile(float (&acc)[4], const uint4 (&a)[2][
   }
 }
 
+// ---------------------------------------------------------------- candidate histogram
+// Emitted candidates have key >= thr; their histogram bucket is the key offset above the
+// threshold at a per-head granularity `shift` (chosen from the sampled score range so the
+// candidates spread over the buckets instead of piling into a few top-bit buckets),
+// clamped into the top bucket.
+constexpr int kHistBins = 4096;
+__device__ __forceinline__ uint32_t hist_digit(uint32_t key, uint32_t thr, uint32_t shift) {
+  const uint32_t d = (key - thr) >> shift;
+  return d < static_cast<uint32_t>(kHistBins - 1) ? d : static_cast<uint32_t>(kHistBins - 1);
+}
+
+// Warp-aggregated shared-memory histogram increment: lanes with equal digits combine into one
+// atomic (score keys are concentrated, so per-lane atomics would serialise on a few bins).
+__device__ __forceinline__ void hist_add_aggregated(uint32_t* hist, uint32_t digit) {
+  const unsigned peers = __match_any_sync(__activemask(), digit);
+  if ((threadIdx.x & 31) == static_cast<unsigned>(__ffs(peers) - 1)) atomicAdd(&hist[digit], __popc(peers));
+}
+
 // ---------------------------------------------------------------- block helpers
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {

@@ -8,16 +8,29 @@
 namespace tkv {
 
 constexpr int kSamples = 4096;       // sampled rows per (b, kv head) for the threshold estimate
-constexpr int kSampleThreads = 256;  // sample kernel CTA
+constexpr int kSampleThreads = 256;  // sample-scoring CTA
+constexpr int kThrThreads = 1024;    // threshold CTA (one per (b, q head))
 constexpr int kScanWarps = 8;        // scan kernel CTA = 8 warps
 constexpr int kScanU = 2;            // 16-row tiles per warp per iteration
 constexpr int kScanRows = kScanWarps * 16 * kScanU;  // rows per CTA iteration
 constexpr int kScanFlushEvery = 4;                   // iterations between staging flushes
 constexpr int kScanStage = kScanRows * kScanFlushEvery;  // staged candidates per head
 constexpr int kSelectThreads = 1024;
+constexpr int kSelectBucketCap = 8192;  // threshold-bucket candidates refined in shared memory
 constexpr int kAttendThreads = 256;
 constexpr int kAttendChunk = 512;  // selected rows per gather CTA
 constexpr int kSortMax = 16384;    // sorted output supported up to this k
+constexpr uint32_t kNoFilterShift = 20;  // histogram shift when every score is a candidate
+
+// per-(b, q head) state shared by the kernels of one call, in the workspace
+struct HeadState {
+  uint32_t* thr;         // [B*Hq] candidate threshold key (0 = emit all)
+  uint32_t* hshift;      // [B*Hq] histogram granularity
+  uint32_t* cand_cnt;    // [B*Hq]
+  uint32_t* hist;        // [B*Hq][kHistBins] histogram of the emitted candidates
+  uint32_t* flag_fail;   // [B*Hq] sampled threshold too high → re-scan with thr = 0
+  uint32_t* group_fail;  // [B*Hkv]
+};
 
 struct SampleParams {
   const __nv_bfloat16* q;
@@ -26,10 +39,8 @@ struct SampleParams {
   int B, Hq, Hkv, G, k;
   const int32_t* n_ctx;
   int no_filter;
-  uint32_t* samp;      // [B*Hq*kSamples]
-  uint32_t* thr;       // [B*Hq]
-  uint32_t* cand_cnt;  // [B*Hq] (reset here)
-  uint32_t* ticket;    // [B*Hkv]
+  uint32_t* samp;  // [B*Hq*kSamples]
+  HeadState hs;
 };
 
 struct ScanParams {
@@ -40,23 +51,19 @@ struct ScanParams {
   int64_t max_ctx;
   const int32_t* n_ctx;
   uint32_t row_offset;
-  const uint32_t* thr;
   uint64_t* cand;  // [B*Hq][cap]
   int64_t cap;
-  uint32_t* cand_cnt;
-  const uint32_t* flag_fail;   // [B*Hq]
-  const uint32_t* group_fail;  // [B*Hkv]
+  HeadState hs;
   int fallback;
 };
 
 enum SelectPass { kPassMain = 0, kPassFallback = 1, kPassMerge = 2 };
 
 struct SelectParams {
-  const uint64_t* src;     // candidates: src + bh*src_stride (main/fallback)
-  int64_t src_stride;      // merge: element i of head bh is
-  int64_t shard_stride;    //   src[(i / k) * shard_stride + bh * k + i % k]
-  const uint32_t* src_cnt;  // per-bh count (main/fallback); nullptr → src_fixed (merge)
-  int64_t src_fixed;
+  const uint64_t* src;   // candidates: src + bh*src_stride (main/fallback)
+  int64_t src_stride;    // merge: element i of head bh is
+  int64_t shard_stride;  //   src[(i / k) * shard_stride + bh * k + i % k]
+  int64_t src_fixed;     // merge: candidates per head (n_shards * k)
   int B, Hq, Hkv, G, k;
   const int32_t* n_ctx;  // kb = min(k, n_ctx[b]) (main/fallback); merge: min(k, #valid)
   int32_t* idx;          // [B*Hq*k]
@@ -64,9 +71,7 @@ struct SelectParams {
   float* meta_max;       // [B*Hq]
   uint64_t* meta_kth;    // [B*Hq]
   int32_t* meta_kb;      // [B*Hq]
-  uint32_t* flag_fail;
-  uint32_t* group_fail;
-  uint32_t* cand_cnt;
+  HeadState hs;
   uint64_t* packed_out;  // optional [B*Hq*k] composites (shard candidates)
   int pass;
 };

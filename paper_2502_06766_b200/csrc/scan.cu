@@ -6,15 +6,16 @@
 // shared by the group) and, instead of materialising all N scores, emits only the rows
 // whose score can still be in the top-k:
 //
-//   sample_kernel : scores a strided sample of S = 4096 rows per (b, kv head) and, in the
-//                   last CTA of each group, picks per q head a threshold key t_h = the r-th
-//                   largest sampled key with r = ceil(mu + 6 sqrt(mu) + 16), mu = k·S_b/N_b
-//                   (expected ≈1.5–2·k survivors). t_h = 0 (emit all) when that would not
-//                   filter. It also resets the per-head candidate counters.
-//   scan_kernel   : persistent CTAs stream contiguous row ranges; each warp scores 16-row
-//                   tiles on the tensor cores (HMMA, see common.cuh) and appends the
-//                   composite (key, ~row) of every score with key >= t_h to a per-head
-//                   staging buffer in shared memory, flushed to HBM in bulk.
+//   sample_kernel    : scores a strided sample of S = 4096 rows per (b, kv head).
+//   threshold_kernel : per (b, q head), the threshold key t_h = the r-th largest sampled key,
+//                      r = ceil(mu + 6 sqrt(mu) + 16), mu = k·S_b/N_b (≈1.5–2·k survivors
+//                      expected; t_h = 0 = emit all when that would not filter), and the
+//                      histogram granularity for the candidates' keys; resets the counters.
+//   scan_kernel      : persistent CTAs stream contiguous row ranges; each warp scores
+//                      16-row tiles on the tensor cores (HMMA, see common.cuh) and appends the
+//                      composite (key, ~row) of every score with key >= t_h to a per-head
+//                      staging buffer in shared memory, flushed to HBM in bulk together with
+//                      the candidates' 4096-bucket key histogram (consumed by select.cu).
 //
 // Exactness does not depend on the sample: the selection kernel checks that at least k
 // candidates survived (then the true top-k ⊆ candidates, since every top-k key >= the k-th
@@ -26,97 +27,113 @@
 
 namespace tkv {
 
-// r-th largest (1-indexed) of n u32 keys held in shared memory; 8-bit radix, 4 passes.
-template <int NT>
-__device__ uint32_t block_kth_largest_u32(const uint32_t* keys, int n, uint32_t r, uint32_t* hist,
-                                          uint32_t* scr, uint32_t* out) {
-  uint32_t prefix = 0, need = r;
-  for (int shift = 24; shift >= 0; shift -= 8) {
-    for (int i = threadIdx.x; i < 256; i += NT) hist[i] = 0u;
-    __syncthreads();
-    for (int i = threadIdx.x; i < n; i += NT) {
-      const uint32_t k = keys[i];
-      if (shift == 24 || (k >> (shift + 8)) == prefix) atomicAdd(&hist[(k >> shift) & 255u], 1u);
-    }
-    __syncthreads();
-    find_bucket<NT, 256>(hist, need, out, scr);
-    need -= out[1];
-    prefix = (prefix << 8) | out[0];
-    __syncthreads();
-  }
-  return prefix;
-}
-
 __global__ void __launch_bounds__(kSampleThreads) sample_kernel(SampleParams p) {
-  __shared__ uint32_t s_keys[kSamples];
-  __shared__ uint32_t s_hist[256];
-  __shared__ uint32_t s_scr[32];
-  __shared__ uint32_t s_out[2];
-  __shared__ int s_last;
-
   const int seg = blockIdx.y;
   const int b = seg / p.Hkv, kvh = seg % p.Hkv;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, c = lane & 3;
   const int64_t N = p.n_ctx[b];
+  if (N <= 0) return;
+  const int64_t stride = (N + kSamples - 1) / kSamples;
+  const int Sb = static_cast<int>((N + stride - 1) / stride);
+  QFrag f;
+  load_qfrag(f, p.q + (static_cast<int64_t>(b) * p.Hq + kvh * p.G) * kD, p.G, lane);
+  const __nv_bfloat16* kbase = p.kc + (static_cast<int64_t>(b) * p.Hkv + kvh) * p.cache_rows * kD;
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int s0 = blockIdx.x * kSampleThreads + warp * 32 + u * 16;
+    const int sA = s0 + g, sB = s0 + g + 8;
+    uint4 a[2][4];
+    load_tile(a, kbase + static_cast<int64_t>(sA) * stride * kD, sA < Sb,
+              kbase + static_cast<int64_t>(sB) * stride * kD, sB < Sb, c);
+    float acc[4];
+    score_tile(acc, a, f);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int col = 2 * c + (i & 1);
+      const int s = (i < 2) ? sA : sB;
+      if (col < p.G && s < Sb)
+        p.samp[(static_cast<int64_t>(b) * p.Hq + kvh * p.G + col) * kSamples + s] = score_key(acc[i]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThrThreads) threshold_kernel(SampleParams p) {
+  constexpr int NT = kThrThreads;
+  __shared__ uint32_t s_keys[kSamples];
+  __shared__ uint32_t s_hist[2048];
+  __shared__ uint32_t s_scr[32];
+  __shared__ uint32_t s_out[2];
+  __shared__ uint32_t s_max[32];
+  const int bh = blockIdx.x;
+  const int b = bh / p.Hq;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t N = p.n_ctx[b];
   const int64_t kb = N < p.k ? N : p.k;
-  int64_t stride = 1;
   int Sb = 0;
   if (N > 0) {
-    stride = (N + kSamples - 1) / kSamples;
+    const int64_t stride = (N + kSamples - 1) / kSamples;
     Sb = static_cast<int>((N + stride - 1) / stride);
   }
-  const bool filter = !p.no_filter && N > 0;
-
-  if (filter) {
-    QFrag f;
-    load_qfrag(f, p.q + (static_cast<int64_t>(b) * p.Hq + kvh * p.G) * kD, p.G, lane);
-    const __nv_bfloat16* kbase = p.kc + (static_cast<int64_t>(b) * p.Hkv + kvh) * p.cache_rows * kD;
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int s0 = blockIdx.x * (kSampleThreads / 32) * 32 + warp * 32 + u * 16;
-      const int sA = s0 + g, sB = s0 + g + 8;
-      uint4 a[2][4];
-      load_tile(a, kbase + static_cast<int64_t>(sA) * stride * kD, sA < Sb,
-                kbase + static_cast<int64_t>(sB) * stride * kD, sB < Sb, c);
-      float acc[4];
-      score_tile(acc, a, f);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int col = 2 * c + (i & 1);
-        const int s = (i < 2) ? sA : sB;
-        if (col < p.G && s < kSamples) {
-          const int64_t bh = static_cast<int64_t>(b) * p.Hq + kvh * p.G + col;
-          p.samp[bh * kSamples + s] = (s < Sb) ? score_key(acc[i]) : 0u;
-        }
-      }
-    }
-  }
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) s_last = (atomicAdd(&p.ticket[seg], 1u) == gridDim.x - 1);
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-
   const double mu = N > 0 ? static_cast<double>(kb) * Sb / static_cast<double>(N) : 0.0;
   const double rr = ceil(mu + 6.0 * sqrt(mu) + 16.0);
-  for (int n = 0; n < p.G; ++n) {
-    const int64_t bh = static_cast<int64_t>(b) * p.Hq + kvh * p.G + n;
-    uint32_t t = 0u;
-    if (filter && kb > 0 && rr < static_cast<double>(Sb)) {
-      for (int i = tid; i < Sb; i += kSampleThreads) s_keys[i] = __ldcg(&p.samp[bh * kSamples + i]);
-      __syncthreads();
-      t = block_kth_largest_u32<kSampleThreads>(s_keys, Sb, static_cast<uint32_t>(rr), s_hist,
-                                                s_scr, s_out);
+  const bool filter = !p.no_filter && kb > 0 && rr < static_cast<double>(Sb);
+
+  uint32_t thr = 0u, shift = kNoFilterShift;
+  if (filter) {
+    uint32_t mx = 0u;
+    for (int i = tid; i < Sb; i += NT) {
+      const uint32_t k = p.samp[static_cast<int64_t>(bh) * kSamples + i];
+      s_keys[i] = k;
+      mx = k > mx ? k : mx;
     }
-    if (tid == 0) {
-      p.thr[bh] = t;
-      p.cand_cnt[bh] = 0u;
-    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(kFull, mx, o));
+    if (lane == 0) s_max[warp] = mx;
     __syncthreads();
+    // r-th largest sampled key: MSB-first radix select (11/11/10-bit digits) in shared memory.
+    // Stopping early when the digit's bucket is taken whole leaves the bucket's lower bound,
+    // which is <= the r-th key (a threshold only has to be a lower bound).
+    uint32_t prefix = 0, need = static_cast<uint32_t>(rr);
+    int sh = 32;
+    for (int pi = 0; pi < 3; ++pi) {
+      const int w = pi < 2 ? 11 : 10;
+      const int nsh = sh - w;
+      const uint32_t mask = (1u << w) - 1u;
+      for (int i = tid; i <= static_cast<int>(mask); i += NT) s_hist[i] = 0u;
+      __syncthreads();
+      for (int i = tid; i < Sb; i += NT) {
+        const uint32_t k = s_keys[i];
+        if (sh == 32 || (k >> sh) == prefix) hist_add_aggregated(s_hist, (k >> nsh) & mask);
+      }
+      __syncthreads();
+      if (w == 11)
+        find_bucket<NT, 2048>(s_hist, need, s_out, s_scr);
+      else
+        find_bucket<NT, 1024>(s_hist, need, s_out, s_scr);
+      need -= s_out[1];
+      prefix = (prefix << w) | s_out[0];
+      sh = nsh;
+      const bool done = s_hist[s_out[0]] == need;
+      __syncthreads();
+      if (done) break;
+    }
+    thr = sh > 0 ? prefix << sh : prefix;
+    uint32_t smax = 0u;
+    for (int w = 0; w < NT / 32; ++w) smax = max(smax, s_max[w]);
+    // histogram granularity: the sampled range [thr, smax] spans ~1/4 of the 4096 buckets,
+    // leaving headroom for the (unsampled) true maximum; the top bucket absorbs the rest
+    const uint32_t range = smax - thr;
+    const int bits = range ? 32 - __clz(range) : 0;
+    shift = bits > 10 ? static_cast<uint32_t>(bits - 10) : 0u;
   }
-  if (tid == 0) p.ticket[seg] = 0u;
+  uint32_t* gh = p.hs.hist + static_cast<int64_t>(bh) * kHistBins;
+  for (int i = tid; i < kHistBins; i += NT) gh[i] = 0u;
+  if (tid == 0) {
+    p.hs.thr[bh] = thr;
+    p.hs.hshift[bh] = shift;
+    p.hs.cand_cnt[bh] = 0u;
+  }
 }
 
 // ------------------------------------------------------------------------------ scan
@@ -136,11 +153,19 @@ __device__ __forceinline__ void scan_flush(const ScanParams& p, const ScanState&
     if (cnt) {
       const int64_t bh = static_cast<int64_t>(st.b) * p.Hq + st.kvh * p.G + warp;
       uint32_t base = 0;
-      if (lane == 0) base = atomicAdd(&p.cand_cnt[bh], cnt);
+      if (lane == 0) base = atomicAdd(&p.hs.cand_cnt[bh], cnt);
       base = __shfl_sync(kFull, base, 0);
+      const uint32_t thr = p.hs.thr[bh], shift = p.hs.hshift[bh];
+      uint32_t* gh = p.hs.hist + bh * kHistBins;
       uint64_t* dst = p.cand + bh * p.cap + base;
       const uint64_t* src = s_buf + warp * kScanStage;
-      for (uint32_t i = lane; i < cnt; i += 32) dst[i] = src[i];
+      for (uint32_t i = lane; i < cnt; i += 32) {
+        const uint64_t cc = src[i];
+        dst[i] = cc;
+        const uint32_t d = hist_digit(comp_key(cc), thr, shift);
+        const unsigned peers = __match_any_sync(__activemask(), d);
+        if (lane == static_cast<int>(__ffs(peers) - 1)) atomicAdd(&gh[d], __popc(peers));
+      }
     }
     if (lane == 0) s_cnt[warp] = 0u;
   }
@@ -177,7 +202,7 @@ __global__ void __launch_bounds__(kScanWarps * 32, 2) scan_kernel(ScanParams p) 
       st.b = static_cast<int>(seg / p.Hkv);
       st.kvh = static_cast<int>(seg % p.Hkv);
       st.nctx = p.n_ctx[st.b];
-      st.active = !p.fallback || p.group_fail[seg] != 0u;
+      st.active = !p.fallback || p.hs.group_fail[seg] != 0u;
       if (!st.active) {
         t = (seg + 1) * tps - 1;  // skip the rest of this segment (CTA-uniform)
         continue;
@@ -185,10 +210,10 @@ __global__ void __launch_bounds__(kScanWarps * 32, 2) scan_kernel(ScanParams p) 
       load_qfrag(f, p.q + (static_cast<int64_t>(st.b) * p.Hq + st.kvh * p.G) * kD, p.G, lane);
       kbase = p.kc + (static_cast<int64_t>(st.b) * p.Hkv + st.kvh) * p.cache_rows * kD;
       const int64_t bh0 = static_cast<int64_t>(st.b) * p.Hq + st.kvh * p.G;
-      en0 = col0 < p.G && (!p.fallback || p.flag_fail[bh0 + col0] != 0u);
-      en1 = col1 < p.G && (!p.fallback || p.flag_fail[bh0 + col1] != 0u);
-      thr0 = (col0 < p.G && !p.fallback) ? p.thr[bh0 + col0] : 0u;
-      thr1 = (col1 < p.G && !p.fallback) ? p.thr[bh0 + col1] : 0u;
+      en0 = col0 < p.G && (!p.fallback || p.hs.flag_fail[bh0 + col0] != 0u);
+      en1 = col1 < p.G && (!p.fallback || p.hs.flag_fail[bh0 + col1] != 0u);
+      thr0 = col0 < p.G ? p.hs.thr[bh0 + col0] : 0u;
+      thr1 = col1 < p.G ? p.hs.thr[bh0 + col1] : 0u;
     }
     const int64_t tile = t - seg * tps;
     const int64_t rbase = tile * kScanRows + warp * 16 * kScanU;
@@ -233,8 +258,13 @@ __global__ void __launch_bounds__(kScanWarps * 32, 2) scan_kernel(ScanParams p) 
 }
 
 cudaError_t launch_sample(const SampleParams& p, cudaStream_t s) {
-  dim3 grid(p.no_filter ? 1 : kSamples / kSampleThreads, p.B * p.Hkv);
-  sample_kernel<<<grid, kSampleThreads, 0, s>>>(p);
+  if (!p.no_filter) {
+    dim3 grid(kSamples / kSampleThreads, p.B * p.Hkv);
+    sample_kernel<<<grid, kSampleThreads, 0, s>>>(p);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  threshold_kernel<<<p.B * p.Hq, kThrThreads, 0, s>>>(p);
   return cudaGetLastError();
 }
 

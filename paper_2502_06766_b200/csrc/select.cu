@@ -1,16 +1,24 @@
 // select.cu — K2: exact top-k over the emitted candidates, one CTA per (b, q head).
 //
 // Reference: _flat_topk (ann.py:154-167): argpartition, then every score strictly above the
-// k-th score plus the LOWEST-id rows tied with it, ordered score-desc / id-asc. Here the
-// candidates are 64-bit composites (score key << 32 | ~row id, common.cuh), unique per row, so
-// the reference's "above + lowest-id ties" set is exactly the k largest composites. It is found
-// with an MSB-first radix select (digit widths 12/10/10 over the score key, then 8-bit digits
-// over the row id, used only while ties remain), each pass a shared-memory histogram over the
-// candidates still matching the prefix, ending as soon as a bucket is taken whole.
+// k-th score plus the LOWEST-id rows tied with it, ordered score-desc / id-asc. Here every
+// candidate is a 64-bit composite (score key << 32 | ~row id, common.cuh), unique per row, so
+// the reference's "above + lowest-id ties" set is exactly the k largest composites.
 //
-// Passes: main (candidates from the sampled-threshold scan; fails → flags the head for the
-// fallback re-scan when fewer than k survived), fallback (re-scanned heads only), merge
-// (sharded: candidates gathered from every shard, empty slots = 0).
+// One pass over the candidates (typical case):
+//   1. the 4096-bucket histogram of the candidates' keys (offset above the threshold, see
+//      hist_digit) is already built by the scan kernel → the bucket d* holding the k-th
+//      largest is found with one block-wide scan;
+//   2. a single compaction pass writes every candidate of a bucket above d* straight to the
+//      output and gathers the few candidates of bucket d* into shared memory;
+//   3. an MSB-first radix select over the 64-bit composites of that bucket (shared memory,
+//      8-bit digits, warp-aggregated histogram atomics) picks the remaining `need` rows,
+//      which resolves score ties to the lower row id exactly.
+// Buckets larger than shared memory fall back to radix passes over global memory.
+//
+// Passes: main (fails → flags the head for the exact re-scan when fewer than k candidates
+// survived the sampled threshold), fallback (re-scanned heads only), merge (sharded:
+// candidates gathered from every shard; histogram built here from the candidates' range).
 #include <math.h>
 
 #include "common.cuh"
@@ -20,37 +28,90 @@ namespace tkv {
 
 namespace {
 constexpr int NT = kSelectThreads;
-__device__ __forceinline__ int digit_width(int pi) { return pi == 0 ? 12 : (pi < 3 ? 10 : 8); }
+constexpr int NWARP = NT / 32;
 
-__device__ __forceinline__ void find_bucket_w(int w, const uint32_t* hist, uint32_t need,
-                                              uint32_t* out, uint32_t* scr) {
-  if (w == 12)
-    find_bucket<NT, 4096>(hist, need, out, scr);
-  else if (w == 10)
-    find_bucket<NT, 1024>(hist, need, out, scr);
-  else
+// Radix select of the `need` largest composites among the elements accepted by `load`
+// (load(i, c) -> bool), MSB first with 8-bit digits. Result: selected ⇔ (c >> shift) >= prefix.
+template <typename Load>
+__device__ void radix_select_u64(Load load, int64_t n, uint32_t need, uint32_t* hist, uint32_t* scr,
+                                 uint32_t* out, int& shift_out, uint64_t& prefix_out) {
+  int shift = 64;
+  uint64_t prefix = 0;
+  while (shift > 0) {
+    const int nshift = shift - 8;
+    for (int i = threadIdx.x; i < 256; i += NT) hist[i] = 0u;
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < n; i += NT) {
+      uint64_t c;
+      if (load(i, c) && (shift == 64 || (c >> shift) == prefix))
+        hist_add_aggregated(hist, static_cast<uint32_t>(c >> nshift) & 255u);
+    }
+    __syncthreads();
     find_bucket<NT, 256>(hist, need, out, scr);
+    const uint32_t d = out[0];
+    need -= out[1];
+    prefix = (prefix << 8) | d;
+    shift = nshift;
+    const bool done = hist[d] == need;
+    __syncthreads();
+    if (done) break;
+  }
+  shift_out = shift;
+  prefix_out = prefix;
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+struct Emit {
+  int32_t* idx;
+  float* sc;
+  uint64_t* pk;
+  uint32_t kb;
+  __device__ __forceinline__ void put(uint32_t pos, uint64_t c) const {
+    if (pos < kb) {
+      idx[pos] = static_cast<int32_t>(comp_gid(c));
+      sc[pos] = key_score(comp_key(c));
+      if (pk) pk[pos] = c;
+    }
+  }
+};
+
+// Warp-aggregated append of the lanes with `sel` set to the output (order unspecified).
+__device__ __forceinline__ void emit_sel(bool sel, uint64_t c, uint32_t* counter, const Emit& e,
+                                         uint64_t& vmin) {
+  const unsigned bs = __ballot_sync(kFull, sel);
+  uint32_t base = 0;
+  if ((threadIdx.x & 31) == 0 && bs) base = atomicAdd(counter, __popc(bs));
+  base = __shfl_sync(kFull, base, 0);
+  if (sel) {
+    e.put(base + __popc(bs & lanemask_lt()), c);
+    vmin = c < vmin ? c : vmin;
+  }
 }
 }  // namespace
 
 __global__ void __launch_bounds__(NT) select_kernel(SelectParams p) {
-  __shared__ uint32_t s_hist[4096];
+  extern __shared__ uint64_t s_bkt[];  // [kSelectBucketCap]
+  __shared__ uint32_t s_hist[kHistBins];
   __shared__ uint32_t s_scr[32];
   __shared__ uint32_t s_out[2];
-  __shared__ uint32_t s_wofs[32];
-  __shared__ uint32_t s_tot;
-  __shared__ uint32_t s_nvalid;
-  __shared__ uint64_t s_rmax[32], s_rmin[32];
+  __shared__ uint32_t s_nout, s_nbkt, s_nvalid;
+  __shared__ uint32_t s_kmin[NWARP], s_kmax[NWARP];
+  __shared__ uint64_t s_rmax[NWARP], s_rmin[NWARP];
 
   const int bh = blockIdx.x;
   const int b = bh / p.Hq, h = bh % p.Hq;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (p.pass == kPassFallback && p.flag_fail[bh] == 0u) return;
+  if (p.pass == kPassFallback && p.hs.flag_fail[bh] == 0u) return;
 
   const bool merge = p.pass == kPassMerge;
   const uint64_t* src = merge ? p.src + static_cast<int64_t>(bh) * p.k
                               : p.src + static_cast<int64_t>(bh) * p.src_stride;
-  int64_t n = p.src_cnt ? static_cast<int64_t>(p.src_cnt[bh]) : p.src_fixed;
+  int64_t n = merge ? p.src_fixed : static_cast<int64_t>(p.hs.cand_cnt[bh]);
   if (!merge && n > p.src_stride) n = p.src_stride;
   auto load = [&](int64_t i) -> uint64_t {
     if (!merge) return src[i];
@@ -58,118 +119,202 @@ __global__ void __launch_bounds__(NT) select_kernel(SelectParams p) {
     return src[s * p.shard_stride + (i - s * p.k)];
   };
 
-  // ---- pass 1: 12-bit histogram of the top digit + number of valid candidates
-  for (int i = tid; i < 4096; i += NT) s_hist[i] = 0u;
-  if (tid == 0) s_nvalid = 0u;
-  __syncthreads();
-  uint32_t nv = 0;
-  for (int64_t i = tid; i < n; i += NT) {
-    const uint64_t c = load(i);
-    if (c) {
-      ++nv;
-      atomicAdd(&s_hist[c >> 52], 1u);
+  // ---- histogram of the candidate keys: from the scan (main/fallback) or built here (merge)
+  uint32_t thr, shift;
+  int64_t nvalid;
+  if (!merge) {
+    thr = p.hs.thr[bh];
+    shift = p.hs.hshift[bh];
+    nvalid = n;
+    const uint32_t* gh = p.hs.hist + static_cast<int64_t>(bh) * kHistBins;
+    for (int i = tid; i < kHistBins; i += NT) s_hist[i] = __ldcg(&gh[i]);
+    __syncthreads();
+  } else {
+    uint32_t kmin = 0xffffffffu, kmax = 0u, nv = 0u;
+    constexpr int UNR = 8;
+    for (int64_t start = 0; start < n; start += NT * UNR) {
+      uint64_t cv[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int64_t i = start + u * NT + tid;
+        cv[u] = i < n ? load(i) : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        if (cv[u]) {
+          ++nv;
+          const uint32_t key = comp_key(cv[u]);
+          kmin = key < kmin ? key : kmin;
+          kmax = key > kmax ? key : kmax;
+        }
+      }
     }
+    nv = warp_sum(nv);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      kmin = min(kmin, __shfl_xor_sync(kFull, kmin, o));
+      kmax = max(kmax, __shfl_xor_sync(kFull, kmax, o));
+    }
+    if (lane == 0) {
+      s_kmin[warp] = kmin;
+      s_kmax[warp] = kmax;
+      s_scr[warp] = nv;
+    }
+    for (int i = tid; i < kHistBins; i += NT) s_hist[i] = 0u;
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t a = lane < NWARP ? s_kmin[lane] : 0xffffffffu;
+      uint32_t z = lane < NWARP ? s_kmax[lane] : 0u;
+      uint32_t v = lane < NWARP ? s_scr[lane] : 0u;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        a = min(a, __shfl_xor_sync(kFull, a, o));
+        z = max(z, __shfl_xor_sync(kFull, z, o));
+        v += __shfl_xor_sync(kFull, v, o);
+      }
+      if (lane == 0) {
+        s_out[0] = a;
+        s_out[1] = z;
+        s_nvalid = v;
+      }
+    }
+    __syncthreads();
+    thr = s_out[0];
+    const uint32_t range = s_out[1] - s_out[0];
+    const int bits = range ? 32 - __clz(range) : 0;
+    shift = bits > 12 ? static_cast<uint32_t>(bits - 12) : 0u;
+    nvalid = s_nvalid;
+    __syncthreads();
+    for (int64_t start = 0; start < n; start += NT * UNR) {
+      uint64_t cv[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int64_t i = start + u * NT + tid;
+        cv[u] = i < n ? load(i) : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u)
+        if (cv[u]) hist_add_aggregated(s_hist, hist_digit(comp_key(cv[u]), thr, shift));
+    }
+    __syncthreads();
   }
-  nv = warp_sum(nv);
-  if (lane == 0 && nv) atomicAdd(&s_nvalid, nv);
-  __syncthreads();
-  const int64_t nvalid = s_nvalid;
 
   int64_t kb;
-  if (p.pass == kPassMerge) {
+  if (merge) {
     kb = nvalid < p.k ? nvalid : p.k;
   } else {
     const int64_t N = p.n_ctx[b];
     kb = N < p.k ? N : p.k;
   }
-  int32_t* idx_out = p.idx + static_cast<int64_t>(bh) * p.k;
-  float* sc_out = p.scores + static_cast<int64_t>(bh) * p.k;
-  uint64_t* pk_out = p.packed_out ? p.packed_out + static_cast<int64_t>(bh) * p.k : nullptr;
+  const Emit em{p.idx + static_cast<int64_t>(bh) * p.k, p.scores + static_cast<int64_t>(bh) * p.k,
+                p.packed_out ? p.packed_out + static_cast<int64_t>(bh) * p.k : nullptr,
+                static_cast<uint32_t>(kb)};
 
   if (p.pass == kPassMain && nvalid < kb) {
-    // Sampled threshold was too high for this head: re-scan it with threshold 0.
+    // The sampled threshold let fewer than k rows through: re-scan this head with thr = 0.
+    uint32_t* gh = p.hs.hist + static_cast<int64_t>(bh) * kHistBins;
+    for (int i = tid; i < kHistBins; i += NT) gh[i] = 0u;
     if (tid == 0) {
-      p.flag_fail[bh] = 1u;
-      p.group_fail[b * p.Hkv + h / p.G] = 1u;
-      p.cand_cnt[bh] = 0u;
+      p.hs.flag_fail[bh] = 1u;
+      p.hs.group_fail[b * p.Hkv + h / p.G] = 1u;
+      p.hs.cand_cnt[bh] = 0u;
+      p.hs.thr[bh] = 0u;
+      p.hs.hshift[bh] = kNoFilterShift;
     }
     return;
   }
 
-  // ---- radix select: find (shift, prefix) with selected = { c : (c >> shift) >= prefix }
-  bool all = kb >= nvalid;
-  int shift = 64;
-  uint64_t prefix = 0;
+  // ---- bucket of the k-th largest
+  const bool all = kb >= nvalid;
+  uint32_t dstar = kHistBins, need = 0, bcnt = 0;
+  bool whole = true;
   if (!all && kb > 0) {
-    uint32_t need = static_cast<uint32_t>(kb);
-    for (int pi = 0; pi < 7; ++pi) {
-      const int w = digit_width(pi);
-      const int nshift = shift - w;
-      const uint32_t mask = (1u << w) - 1u;
-      if (pi > 0) {
-        for (int i = tid; i <= static_cast<int>(mask); i += NT) s_hist[i] = 0u;
-        __syncthreads();
-        for (int64_t i = tid; i < n; i += NT) {
-          const uint64_t c = load(i);
-          if (c && (c >> shift) == prefix) atomicAdd(&s_hist[(c >> nshift) & mask], 1u);
-        }
-        __syncthreads();
+    find_bucket<NT, kHistBins>(s_hist, static_cast<uint32_t>(kb), s_out, s_scr);
+    dstar = s_out[0];
+    need = static_cast<uint32_t>(kb) - s_out[1];
+    bcnt = s_hist[dstar];
+    whole = bcnt == need;
+  }
+  const bool refine = !all && !whole;
+  const bool big = refine && bcnt > static_cast<uint32_t>(kSelectBucketCap);
+  if (tid == 0) {
+    s_nout = 0u;
+    s_nbkt = 0u;
+  }
+  __syncthreads();
+
+  // ---- compaction: buckets above d* (or d* itself when taken whole) go straight out,
+  //      the candidates of d* are gathered for refinement
+  uint64_t vmax = 0ull, vmin = ~0ull;
+  if (kb > 0) {
+    constexpr int UNR = 8;  // loads in flight per thread (the loop is latency-bound otherwise)
+    for (int64_t start = 0; start < n; start += NT * UNR) {
+      uint64_t cv[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int64_t i = start + u * NT + tid;
+        cv[u] = i < n ? load(i) : 0ull;
       }
-      find_bucket_w(w, s_hist, need, s_out, s_scr);
-      const uint32_t d = s_out[0];
-      need -= s_out[1];
-      prefix = (prefix << w) | d;
-      shift = nshift;
-      const bool done = (s_hist[d] == need);
-      __syncthreads();
-      if (done) break;
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const uint64_t c = cv[u];
+        const bool valid = c != 0ull;
+        const uint32_t dg = valid ? hist_digit(comp_key(c), thr, shift) : 0u;
+        const bool sel = valid && (all || dg > dstar || (dg == dstar && whole));
+        const bool inb = valid && refine && !big && dg == dstar;
+        if (valid) vmax = c > vmax ? c : vmax;
+        emit_sel(sel, c, &s_nout, em, vmin);
+        const unsigned bb = __ballot_sync(kFull, inb);
+        uint32_t base_b = 0;
+        if (lane == 0 && bb) base_b = atomicAdd(&s_nbkt, __popc(bb));
+        base_b = __shfl_sync(kFull, base_b, 0);
+        if (inb) {
+          const uint32_t pos = base_b + __popc(bb & lanemask_lt());
+          if (pos < static_cast<uint32_t>(kSelectBucketCap)) s_bkt[pos] = c;
+        }
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- exact refinement inside the threshold bucket
+  if (refine) {
+    int cs = 64;
+    uint64_t cp = 0;
+    if (!big) {
+      const int64_t nb = s_nbkt;
+      auto ld = [&](int64_t i, uint64_t& c) {
+        c = s_bkt[i];
+        return true;
+      };
+      radix_select_u64(ld, nb, need, s_hist, s_scr, s_out, cs, cp);
+      for (int64_t start = 0; start < nb; start += NT) {
+        const int64_t i = start + tid;
+        const uint64_t c = i < nb ? s_bkt[i] : 0ull;
+        emit_sel(i < nb && (c >> cs) >= cp, c, &s_nout, em, vmin);
+      }
+    } else {
+      // rare: a threshold bucket larger than shared memory (heavy exact ties) — refine with
+      // radix passes over global memory restricted to bucket d*
+      auto ld = [&](int64_t i, uint64_t& c) {
+        c = load(i);
+        return c != 0ull && hist_digit(comp_key(c), thr, shift) == dstar;
+      };
+      radix_select_u64(ld, n, need, s_hist, s_scr, s_out, cs, cp);
+      for (int64_t start = 0; start < n; start += NT) {
+        const int64_t i = start + tid;
+        uint64_t c = 0ull;
+        const bool in = i < n && ld(i, c);
+        emit_sel(in && (c >> cs) >= cp, c, &s_nout, em, vmin);
+      }
     }
   }
 
-  // ---- ordered compaction of the selected candidates
-  if (tid == 0) s_tot = 0u;
-  uint64_t vmax = 0ull, vmin = ~0ull;
-  uint32_t base = 0;
-  __syncthreads();
-  if (kb > 0) {
-    for (int64_t start = 0; start < n; start += NT) {
-      const int64_t i = start + tid;
-      const uint64_t c = i < n ? load(i) : 0ull;
-      const bool sel = c != 0ull && (all || (c >> shift) >= prefix);
-      const unsigned bal = __ballot_sync(kFull, sel);
-      if (lane == 0) s_wofs[warp] = __popc(bal);
-      __syncthreads();
-      if (warp == 0) {
-        const uint32_t v = s_wofs[lane];
-        uint32_t incl = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t t = __shfl_up_sync(kFull, incl, o);
-          if (lane >= o) incl += t;
-        }
-        s_wofs[lane] = incl - v;
-        if (lane == 31) s_tot = incl;
-      }
-      __syncthreads();
-      if (sel) {
-        const uint32_t pos = base + s_wofs[warp] + __popc(bal & ((1u << lane) - 1u));
-        if (pos < static_cast<uint32_t>(kb)) {
-          idx_out[pos] = static_cast<int32_t>(comp_gid(c));
-          sc_out[pos] = key_score(comp_key(c));
-          if (pk_out) pk_out[pos] = c;
-        }
-        vmax = c > vmax ? c : vmax;
-        vmin = c < vmin ? c : vmin;
-      }
-      base += s_tot;
-      __syncthreads();
-    }
-  }
   // pads for k > kb (reference clamps k to N, attention.py:147-149)
   for (int64_t i = kb + tid; i < p.k; i += NT) {
-    idx_out[i] = -1;
-    sc_out[i] = -INFINITY;
-    if (pk_out) pk_out[i] = 0ull;
+    em.idx[i] = -1;
+    em.sc[i] = -INFINITY;
+    if (em.pk) em.pk[i] = 0ull;
   }
   vmax = warp_max_u64(vmax);
   vmin = warp_min_u64(vmin);
@@ -179,15 +324,15 @@ __global__ void __launch_bounds__(NT) select_kernel(SelectParams p) {
   }
   __syncthreads();
   if (warp == 0) {
-    vmax = warp_max_u64(s_rmax[lane]);
-    vmin = warp_min_u64(s_rmin[lane]);
+    vmax = warp_max_u64(lane < NWARP ? s_rmax[lane] : 0ull);
+    vmin = warp_min_u64(lane < NWARP ? s_rmin[lane] : ~0ull);
     if (lane == 0) {
       p.meta_max[bh] = kb > 0 ? key_score(comp_key(vmax)) : -INFINITY;
       p.meta_kth[bh] = kb > 0 ? vmin : ~0ull;
       p.meta_kb[bh] = static_cast<int32_t>(kb);
       if (p.pass == kPassFallback) {
-        p.flag_fail[bh] = 0u;
-        p.group_fail[b * p.Hkv + h / p.G] = 0u;
+        p.hs.flag_fail[bh] = 0u;
+        p.hs.group_fail[b * p.Hkv + h / p.G] = 0u;
       }
     }
   }
@@ -231,7 +376,13 @@ __global__ void __launch_bounds__(NT) sort_kernel(SortParams p) {
 }
 
 cudaError_t launch_select(const SelectParams& p, cudaStream_t s) {
-  select_kernel<<<p.B * p.Hq, NT, 0, s>>>(p);
+  const int smem = kSelectBucketCap * static_cast<int>(sizeof(uint64_t));
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  select_kernel<<<p.B * p.Hq, NT, smem, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -240,8 +391,12 @@ cudaError_t launch_sort(const SortParams& p, int nbh, cudaStream_t s) {
   const int kmax = p.k < kSortMax ? p.k : kSortMax;
   while (P < kmax) P <<= 1;
   const size_t smem = static_cast<size_t>(P) * sizeof(uint64_t);
-  cudaFuncSetAttribute(sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       static_cast<int>(kSortMax * sizeof(uint64_t)));
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kSortMax * sizeof(uint64_t)));
+    attr = true;
+  }
   sort_kernel<<<nbh, NT, smem, s>>>(p);
   return cudaGetLastError();
 }
