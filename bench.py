@@ -58,6 +58,18 @@ def peaks():
     return 6650.0, "fallback"
 
 
+def scan_traffic(config: str, world: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the scan kernel per launch, from the
+    committed ncu --set full capture (profiles/r*_summary.json); None when not captured."""
+    if config != "cfg3" or world != 1:
+        return None
+    caps = sorted((ROOT / "profiles").glob("r*_summary.json"))
+    if not caps:
+        return None
+    j = json.loads(caps[-1].read_text())
+    return j.get("scan_kernel", {}).get("traffic_bytes")
+
+
 class ClockSampler:
     """nvidia-smi-equivalent clock / throttle-reason sampling (NVML) during the timed region."""
 
@@ -187,7 +199,7 @@ def run_reference(args, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
@@ -318,7 +330,7 @@ def main():
                    "seed": args.seed},
         "roofline": {"bound": "hbm", "kernel": "scan_kernel (GQA key scan + candidate emit)",
                      "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": None,
+                     "frac": round(achieved / peak, 4), "traffic": scan_traffic(args.config, world),
                      "algorithmic_bytes_per_launch": kbytes, "kernel_us": round(scan_ms * 1e3, 2)},
         "step_roofline": {"algorithmic_bytes": int(step_bytes),
                           "achieved_gbs": round(step_bytes / (ms * 1e-3) / 1e9, 1),

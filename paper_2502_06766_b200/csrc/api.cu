@@ -42,7 +42,8 @@ int fail(int code, const char* fmt, ...) {
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct Layout {
-  size_t ticket_g, flag, gflag, ctrl_end;
+  size_t ticket_g, ticket_k, flag, gflag, ctrl_end;
+  size_t maxc, bktc, bkt, outc;
   size_t cnt, thr, hshift, hist, mmax, mkth, mkb, samp, cand, sidx, sscore, pl, po, total;
   int64_t cap;
   int nchunks;
@@ -59,6 +60,7 @@ Layout make_layout(const tkv_problem* p) {
     return o;
   };
   L.ticket_g = take(BH * 4);
+  L.ticket_k = take(BH * 4);
   L.flag = take(BH * 4);
   L.gflag = take(BK * 4);
   L.ctrl_end = off;
@@ -66,6 +68,10 @@ Layout make_layout(const tkv_problem* p) {
   L.thr = take(BH * 4);
   L.hshift = take(BH * 4);
   L.hist = take(BH * kHistBins * 4);
+  L.maxc = take(BH * 8);
+  L.bktc = take(BH * 4);
+  L.outc = take(BH * 4);
+  L.bkt = take(BH * kSelectBucketCap * 8);
   L.mmax = take(BH * 4);
   L.mkth = take(BH * 8);
   L.mkb = take(BH * 4);
@@ -74,7 +80,12 @@ Layout make_layout(const tkv_problem* p) {
   L.cand = take(BH * static_cast<size_t>(L.cap) * 8);
   L.sidx = take(BH * static_cast<size_t>(p->k) * 4);
   L.sscore = take(BH * static_cast<size_t>(p->k) * 4);
-  L.nchunks = static_cast<int>((p->k + kAttendChunk - 1) / kAttendChunk);
+  {
+    // partial slots per head: list mode (k / kAttendChunk) or candidate mode (cap / kCandChunk)
+    const int64_t a = (p->k + kAttendChunk - 1) / kAttendChunk;
+    const int64_t c = (L.cap + kCandChunk - 1) / kCandChunk + 1;
+    L.nchunks = static_cast<int>(a > c ? a : c);
+  }
   L.pl = take(BH * L.nchunks * 4);
   L.po = take(BH * L.nchunks * kD * 4);
   L.total = off;
@@ -143,13 +154,18 @@ HeadState head_state(void* ws, const Layout& L) {
   hs.hist = at<uint32_t>(ws, L.hist);
   hs.flag_fail = at<uint32_t>(ws, L.flag);
   hs.group_fail = at<uint32_t>(ws, L.gflag);
+  hs.max_comp = at<uint64_t>(ws, L.maxc);
+  hs.bkt_cnt = at<uint32_t>(ws, L.bktc);
+  hs.bkt = at<uint64_t>(ws, L.bkt);
+  hs.kth_ticket = at<uint32_t>(ws, L.ticket_k);
+  hs.out_cnt = at<uint32_t>(ws, L.outc);
   return hs;
 }
 
-// sample → threshold → scan → select (+ fallback scan/select) [→ sort]; results in idx/scores
+// sample → threshold → scan → k-th threshold (+ exactness fallback: re-scan / k-th); the
+// selected set is { candidates c : c >= meta_kth }, materialised by run_emit
 int run_select(const tkv_problem* p, const void* q, const void* k_cache, const int32_t* n_ctx,
-               int32_t* idx, float* scores, void* ws, const Layout& L, cudaStream_t st,
-               uint64_t* packed_out) {
+               void* ws, const Layout& L, cudaStream_t st) {
   const int G = p->n_q_heads / p->n_kv_heads;
   const HeadState hs = head_state(ws, L);
   SampleParams sp{};
@@ -196,26 +212,18 @@ int run_select(const tkv_problem* p, const void* q, const void* k_cache, const i
   sl.G = G;
   sl.k = p->k;
   sl.n_ctx = n_ctx;
-  sl.idx = idx;
-  sl.scores = scores;
   sl.meta_max = at<float>(ws, L.mmax);
   sl.meta_kth = at<uint64_t>(ws, L.mkth);
   sl.meta_kb = at<int32_t>(ws, L.mkb);
   sl.hs = hs;
-  sl.packed_out = packed_out;
   sl.pass = kPassMain;
-  TKV_LAUNCH(launch_select(sl, st));
+  TKV_LAUNCH(launch_kth(sl, st));
 
   // exactness fallback: heads whose sampled threshold let fewer than k rows through
   cp.fallback = 1;
   TKV_LAUNCH(launch_scan(cp, st));
   sl.pass = kPassFallback;
-  TKV_LAUNCH(launch_select(sl, st));
-
-  if (p->flags & TKV_F_SORTED) {
-    SortParams so{idx, scores, sl.meta_kb, p->k};
-    TKV_LAUNCH(launch_sort(so, p->batch * p->n_q_heads, st));
-  }
+  TKV_LAUNCH(launch_kth(sl, st));
   return TKV_OK;
 }
 
@@ -247,7 +255,31 @@ AttendParams make_attend(const tkv_problem* p, const void* q, const void* k_cach
   a.part_o = at<float>(ws, L.po);
   a.ticket = at<uint32_t>(ws, L.ticket_g);
   a.nchunks = L.nchunks;
+  a.cand = at<uint64_t>(ws, L.cand);
+  a.cap = L.cap;
+  a.cand_cnt = at<uint32_t>(ws, L.cnt);
+  a.out_cnt = at<uint32_t>(ws, L.outc);
   return a;
+}
+
+// Materialise the selected rows (idx/scores[/packed]) from the candidates, with the V
+// gather + softmax fused when gather != 0; then the optional TopKResult-order sort.
+int run_emit(const tkv_problem* p, const void* q, const void* k_cache, const void* v_cache,
+             const int32_t* n_ctx, const int32_t* n_win, int32_t* idx, float* scores,
+             uint64_t* packed, float* out, int gather, void* ws, const Layout& L, cudaStream_t st) {
+  AttendParams a = make_attend(p, q, k_cache, v_cache, n_ctx, n_win, idx, scores, ws, L);
+  a.idx_out = idx;
+  a.scores_out = scores;
+  a.packed_out = packed;
+  a.out = out;
+  a.gather = gather;
+  a.partial_only = 0;
+  TKV_LAUNCH(launch_attend_cand(a, st));
+  if (p->flags & TKV_F_SORTED) {
+    SortParams so{idx, scores, at<int32_t>(ws, L.mkb), p->k};
+    TKV_LAUNCH(launch_sort(so, p->batch * p->n_q_heads, st));
+  }
+  return TKV_OK;
 }
 
 }  // namespace
@@ -314,12 +346,8 @@ int tkv_topk_decode_attention(const tkv_problem* p, const void* q, const void* k
   if (n_win) TRY(check_ptr(n_win, "n_win", 4));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   float* sc = scores ? scores : at<float>(ws, L.sscore);
-  TRY(run_select(p, q, k_cache, n_ctx, idx, sc, ws, L, st, nullptr));
-  AttendParams a = make_attend(p, q, k_cache, v_cache, n_ctx, n_win, idx, sc, ws, L);
-  a.partial_only = 0;
-  a.out = out;
-  TKV_LAUNCH(launch_attend(a, st));
-  return TKV_OK;
+  TRY(run_select(p, q, k_cache, n_ctx, ws, L, st));
+  return run_emit(p, q, k_cache, v_cache, n_ctx, n_win, idx, sc, nullptr, out, 1, ws, L, st);
 }
 
 int tkv_topk_search(const tkv_problem* p, const void* q, const void* k_cache, const int32_t* n_ctx,
@@ -333,7 +361,9 @@ int tkv_topk_search(const tkv_problem* p, const void* q, const void* k_cache, co
   TRY(check_ptr(n_ctx, "n_ctx", 4));
   TRY(check_ptr(idx, "idx", 4));
   float* sc = scores ? scores : at<float>(ws, L.sscore);
-  return run_select(p, q, k_cache, n_ctx, idx, sc, ws, L, static_cast<cudaStream_t>(stream), nullptr);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  TRY(run_select(p, q, k_cache, n_ctx, ws, L, st));
+  return run_emit(p, q, k_cache, k_cache, n_ctx, nullptr, idx, sc, nullptr, nullptr, 0, ws, L, st);
 }
 
 int tkv_kv_append(int32_t batch, int32_t n_kv_heads, int32_t head_dim, int64_t cache_rows,
@@ -374,8 +404,12 @@ int tkv_shard_candidates(const tkv_problem* p, const void* q, const void* k_cach
   TRY(check_ptr(k_cache, "k_cache", 16));
   TRY(check_ptr(n_ctx, "n_ctx", 4));
   TRY(check_ptr(cand, "cand", 8));
-  return run_select(p, q, k_cache, n_ctx, at<int32_t>(ws, L.sidx), at<float>(ws, L.sscore), ws, L,
-                    static_cast<cudaStream_t>(stream), cand);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  TRY(run_select(p, q, k_cache, n_ctx, ws, L, st));
+  tkv_problem pu = *p;
+  pu.flags &= ~TKV_F_SORTED;
+  return run_emit(&pu, q, k_cache, k_cache, n_ctx, nullptr, at<int32_t>(ws, L.sidx), at<float>(ws, L.sscore),
+                  cand, nullptr, 0, ws, L, st);
 }
 
 int tkv_shard_merge(const tkv_problem* p, const uint64_t* gathered, int32_t n_shards, int32_t* idx,

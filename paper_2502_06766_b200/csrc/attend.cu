@@ -127,39 +127,27 @@ __device__ void finalize_head(const AttendParams& p, int b, int h, int kvh, int6
   __syncthreads();
   if (tid < kD) p.out[static_cast<int64_t>(bh) * kD + tid] = s_o[tid] + s_o[tid + kD];
 }
-}  // namespace
 
-__global__ void __launch_bounds__(NT) attend_kernel(AttendParams p) {
-  __shared__ float s_w[kAttendChunk];
-  __shared__ int32_t s_row[kAttendChunk];
-  __shared__ float s_red[NW][kD];
-  __shared__ float s_l[NW];
-  __shared__ float s_z[128];
-  __shared__ float s_scr[32];
-  __shared__ float s_o[NT];
-  __shared__ int s_last;
+struct AttSmem {
+  float w[kCandChunk];
+  int32_t row[kCandChunk];
+  float red[NW][kD];
+  float l[NW];
+  float z[128];
+  float scr[32];
+  float o[NT];
+  uint32_t wcnt[NW];
+  uint32_t base;
+  int last;
+};
 
-  const int ch = blockIdx.x, bh = blockIdx.y;
+// Gather the V rows listed in sm.row (local rows, -1 = skip) weighted by sm.w, reduce into the
+// head's partial slot, and let the last CTA of the head (atomic ticket over nslots) combine
+// the partials in slot order (deterministic), add the pinned-prefix rows and the window, and
+// write out (or the (l, o) partial in sharded mode).
+__device__ void chunk_body(const AttendParams& p, int bh, int slot, int nslots, int nrows, AttSmem& sm) {
   const int b = bh / p.Hq, h = bh % p.Hq, kvh = h / p.G;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int kb = p.meta_kb[bh];
-  const int lo = ch * kAttendChunk;
-  int nrows = kb - lo;
-  nrows = nrows < 0 ? 0 : (nrows > kAttendChunk ? kAttendChunk : nrows);
-  const float zs = p.scale * kLog2e;
-  const float zref = kb > 0 ? p.meta_max[bh] * zs : 0.f;
-  const int64_t nctx = p.n_ctx[b];
-
-  for (int i = tid; i < nrows; i += NT) {
-    const int64_t gid = p.idx[static_cast<int64_t>(bh) * p.k + lo + i];
-    const float s = p.scores[static_cast<int64_t>(bh) * p.k + lo + i];
-    const int64_t local = gid - p.row_offset;
-    const bool owned = local >= 0 && local < nctx;
-    s_row[i] = owned ? static_cast<int32_t>(local) : -1;
-    s_w[i] = owned ? exp2f(fmaf(s, zs, -zref)) : 0.f;
-  }
-  __syncthreads();
-
   const int half = lane >> 4, part = lane & 15;
   const __nv_bfloat16* vb =
       p.vc + (static_cast<int64_t>(b) * p.Hkv + kvh) * p.cache_rows * kD + part * 8;
@@ -173,8 +161,8 @@ __global__ void __launch_bounds__(NT) attend_kernel(AttendParams p) {
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
       const int r = r0 + 2 * NW * u;
-      const int row = r < nrows ? s_row[r] : -1;
-      w[u] = r < nrows ? s_w[r] : 0.f;
+      const int row = r < nrows ? sm.row[r] : -1;
+      w[u] = r < nrows ? sm.w[r] : 0.f;
       v[u] = row >= 0 ? ldg_nc(vb + static_cast<int64_t>(row) * kD) : make_uint4(0, 0, 0, 0);
     }
 #pragma unroll
@@ -193,49 +181,205 @@ __global__ void __launch_bounds__(NT) attend_kernel(AttendParams p) {
   for (int j = 0; j < 8; ++j) acc[j] += __shfl_xor_sync(kFull, acc[j], 16);
   if (half == 0) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) s_red[warp][part * 8 + j] = acc[j];
+    for (int j = 0; j < 8; ++j) sm.red[warp][part * 8 + j] = acc[j];
   }
   float lw = 0.f;
-  for (int i = tid; i < nrows; i += NT) lw += s_w[i];
+  for (int i = tid; i < nrows; i += NT) lw += sm.w[i];
   lw = warp_sum(lw);
-  if (lane == 0) s_l[warp] = lw;
+  if (lane == 0) sm.l[warp] = lw;
   __syncthreads();
   if (tid < kD) {
     float o = 0.f;
 #pragma unroll
-    for (int w2 = 0; w2 < NW; ++w2) o += s_red[w2][tid];
-    p.part_o[(static_cast<int64_t>(bh) * p.nchunks + ch) * kD + tid] = o;
+    for (int w2 = 0; w2 < NW; ++w2) o += sm.red[w2][tid];
+    p.part_o[(static_cast<int64_t>(bh) * p.nchunks + slot) * kD + tid] = o;
   }
   if (tid == 0) {
     float l = 0.f;
 #pragma unroll
-    for (int w2 = 0; w2 < NW; ++w2) l += s_l[w2];
-    p.part_l[static_cast<int64_t>(bh) * p.nchunks + ch] = l;
+    for (int w2 = 0; w2 < NW; ++w2) l += sm.l[w2];
+    p.part_l[static_cast<int64_t>(bh) * p.nchunks + slot] = l;
   }
   __threadfence();
   __syncthreads();
-  if (tid == 0) s_last = (atomicAdd(&p.ticket[bh], 1u) == static_cast<unsigned>(p.nchunks - 1));
+  if (tid == 0) sm.last = (atomicAdd(&p.ticket[bh], 1u) == static_cast<unsigned>(nslots - 1));
   __syncthreads();
-  if (!s_last) return;
+  if (!sm.last) return;
   __threadfence();
 
-  // ---- last CTA of this head: deterministic chunk-order combine
+  // ---- last CTA of this head: deterministic slot-order combine
+  const int kb = p.meta_kb[bh];
+  const float zref = kb > 0 ? p.meta_max[bh] * p.scale * kLog2e : 0.f;
+  const int64_t nctx = p.n_ctx[b];
   float o_c = 0.f, l_c = 0.f;
-  for (int c2 = 0; c2 < p.nchunks; ++c2) {
+  for (int c2 = 0; c2 < nslots; ++c2) {
     if (tid < kD) o_c += __ldcg(&p.part_o[(static_cast<int64_t>(bh) * p.nchunks + c2) * kD + tid]);
     l_c += __ldcg(&p.part_l[static_cast<int64_t>(bh) * p.nchunks + c2]);
   }
   if (tid == 0) p.ticket[bh] = 0u;
-  add_pinned(p, b, h, kvh, nctx, kb, zref, l_c, o_c, s_z, s_scr);
+  add_pinned(p, b, h, kvh, nctx, kb, zref, l_c, o_c, sm.z, sm.scr);
   if (p.partial_only) {
-    s_o[tid] = o_c;
+    sm.o[tid] = o_c;
     __syncthreads();
     float* dst = p.partial_out + static_cast<int64_t>(bh) * (kD + 1);
     if (tid == 0) dst[0] = l_c;
-    if (tid < kD) dst[1 + tid] = s_o[tid] + s_o[tid + kD];
+    if (tid < kD) dst[1 + tid] = sm.o[tid] + sm.o[tid + kD];
+    __syncthreads();
     return;
   }
-  finalize_head(p, b, h, kvh, nctx, zref, l_c, o_c, s_z, s_scr, s_o);
+  finalize_head(p, b, h, kvh, nctx, zref, l_c, o_c, sm.z, sm.scr, sm.o);
+  __syncthreads();
+}
+}  // namespace
+
+// List mode (sharded partial): the selected (idx, score) list is given.
+__global__ void __launch_bounds__(NT) attend_kernel(AttendParams p) {
+  __shared__ AttSmem sm;
+  const int ch = blockIdx.x, bh = blockIdx.y;
+  const int b = bh / p.Hq;
+  const int kb = p.meta_kb[bh];
+  const int lo = ch * kAttendChunk;
+  int nrows = kb - lo;
+  nrows = nrows < 0 ? 0 : (nrows > kAttendChunk ? kAttendChunk : nrows);
+  const float zs = p.scale * kLog2e;
+  const float zref = kb > 0 ? p.meta_max[bh] * zs : 0.f;
+  const int64_t nctx = p.n_ctx[b];
+  for (int i = threadIdx.x; i < nrows; i += NT) {
+    const int64_t gid = p.idx[static_cast<int64_t>(bh) * p.k + lo + i];
+    const float s = p.scores[static_cast<int64_t>(bh) * p.k + lo + i];
+    const int64_t local = gid - p.row_offset;
+    const bool owned = local >= 0 && local < nctx;
+    sm.row[i] = owned ? static_cast<int32_t>(local) : -1;
+    sm.w[i] = owned ? exp2f(fmaf(s, zs, -zref)) : 0.f;
+  }
+  __syncthreads();
+  chunk_body(p, bh, ch, p.nchunks, nrows, sm);
+}
+
+// Candidate mode (single GPU): persistent CTAs walk (head, chunk of kCandChunk candidates)
+// work items; a candidate is selected iff its composite >= meta_kth (kth_kernel), which is
+// exactly the top-kb set. Selected rows are appended to idx/scores (order unspecified) and,
+// with p.gather, their V rows are gathered in the same pass.
+__global__ void __launch_bounds__(NT) attend_cand_kernel(AttendParams p) {
+  __shared__ AttSmem sm;
+  extern __shared__ uint32_t s_pref[];  // [B*Hq + 1] work-item prefix over heads
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int BH = p.B * p.Hq;
+  auto nslots_of = [&](int bh) -> int {
+    int64_t n = p.cand_cnt[bh];
+    if (n > p.cap) n = p.cap;
+    const int c = static_cast<int>((n + kCandChunk - 1) / kCandChunk);
+    return c > 0 ? c : 1;  // every head gets >= 1 item so its output is always finalized
+  };
+  // exclusive prefix of work items per head (block-wide, BH <= a few thousand)
+  {
+    const int per = (BH + NT - 1) / NT;
+    uint32_t sum = 0;
+    for (int j = 0; j < per; ++j) {
+      const int bh = tid * per + j;
+      sum += bh < BH ? nslots_of(bh) : 0;
+    }
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) sm.wcnt[warp] = incl;
+    __syncthreads();
+    uint32_t woff = 0;
+    for (int w = 0; w < warp; ++w) woff += sm.wcnt[w];
+    uint32_t run = woff + incl - sum;
+    for (int j = 0; j < per; ++j) {
+      const int bh = tid * per + j;
+      if (bh < BH) {
+        s_pref[bh] = run;
+        run += nslots_of(bh);
+      }
+    }
+    if (tid == NT - 1) s_pref[BH] = run;
+    __syncthreads();
+  }
+  const uint32_t total = s_pref[BH];
+  const float zs = p.scale * kLog2e;
+  for (uint32_t item = blockIdx.x; item < total; item += gridDim.x) {
+    int lo = 0, hi = BH;  // largest bh with s_pref[bh] <= item
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (s_pref[mid] <= item) lo = mid; else hi = mid;
+    }
+    const int bh = lo;
+    const int slot = static_cast<int>(item - s_pref[bh]);
+    const int nslots = static_cast<int>(s_pref[bh + 1] - s_pref[bh]);
+    const int b = bh / p.Hq;
+    int64_t n = p.cand_cnt[bh];
+    if (n > p.cap) n = p.cap;
+    const int kb = p.meta_kb[bh];
+    const uint64_t T = p.meta_kth[bh];
+    const float zref = kb > 0 ? p.meta_max[bh] * zs : 0.f;
+    const uint64_t* src = p.cand + static_cast<int64_t>(bh) * p.cap + static_cast<int64_t>(slot) * kCandChunk;
+    int64_t cnt = n - static_cast<int64_t>(slot) * kCandChunk;
+    cnt = cnt < 0 ? 0 : (cnt > kCandChunk ? kCandChunk : cnt);
+    constexpr int PER = kCandChunk / NT;
+    uint64_t cv[PER];
+    bool sel[PER];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int i = u * NT + tid;
+      cv[u] = (i < cnt && kb > 0) ? src[i] : 0ull;
+      sel[u] = cv[u] != 0ull && cv[u] >= T;
+    }
+    // block-ordered compaction of the selected candidates
+    uint32_t mine = 0;
+#pragma unroll
+    for (int u = 0; u < PER; ++u) mine += sel[u] ? 1u : 0u;
+    uint32_t incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) sm.wcnt[warp] = incl;
+    __syncthreads();
+    uint32_t woff = 0, m = 0;
+    for (int w = 0; w < NW; ++w) {
+      woff += w < warp ? sm.wcnt[w] : 0u;
+      m += sm.wcnt[w];
+    }
+    if (tid == 0) sm.base = m ? atomicAdd(&p.out_cnt[bh], m) : 0u;
+    __syncthreads();
+    const uint32_t obase = sm.base;
+    uint32_t pos = woff + incl - mine;
+    int32_t* idx_o = p.idx_out + static_cast<int64_t>(bh) * p.k;
+    float* sc_o = p.scores_out + static_cast<int64_t>(bh) * p.k;
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      if (sel[u]) {
+        const uint64_t c = cv[u];
+        const uint32_t gid = comp_gid(c);
+        const float s = key_score(comp_key(c));
+        const uint32_t o = obase + pos;
+        if (o < static_cast<uint32_t>(p.k)) {
+          idx_o[o] = static_cast<int32_t>(gid);
+          sc_o[o] = s;
+          if (p.packed_out) p.packed_out[static_cast<int64_t>(bh) * p.k + o] = c;
+        }
+        sm.row[pos] = static_cast<int32_t>(static_cast<int64_t>(gid) - p.row_offset);
+        sm.w[pos] = exp2f(fmaf(s, zs, -zref));
+        ++pos;
+      }
+    }
+    if (slot == 0) {  // pads for k > kb (reference clamps k to N, attention.py:147-149)
+      for (int i = kb + tid; i < p.k; i += NT) {
+        idx_o[i] = -1;
+        sc_o[i] = -INFINITY;
+        if (p.packed_out) p.packed_out[static_cast<int64_t>(bh) * p.k + i] = 0ull;
+      }
+    }
+    __syncthreads();
+    if (p.gather) chunk_body(p, bh, slot, nslots, static_cast<int>(m), sm);
+    (void)b;
+  }
 }
 
 // Sharded finalize: partial_in holds the all-reduced (l, o[128]) per head.
@@ -278,6 +422,20 @@ __global__ void __launch_bounds__(256) append_kernel(AppendParams p) {
 cudaError_t launch_attend(const AttendParams& p, cudaStream_t s) {
   dim3 grid(p.nchunks, p.B * p.Hq);
   attend_kernel<<<grid, NT, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_attend_cand(const AttendParams& p, cudaStream_t s) {
+  static int grid = 0;
+  if (!grid) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, attend_cand_kernel, NT, 8192);
+    grid = sms * (per > 0 ? per : 1);
+  }
+  const size_t smem = (static_cast<size_t>(p.B) * p.Hq + 1) * sizeof(uint32_t);
+  attend_cand_kernel<<<grid, NT, smem, s>>>(p);
   return cudaGetLastError();
 }
 

@@ -150,6 +150,47 @@ __device__ __forceinline__ void hist_add_aggregated(uint32_t* hist, uint32_t dig
   if ((threadIdx.x & 31) == static_cast<unsigned>(__ffs(peers) - 1)) atomicAdd(&hist[digit], __popc(peers));
 }
 
+// Copy n (multiple of 4, 16-byte aligned) u32 words global → shared with every load of a
+// thread issued before its first store (one memory round trip instead of n / NT). L2 path.
+template <int NT, int MAXN>
+__device__ __forceinline__ void copy_g2s_u32(uint32_t* dst, const uint32_t* src, int n) {
+  constexpr int PER = (MAXN / 4 + NT - 1) / NT;
+  uint4 v[PER];
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int i = (u * NT + threadIdx.x) * 4;
+    v[u] = i < n ? __ldcg(reinterpret_cast<const uint4*>(src + i)) : make_uint4(0, 0, 0, 0);
+  }
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int i = (u * NT + threadIdx.x) * 4;
+    if (i < n) *reinterpret_cast<uint4*>(dst + i) = v[u];
+  }
+}
+
+// ---------------------------------------------------------------- small-set selection
+// need-th largest (1-indexed) of m values in shared memory by rank counting: thread-parallel
+// O(m^2 / NT) compares, two barriers — for the few hundred elements of a threshold bucket
+// this beats any multi-pass radix. Duplicates allowed: returns the value v with
+// #{> v} < need <= #{>= v}. Result broadcast through *out. Block-wide call.
+template <int NT, typename T>
+__device__ __forceinline__ T block_rank_select(const T* vals, int m, int need, T* out) {
+  for (int i = threadIdx.x; i < m; i += NT) {
+    const T v = vals[i];
+    int gt = 0, ge = 0;
+    for (int j = 0; j < m; ++j) {
+      const T w = vals[j];
+      gt += w > v;
+      ge += w >= v;
+    }
+    if (gt < need && need <= ge) *out = v;  // all qualifying threads hold the same value
+  }
+  __syncthreads();
+  const T r = *out;
+  __syncthreads();
+  return r;
+}
+
 // ---------------------------------------------------------------- block helpers
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {

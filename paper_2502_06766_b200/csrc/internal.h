@@ -17,9 +17,12 @@ constexpr int kScanFlushEvery = 4;                   // iterations between stagi
 constexpr int kScanStage = kScanRows * kScanFlushEvery;  // staged candidates per head
 constexpr int kSelectThreads = 1024;
 constexpr int kSelectBucketCap = 8192;  // threshold-bucket candidates refined in shared memory
+constexpr int kKthThreads = 512;        // kth_kernel CTA
+constexpr int kKthCtas = 4;             // kth_kernel CTAs per (b, q head)
 constexpr int kAttendThreads = 256;
-constexpr int kAttendChunk = 512;  // selected rows per gather CTA
-constexpr int kSortMax = 16384;    // sorted output supported up to this k
+constexpr int kAttendChunk = 512;    // selected rows per gather CTA (list mode)
+constexpr int kCandChunk = 1024;     // candidates per work item (candidate mode)
+constexpr int kSortMax = 16384;      // sorted output supported up to this k
 constexpr uint32_t kNoFilterShift = 20;  // histogram shift when every score is a candidate
 
 // per-(b, q head) state shared by the kernels of one call, in the workspace
@@ -30,6 +33,11 @@ struct HeadState {
   uint32_t* hist;        // [B*Hq][kHistBins] histogram of the emitted candidates
   uint32_t* flag_fail;   // [B*Hq] sampled threshold too high → re-scan with thr = 0
   uint32_t* group_fail;  // [B*Hkv]
+  uint64_t* max_comp;    // [B*Hq] largest candidate composite (reset by threshold_kernel)
+  uint32_t* bkt_cnt;     // [B*Hq] candidates of the threshold bucket gathered so far
+  uint64_t* bkt;         // [B*Hq][kSelectBucketCap] threshold-bucket candidates
+  uint32_t* kth_ticket;  // [B*Hq] kth_kernel CTAs done (self-resetting)
+  uint32_t* out_cnt;     // [B*Hq] selected rows written so far (reset by threshold_kernel)
 };
 
 struct SampleParams {
@@ -103,11 +111,21 @@ struct AttendParams {
   float* part_l;  // [B*Hq*nchunks]
   float* part_o;  // [B*Hq*nchunks*D]
   uint32_t* ticket;
-  int nchunks;
+  int nchunks;       // list mode: chunks per head; candidate mode: partial slots per head
   int partial_only;  // 1: write (l, o) to partial_out; 0: finalize into out
   float* partial_out;
   const float* partial_in;  // finalize kernel input
   float* out;
+  // candidate mode (single GPU): read the scan's candidates, keep c >= meta_kth, write
+  // idx/scores (and packed composites) as a side effect, gather V of the kept rows
+  const uint64_t* cand;
+  int64_t cap;
+  const uint32_t* cand_cnt;
+  uint32_t* out_cnt;
+  int32_t* idx_out;
+  float* scores_out;
+  uint64_t* packed_out;
+  int gather;  // 0: only write the selected rows (no attention)
 };
 
 struct AppendParams {
@@ -125,6 +143,8 @@ struct AppendParams {
 cudaError_t launch_sample(const SampleParams& p, cudaStream_t s);
 cudaError_t launch_scan(const ScanParams& p, cudaStream_t s);
 cudaError_t launch_select(const SelectParams& p, cudaStream_t s);
+cudaError_t launch_kth(const SelectParams& p, cudaStream_t s);
+cudaError_t launch_attend_cand(const AttendParams& p, cudaStream_t s);
 cudaError_t launch_sort(const SortParams& p, int nbh, cudaStream_t s);
 cudaError_t launch_attend(const AttendParams& p, cudaStream_t s);
 cudaError_t launch_finalize(const AttendParams& p, cudaStream_t s);

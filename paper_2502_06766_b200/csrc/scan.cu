@@ -81,12 +81,10 @@ __global__ void __launch_bounds__(kThrThreads) threshold_kernel(SampleParams p) 
 
   uint32_t thr = 0u, shift = kNoFilterShift;
   if (filter) {
+    copy_g2s_u32<NT, kSamples>(s_keys, p.samp + static_cast<int64_t>(bh) * kSamples, (Sb + 3) & ~3);
+    __syncthreads();
     uint32_t mx = 0u;
-    for (int i = tid; i < Sb; i += NT) {
-      const uint32_t k = p.samp[static_cast<int64_t>(bh) * kSamples + i];
-      s_keys[i] = k;
-      mx = k > mx ? k : mx;
-    }
+    for (int i = tid; i < Sb; i += NT) mx = max(mx, s_keys[i]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(kFull, mx, o));
     if (lane == 0) s_max[warp] = mx;
@@ -96,6 +94,7 @@ __global__ void __launch_bounds__(kThrThreads) threshold_kernel(SampleParams p) 
     // which is <= the r-th key (a threshold only has to be a lower bound).
     uint32_t prefix = 0, need = static_cast<uint32_t>(rr);
     int sh = 32;
+    bool exact = false;
     for (int pi = 0; pi < 3; ++pi) {
       const int w = pi < 2 ? 11 : 10;
       const int nsh = sh - w;
@@ -114,11 +113,27 @@ __global__ void __launch_bounds__(kThrThreads) threshold_kernel(SampleParams p) 
       need -= s_out[1];
       prefix = (prefix << w) | s_out[0];
       sh = nsh;
-      const bool done = s_hist[s_out[0]] == need;
+      const uint32_t bc = s_hist[s_out[0]];
+      const bool done = bc == need;
       __syncthreads();
       if (done) break;
+      if (bc <= 2048u) {
+        // small bucket (the usual case after one 11-bit digit): gather it and finish with
+        // rank counting instead of two more radix passes
+        __shared__ uint32_t s_n, s_res;
+        if (tid == 0) s_n = 0u;
+        __syncthreads();
+        for (int i = tid; i < Sb; i += NT) {
+          const uint32_t k = s_keys[i];
+          if ((k >> sh) == prefix) s_hist[atomicAdd(&s_n, 1u)] = k;
+        }
+        __syncthreads();
+        thr = block_rank_select<NT>(s_hist, static_cast<int>(s_n), static_cast<int>(need), &s_res);
+        exact = true;
+        break;
+      }
     }
-    thr = sh > 0 ? prefix << sh : prefix;
+    if (!exact) thr = sh > 0 ? prefix << sh : prefix;
     uint32_t smax = 0u;
     for (int w = 0; w < NT / 32; ++w) smax = max(smax, s_max[w]);
     // histogram granularity: the sampled range [thr, smax] spans ~1/4 of the 4096 buckets,
@@ -133,6 +148,9 @@ __global__ void __launch_bounds__(kThrThreads) threshold_kernel(SampleParams p) 
     p.hs.thr[bh] = thr;
     p.hs.hshift[bh] = shift;
     p.hs.cand_cnt[bh] = 0u;
+    p.hs.max_comp[bh] = 0ull;
+    p.hs.bkt_cnt[bh] = 0u;
+    p.hs.out_cnt[bh] = 0u;
   }
 }
 

@@ -32,22 +32,22 @@ constexpr int NWARP = NT / 32;
 
 // Radix select of the `need` largest composites among the elements accepted by `load`
 // (load(i, c) -> bool), MSB first with 8-bit digits. Result: selected ⇔ (c >> shift) >= prefix.
-template <typename Load>
+template <int T = NT, typename Load>
 __device__ void radix_select_u64(Load load, int64_t n, uint32_t need, uint32_t* hist, uint32_t* scr,
                                  uint32_t* out, int& shift_out, uint64_t& prefix_out) {
   int shift = 64;
   uint64_t prefix = 0;
   while (shift > 0) {
     const int nshift = shift - 8;
-    for (int i = threadIdx.x; i < 256; i += NT) hist[i] = 0u;
+    for (int i = threadIdx.x; i < 256; i += T) hist[i] = 0u;
     __syncthreads();
-    for (int64_t i = threadIdx.x; i < n; i += NT) {
+    for (int64_t i = threadIdx.x; i < n; i += T) {
       uint64_t c;
       if (load(i, c) && (shift == 64 || (c >> shift) == prefix))
         hist_add_aggregated(hist, static_cast<uint32_t>(c >> nshift) & 255u);
     }
     __syncthreads();
-    find_bucket<NT, 256>(hist, need, out, scr);
+    find_bucket<T, 256>(hist, need, out, scr);
     const uint32_t d = out[0];
     need -= out[1];
     prefix = (prefix << 8) | d;
@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(NT) select_kernel(SelectParams p) {
     shift = p.hs.hshift[bh];
     nvalid = n;
     const uint32_t* gh = p.hs.hist + static_cast<int64_t>(bh) * kHistBins;
-    for (int i = tid; i < kHistBins; i += NT) s_hist[i] = __ldcg(&gh[i]);
+    copy_g2s_u32<NT, kHistBins>(s_hist, gh, kHistBins);
     __syncthreads();
   } else {
     uint32_t kmin = 0xffffffffu, kmax = 0u, nv = 0u;
@@ -336,6 +336,182 @@ __global__ void __launch_bounds__(NT) select_kernel(SelectParams p) {
       }
     }
   }
+}
+
+// ---------------------------------------------------------------- k-th threshold only
+// kth_kernel: grid (kKthCtas, B*Hq). Finds the composite threshold T of each head such that
+// { c >= T } is exactly the top-kb candidate set, without writing the set itself (the
+// candidate-mode attend kernel filters the candidates with T while gathering V):
+//   every CTA derives the bucket d* of the kb-th largest from the scan's histogram, scans its
+//   slice of the candidates for the maximum and for the members of d* (appended to a small
+//   per-head buffer); the last CTA of the head refines inside that buffer (shared memory,
+//   8-bit radix over the 64-bit composites → exact lower-id tie resolution).
+__global__ void __launch_bounds__(kKthThreads) kth_kernel(SelectParams p) {
+  constexpr int KT = kKthThreads, KW = KT / 32;
+  extern __shared__ uint64_t s_bkt[];  // [kSelectBucketCap]
+  __shared__ uint32_t s_hist[kHistBins];
+  __shared__ uint32_t s_scr[32];
+  __shared__ uint32_t s_out[2];
+  __shared__ uint64_t s_rmax[KW];
+  __shared__ int s_last;
+
+  const int bh = blockIdx.y, part = blockIdx.x, P = gridDim.x;
+  const int b = bh / p.Hq, h = bh % p.Hq;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (p.pass == kPassFallback && p.hs.flag_fail[bh] == 0u) return;
+
+  const uint64_t* src = p.src + static_cast<int64_t>(bh) * p.src_stride;
+  int64_t n = p.hs.cand_cnt[bh];
+  if (n > p.src_stride) n = p.src_stride;
+  const int64_t N = p.n_ctx[b];
+  const int64_t kb = N < p.k ? N : p.k;
+
+  if (p.pass == kPassMain && n < kb) {
+    // The sampled threshold let fewer than k rows through: re-scan this head with thr = 0.
+    if (part == 0) {
+      uint32_t* gh = p.hs.hist + static_cast<int64_t>(bh) * kHistBins;
+      for (int i = tid; i < kHistBins; i += KT) gh[i] = 0u;
+      if (tid == 0) {
+        p.hs.flag_fail[bh] = 1u;
+        p.hs.group_fail[b * p.Hkv + h / p.G] = 1u;
+        p.hs.cand_cnt[bh] = 0u;
+        p.hs.thr[bh] = 0u;
+        p.hs.hshift[bh] = kNoFilterShift;
+      }
+    }
+    return;
+  }
+  if (kb == 0) {
+    if (part == 0 && tid == 0) {
+      p.meta_kth[bh] = ~0ull;
+      p.meta_kb[bh] = 0;
+      p.meta_max[bh] = -INFINITY;
+      if (p.pass == kPassFallback) {
+        p.hs.flag_fail[bh] = 0u;
+        p.hs.group_fail[b * p.Hkv + h / p.G] = 0u;
+      }
+    }
+    return;
+  }
+
+  const uint32_t thr = p.hs.thr[bh], shift = p.hs.hshift[bh];
+  const bool all = kb >= n;
+  uint32_t dstar = 0, need = 0, bcnt = 0;
+  bool whole = true;
+  if (!all) {
+    const uint32_t* gh = p.hs.hist + static_cast<int64_t>(bh) * kHistBins;
+    copy_g2s_u32<KT, kHistBins>(s_hist, gh, kHistBins);
+    __syncthreads();
+    find_bucket<KT, kHistBins>(s_hist, static_cast<uint32_t>(kb), s_out, s_scr);
+    dstar = s_out[0];
+    need = static_cast<uint32_t>(kb) - s_out[1];
+    bcnt = s_hist[dstar];
+    whole = bcnt == need;
+  }
+  const bool refine = !all && !whole;
+  const bool big = refine && bcnt > static_cast<uint32_t>(kSelectBucketCap);
+
+  // ---- slice scan: maximum + members of the threshold bucket
+  const int64_t lo = n * part / P, hi = n * (part + 1) / P;
+  uint64_t vmax = 0ull;
+  uint64_t* gbkt = p.hs.bkt + static_cast<int64_t>(bh) * kSelectBucketCap;
+  constexpr int UNR = 8;
+  for (int64_t start = lo; start < hi; start += KT * UNR) {
+    uint64_t cv[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int64_t i = start + u * KT + tid;
+      cv[u] = i < hi ? src[i] : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const uint64_t c = cv[u];
+      vmax = c > vmax ? c : vmax;
+      const bool inb = refine && !big && c != 0ull && hist_digit(comp_key(c), thr, shift) == dstar;
+      const unsigned bb = __ballot_sync(kFull, inb);
+      if (bb) {
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(&p.hs.bkt_cnt[bh], __popc(bb));
+        base = __shfl_sync(kFull, base, 0);
+        if (inb) {
+          const uint32_t pos = base + __popc(bb & lanemask_lt());
+          if (pos < static_cast<uint32_t>(kSelectBucketCap)) gbkt[pos] = c;
+        }
+      }
+    }
+  }
+  vmax = warp_max_u64(vmax);
+  if (lane == 0) s_rmax[warp] = vmax;
+  __syncthreads();
+  if (tid == 0) {
+    uint64_t m = 0ull;
+    for (int w = 0; w < KW; ++w) m = s_rmax[w] > m ? s_rmax[w] : m;
+    atomicMax(reinterpret_cast<unsigned long long*>(&p.hs.max_comp[bh]), static_cast<unsigned long long>(m));
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = atomicAdd(&p.hs.kth_ticket[bh], 1u) == static_cast<unsigned>(P - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+
+  // ---- last CTA of the head: exact threshold
+  uint64_t T;
+  if (all) {
+    T = 1ull;  // every valid (non-zero) candidate
+  } else if (whole) {
+    T = static_cast<uint64_t>(thr + (dstar << shift)) << 32;  // lower bound of bucket d*
+  } else {
+    int cs = 64;
+    uint64_t cp = 0;
+    if (!big) {
+      const int64_t nb = __ldcg(&p.hs.bkt_cnt[bh]);
+      for (int64_t i = tid; i < nb; i += KT) s_bkt[i] = __ldcg(&gbkt[i]);
+      __syncthreads();
+      if (nb <= 2048) {  // typical: a few hundred → rank counting, two barriers
+        __shared__ uint64_t s_res;
+        cp = block_rank_select<KT>(s_bkt, static_cast<int>(nb), static_cast<int>(need), &s_res);
+        cs = 0;
+      } else {
+        auto ld = [&](int64_t i, uint64_t& c) {
+          c = s_bkt[i];
+          return true;
+        };
+        radix_select_u64<KT>(ld, nb, need, s_hist, s_scr, s_out, cs, cp);
+      }
+    } else {
+      // rare: a threshold bucket larger than the buffer (heavy exact ties) — radix passes over
+      // all candidates restricted to bucket d*
+      auto ld = [&](int64_t i, uint64_t& c) {
+        c = __ldcg(&src[i]);
+        return c != 0ull && hist_digit(comp_key(c), thr, shift) == dstar;
+      };
+      radix_select_u64<KT>(ld, n, need, s_hist, s_scr, s_out, cs, cp);
+    }
+    T = cp << cs;
+  }
+  if (tid == 0) {
+    p.meta_kth[bh] = T;
+    p.meta_kb[bh] = static_cast<int32_t>(kb);
+    p.meta_max[bh] = key_score(comp_key(__ldcg(&p.hs.max_comp[bh])));
+    p.hs.kth_ticket[bh] = 0u;
+    p.hs.bkt_cnt[bh] = 0u;
+    if (p.pass == kPassFallback) {
+      p.hs.flag_fail[bh] = 0u;
+      p.hs.group_fail[b * p.Hkv + h / p.G] = 0u;
+    }
+  }
+}
+
+cudaError_t launch_kth(const SelectParams& p, cudaStream_t s) {
+  const int smem = kSelectBucketCap * static_cast<int>(sizeof(uint64_t));
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  kth_kernel<<<dim3(kKthCtas, p.B * p.Hq), kKthThreads, smem, s>>>(p);
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- optional sorted output
