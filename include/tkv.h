@@ -59,6 +59,7 @@ extern "C" {
 /* flags */
 #define TKV_F_SORTED 1u    /* idx/scores ordered score-desc, id-asc (TopKResult order, ann.py:166) */
 #define TKV_F_NO_FILTER 2u /* disable the sampled-threshold pre-filter (emit every score)       */
+#define TKV_F_FUSED 4u     /* run the layer step as one persistent work-queue kernel (fused.cu)   */
 
 typedef struct tkv_problem {
   int32_t batch;         /* B                                                                  */
@@ -154,10 +155,17 @@ int tkv_last_launch_count(void);
 /*
  * Measurement hook: when both events are non-NULL (cudaEvent_t as void*), subsequent compute
  * calls on this thread record `start` / `stop` on their stream immediately before / after the
- * main key-scan kernel launch, so a caller can time the dominant kernel with CUDA events on
- * the stream it runs on. Pass NULLs to disable.
+ * dominant kernel launch (the fused layer-step kernel; with TKV_F_UNFUSED the key-scan kernel),
+ * so a caller can time it with CUDA events on the stream it runs on. Pass NULLs to disable.
  */
 int tkv_profile_scan_events(void* start, void* stop);
+
+/*
+ * Measurement hook: with a non-NULL device buffer of n_items × 4 uint64, the fused layer-step
+ * kernel records, per work item index i < n_items, {start ns, end ns, type << 32 | cta,
+ * a << 32 | b} (%globaltimer). NULL disables. Diagnostic only.
+ */
+int tkv_debug_trace(void* buf, uint32_t n_items);
 
 #ifdef __cplusplus
 }

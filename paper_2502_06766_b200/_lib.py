@@ -31,12 +31,14 @@ EXPORTS = (
     "tkv_shard_finalize",
     "tkv_last_launch_count",
     "tkv_profile_scan_events",
+    "tkv_debug_trace",
 )
 
 COMBINE_JOINT = 0
 COMBINE_ADDITIVE = 1
 F_SORTED = 1
 F_NO_FILTER = 2
+F_FUSED = 4
 
 
 class Problem(ctypes.Structure):
@@ -69,6 +71,7 @@ _SIG = {
     "tkv_device_check": ([], _I),
     "tkv_last_launch_count": ([], _I),
     "tkv_profile_scan_events": ([_P, _P], _I),
+    "tkv_debug_trace": ([_P, ctypes.c_uint32], _I),
     "tkv_workspace_bytes": ([ctypes.POINTER(Problem), ctypes.POINTER(ctypes.c_size_t)], _I),
     "tkv_workspace_init": ([ctypes.POINTER(Problem), _P, ctypes.c_size_t, _P], _I),
     "tkv_topk_decode_attention": (

@@ -41,15 +41,16 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > t for p in deps if p.exists())
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: Path | None = None) -> Path:
+    lib = Path(out) if out else LIB
+    if not force and not _stale() and out is None:
         return LIB
     OUT_DIR.mkdir(parents=True, exist_ok=True)
     objs = []
     flags = ARCH + [
         "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
         "-I", str(ROOT / "include"), "-Xptxas", "-v" if verbose else "-O3",
-    ]
+    ] + os.environ.get("TKV_NVCC_FLAGS", "").split()
     for src in sources():
         obj = OUT_DIR / (src.stem + ".o")
         cmd = [nvcc(), "-c", str(src), "-o", str(obj)] + flags
@@ -64,10 +65,10 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     for o in objs:
         os.unlink(o)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

@@ -7,6 +7,7 @@
 // inspected here — that would cost a host synchronisation or a full scan.
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -21,6 +22,8 @@ namespace {
 thread_local std::string g_err;
 thread_local int g_launches = 0;
 thread_local cudaEvent_t g_scan_start = nullptr, g_scan_stop = nullptr;
+thread_local uint64_t* g_trace = nullptr;
+thread_local uint32_t g_trace_cap = 0;
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -42,7 +45,7 @@ int fail(int code, const char* fmt, ...) {
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct Layout {
-  size_t ticket_g, ticket_k, flag, gflag, ctrl_end;
+  size_t ticket_g, ticket_k, flag, gflag, fctl, ctrl_end;
   size_t maxc, bktc, bkt, outc;
   size_t cnt, thr, hshift, hist, mmax, mkth, mkb, samp, cand, sidx, sscore, pl, po, total;
   int64_t cap;
@@ -63,6 +66,7 @@ Layout make_layout(const tkv_problem* p) {
   L.ticket_k = take(BH * 4);
   L.flag = take(BH * 4);
   L.gflag = take(BK * 4);
+  L.fctl = take(static_cast<size_t>(fused_ctl_words(static_cast<int>(BK), static_cast<int>(BH))) * 4);
   L.ctrl_end = off;
   L.cnt = take(BH * 4);
   L.thr = take(BH * 4);
@@ -282,6 +286,60 @@ int run_emit(const tkv_problem* p, const void* q, const void* k_cache, const voi
   return TKV_OK;
 }
 
+// The whole layer step: the multi-kernel pipeline (default) or, with TKV_F_FUSED, the fused
+// persistent work-queue kernel (fused.cu).
+int run_layer(const tkv_problem* p, const void* q, const void* k_cache, const void* v_cache,
+              const int32_t* n_ctx, const int32_t* n_win, int32_t* idx, float* scores,
+              uint64_t* packed, float* out, int gather, void* ws, const Layout& L, cudaStream_t st) {
+  if (!(p->flags & TKV_F_FUSED)) {
+    TRY(run_select(p, q, k_cache, n_ctx, ws, L, st));
+    return run_emit(p, q, k_cache, v_cache, n_ctx, n_win, idx, scores, packed, out, gather, ws, L, st);
+  }
+  FusedParams f{};
+  f.a = make_attend(p, q, k_cache, v_cache, n_ctx, n_win, idx, scores, ws, L);
+  f.a.idx_out = idx;
+  f.a.scores_out = scores;
+  f.a.packed_out = packed;
+  f.a.out = out;
+  f.a.gather = gather;
+  f.a.partial_only = 0;
+  f.hs = head_state(ws, L);
+  f.samp = at<uint32_t>(ws, L.samp);
+  f.ctl = at<uint32_t>(ws, L.fctl);
+  f.max_ctx = p->max_ctx;
+  f.no_filter = (p->flags & TKV_F_NO_FILTER) ? 1 : 0;
+  f.NS = f.no_filter ? 0 : kSamples / kSampleThreads;
+  const int NG = p->batch * p->n_kv_heads, NH = p->batch * p->n_q_heads;
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = 2 * sms;
+  // tile size: 1024 rows per scan item when there are enough items to balance, else smaller
+  static const int tile_env = [] {
+    const char* e = getenv("TKV_TILE_ITERS");
+    return e ? atoi(e) : 0;
+  }();
+  f.tile_iters = tile_env > 0 ? tile_env : 8;
+  while (tile_env <= 0 && f.tile_iters > 1 &&
+         static_cast<int64_t>(NG) * ((p->max_ctx + f.tile_iters * kScanRows - 1) / (f.tile_iters * kScanRows)) <
+             4LL * grid)
+    f.tile_iters >>= 1;
+  f.T = static_cast<int>((p->max_ctx + f.tile_iters * kScanRows - 1) / (f.tile_iters * kScanRows));
+  f.KS = kFusedKS;
+  int ka = (2 * grid + NH - 1) / NH;
+  f.KA = ka < 1 ? 1 : (ka > 16 ? 16 : ka);
+  f.trace = g_trace;
+  f.trace_cap = g_trace_cap;
+  if (g_scan_start && g_scan_stop) cudaEventRecord(g_scan_start, st);
+  TKV_LAUNCH(launch_fused(f, st));
+  if (g_scan_start && g_scan_stop) cudaEventRecord(g_scan_stop, st);
+  if (p->flags & TKV_F_SORTED) {
+    SortParams so{idx, scores, at<int32_t>(ws, L.mkb), p->k};
+    TKV_LAUNCH(launch_sort(so, p->batch * p->n_q_heads, st));
+  }
+  return TKV_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -291,6 +349,12 @@ int tkv_version(void) { return TKV_VERSION; }
 const char* tkv_last_error(void) { return g_err.c_str(); }
 
 int tkv_last_launch_count(void) { return g_launches; }
+
+int tkv_debug_trace(void* buf, uint32_t n_items) {
+  g_trace = static_cast<uint64_t*>(buf);
+  g_trace_cap = buf ? n_items : 0u;
+  return TKV_OK;
+}
 
 int tkv_profile_scan_events(void* start, void* stop) {
   g_scan_start = static_cast<cudaEvent_t>(start);
@@ -346,8 +410,7 @@ int tkv_topk_decode_attention(const tkv_problem* p, const void* q, const void* k
   if (n_win) TRY(check_ptr(n_win, "n_win", 4));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   float* sc = scores ? scores : at<float>(ws, L.sscore);
-  TRY(run_select(p, q, k_cache, n_ctx, ws, L, st));
-  return run_emit(p, q, k_cache, v_cache, n_ctx, n_win, idx, sc, nullptr, out, 1, ws, L, st);
+  return run_layer(p, q, k_cache, v_cache, n_ctx, n_win, idx, sc, nullptr, out, 1, ws, L, st);
 }
 
 int tkv_topk_search(const tkv_problem* p, const void* q, const void* k_cache, const int32_t* n_ctx,
@@ -362,8 +425,7 @@ int tkv_topk_search(const tkv_problem* p, const void* q, const void* k_cache, co
   TRY(check_ptr(idx, "idx", 4));
   float* sc = scores ? scores : at<float>(ws, L.sscore);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  TRY(run_select(p, q, k_cache, n_ctx, ws, L, st));
-  return run_emit(p, q, k_cache, k_cache, n_ctx, nullptr, idx, sc, nullptr, nullptr, 0, ws, L, st);
+  return run_layer(p, q, k_cache, k_cache, n_ctx, nullptr, idx, sc, nullptr, nullptr, 0, ws, L, st);
 }
 
 int tkv_kv_append(int32_t batch, int32_t n_kv_heads, int32_t head_dim, int64_t cache_rows,
@@ -405,10 +467,9 @@ int tkv_shard_candidates(const tkv_problem* p, const void* q, const void* k_cach
   TRY(check_ptr(n_ctx, "n_ctx", 4));
   TRY(check_ptr(cand, "cand", 8));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  TRY(run_select(p, q, k_cache, n_ctx, ws, L, st));
   tkv_problem pu = *p;
   pu.flags &= ~TKV_F_SORTED;
-  return run_emit(&pu, q, k_cache, k_cache, n_ctx, nullptr, at<int32_t>(ws, L.sidx), at<float>(ws, L.sscore),
+  return run_layer(&pu, q, k_cache, k_cache, n_ctx, nullptr, at<int32_t>(ws, L.sidx), at<float>(ws, L.sscore),
                   cand, nullptr, 0, ws, L, st);
 }
 

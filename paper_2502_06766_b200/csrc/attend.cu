@@ -17,220 +17,10 @@
 // writes out[b, h, :].
 #include <math.h>
 
-#include "common.cuh"
-#include "internal.h"
+#include "attend_dev.cuh"
 
 namespace tkv {
 
-namespace {
-constexpr int NT = kAttendThreads;
-constexpr int NW = NT / 32;
-
-// Online softmax accumulation over local rows [r_begin, r_end) of kv head (b, kvh) for q head
-// h. State (m, l, o) in the log2-scaled domain; thread t accumulates o for d = t % 128 over rows
-// of parity t / 128. With `pinned`, a row is skipped when it is among the selected top-k
-// (composite >= kth).
-__device__ void accumulate_rows(const AttendParams& p, int b, int h, int kvh, int64_t r_begin,
-                                int64_t r_end, bool pinned, uint64_t kth, float& m, float& l,
-                                float& o, float* s_z, float* s_scr) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, c = lane & 3;
-  const int n = h - kvh * p.G;
-  const float zs = p.scale * kLog2e;
-  QFrag f;
-  load_qfrag(f, p.q + (static_cast<int64_t>(b) * p.Hq + kvh * p.G) * kD, p.G, lane);
-  const int64_t head_off = (static_cast<int64_t>(b) * p.Hkv + kvh) * p.cache_rows * kD;
-  const __nv_bfloat16* kb = p.kc + head_off;
-  const __nv_bfloat16* vb = p.vc + head_off;
-  const int d = tid & (kD - 1), par = tid >> 7;
-  for (int64_t base = r_begin; base < r_end; base += 8 * 16) {
-    {
-      const int64_t rA = base + warp * 16 + g, rB = rA + 8;
-      uint4 a[2][4];
-      load_tile(a, kb + rA * kD, rA < r_end, kb + rB * kD, rB < r_end, c);
-      float acc[4];
-      score_tile(acc, a, f);
-      if (c == (n >> 1)) {
-        const float sA = acc[n & 1], sB = acc[2 + (n & 1)];
-        bool okA = rA < r_end, okB = rB < r_end;
-        if (pinned) {
-          okA = okA && make_comp(score_key(sA), static_cast<uint32_t>(p.row_offset + rA)) < kth;
-          okB = okB && make_comp(score_key(sB), static_cast<uint32_t>(p.row_offset + rB)) < kth;
-        }
-        s_z[warp * 16 + g] = okA ? sA * zs : -INFINITY;
-        s_z[warp * 16 + g + 8] = okB ? sB * zs : -INFINITY;
-      }
-    }
-    __syncthreads();
-    float v = tid < 128 ? s_z[tid] : -INFINITY;
-    v = warp_max(v);
-    if (lane == 0) s_scr[warp] = v;
-    __syncthreads();
-    float cm = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) cm = fmaxf(cm, s_scr[w]);
-    const float mn = fmaxf(m, cm);
-    if (mn != -INFINITY) {
-      const float fold = (m == -INFINITY) ? 0.f : exp2f(m - mn);
-      float lsum = 0.f, osum = 0.f;
-      for (int r = 0; r < 128; ++r) {
-        const float z = s_z[r];
-        if (z == -INFINITY) continue;
-        const float w = exp2f(z - mn);
-        lsum += w;
-        if ((r & 1) == par) osum += w * __bfloat162float(vb[(base + r) * kD + d]);
-      }
-      l = l * fold + lsum;
-      o = o * fold + osum;
-      m = mn;
-    }
-    __syncthreads();
-  }
-}
-
-// Pinned-prefix rows [0, p) that the top-k did not select join the context softmax
-// (attention.py:152-154 unions them into the retrieved ids). Local rows of this shard only.
-__device__ void add_pinned(const AttendParams& p, int b, int h, int kvh, int64_t nctx, int kb,
-                           float zref, float& l, float& o, float* s_z, float* s_scr) {
-  if (p.pinned <= 0 || kb <= 0) return;
-  int64_t lo = -p.row_offset;
-  if (lo < 0) lo = 0;
-  int64_t hi = static_cast<int64_t>(p.pinned) - p.row_offset;
-  if (hi > nctx) hi = nctx;
-  if (hi <= lo) return;
-  const int bh = b * p.Hq + h;
-  float m = zref;
-  accumulate_rows(p, b, h, kvh, lo, hi, true, p.meta_kth[bh], m, l, o, s_z, s_scr);
-  // every unselected row scores <= the k-th selected score <= M, so m stays zref
-}
-
-// Window rows + normalisation. Inputs: context state (zref, l_c, o_c) where o_c is this
-// thread's share (d = tid % 128, parity tid / 128). Writes out[bh, :].
-__device__ void finalize_head(const AttendParams& p, int b, int h, int kvh, int64_t nctx, float zref,
-                              float l_c, float o_c, float* s_z, float* s_scr, float* s_o) {
-  const int tid = threadIdx.x;
-  const int bh = b * p.Hq + h;
-  const int64_t nwin = p.n_win ? p.n_win[b] : 0;
-  float m_w = -INFINITY, l_w = 0.f, o_w = 0.f;
-  if (nwin > 0) accumulate_rows(p, b, h, kvh, nctx, nctx + nwin, false, 0ull, m_w, l_w, o_w, s_z, s_scr);
-  float val;
-  if (p.combine == 0) {  // joint (attention.py:109-114)
-    const float mm = fmaxf(l_c > 0.f ? zref : -INFINITY, m_w);
-    const float fc = (l_c > 0.f) ? exp2f(zref - mm) : 0.f;
-    const float fw = (l_w > 0.f) ? exp2f(m_w - mm) : 0.f;
-    const float L = l_c * fc + l_w * fw;
-    val = L > 0.f ? (o_c * fc + o_w * fw) / L : 0.f;
-  } else {  // additive (attention.py:115-121)
-    val = (l_c > 0.f ? o_c / l_c : 0.f) + (l_w > 0.f ? o_w / l_w : 0.f);
-  }
-  s_o[tid] = val;
-  __syncthreads();
-  if (tid < kD) p.out[static_cast<int64_t>(bh) * kD + tid] = s_o[tid] + s_o[tid + kD];
-}
-
-struct AttSmem {
-  float w[kCandChunk];
-  int32_t row[kCandChunk];
-  float red[NW][kD];
-  float l[NW];
-  float z[128];
-  float scr[32];
-  float o[NT];
-  uint32_t wcnt[NW];
-  uint32_t base;
-  int last;
-};
-
-// Gather the V rows listed in sm.row (local rows, -1 = skip) weighted by sm.w, reduce into the
-// head's partial slot, and let the last CTA of the head (atomic ticket over nslots) combine
-// the partials in slot order (deterministic), add the pinned-prefix rows and the window, and
-// write out (or the (l, o) partial in sharded mode).
-__device__ void chunk_body(const AttendParams& p, int bh, int slot, int nslots, int nrows, AttSmem& sm) {
-  const int b = bh / p.Hq, h = bh % p.Hq, kvh = h / p.G;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int half = lane >> 4, part = lane & 15;
-  const __nv_bfloat16* vb =
-      p.vc + (static_cast<int64_t>(b) * p.Hkv + kvh) * p.cache_rows * kD + part * 8;
-  float acc[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) acc[j] = 0.f;
-  constexpr int UNR = 8;
-  for (int r0 = warp * 2 + half; r0 < nrows; r0 += 2 * NW * UNR) {
-    uint4 v[UNR];
-    float w[UNR];
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      const int r = r0 + 2 * NW * u;
-      const int row = r < nrows ? sm.row[r] : -1;
-      w[u] = r < nrows ? sm.w[r] : 0.f;
-      v[u] = row >= 0 ? ldg_nc(vb + static_cast<int64_t>(row) * kD) : make_uint4(0, 0, 0, 0);
-    }
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      acc[0] = fmaf(w[u], bf16lo(v[u].x), acc[0]);
-      acc[1] = fmaf(w[u], bf16hi(v[u].x), acc[1]);
-      acc[2] = fmaf(w[u], bf16lo(v[u].y), acc[2]);
-      acc[3] = fmaf(w[u], bf16hi(v[u].y), acc[3]);
-      acc[4] = fmaf(w[u], bf16lo(v[u].z), acc[4]);
-      acc[5] = fmaf(w[u], bf16hi(v[u].z), acc[5]);
-      acc[6] = fmaf(w[u], bf16lo(v[u].w), acc[6]);
-      acc[7] = fmaf(w[u], bf16hi(v[u].w), acc[7]);
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < 8; ++j) acc[j] += __shfl_xor_sync(kFull, acc[j], 16);
-  if (half == 0) {
-#pragma unroll
-    for (int j = 0; j < 8; ++j) sm.red[warp][part * 8 + j] = acc[j];
-  }
-  float lw = 0.f;
-  for (int i = tid; i < nrows; i += NT) lw += sm.w[i];
-  lw = warp_sum(lw);
-  if (lane == 0) sm.l[warp] = lw;
-  __syncthreads();
-  if (tid < kD) {
-    float o = 0.f;
-#pragma unroll
-    for (int w2 = 0; w2 < NW; ++w2) o += sm.red[w2][tid];
-    p.part_o[(static_cast<int64_t>(bh) * p.nchunks + slot) * kD + tid] = o;
-  }
-  if (tid == 0) {
-    float l = 0.f;
-#pragma unroll
-    for (int w2 = 0; w2 < NW; ++w2) l += sm.l[w2];
-    p.part_l[static_cast<int64_t>(bh) * p.nchunks + slot] = l;
-  }
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) sm.last = (atomicAdd(&p.ticket[bh], 1u) == static_cast<unsigned>(nslots - 1));
-  __syncthreads();
-  if (!sm.last) return;
-  __threadfence();
-
-  // ---- last CTA of this head: deterministic slot-order combine
-  const int kb = p.meta_kb[bh];
-  const float zref = kb > 0 ? p.meta_max[bh] * p.scale * kLog2e : 0.f;
-  const int64_t nctx = p.n_ctx[b];
-  float o_c = 0.f, l_c = 0.f;
-  for (int c2 = 0; c2 < nslots; ++c2) {
-    if (tid < kD) o_c += __ldcg(&p.part_o[(static_cast<int64_t>(bh) * p.nchunks + c2) * kD + tid]);
-    l_c += __ldcg(&p.part_l[static_cast<int64_t>(bh) * p.nchunks + c2]);
-  }
-  if (tid == 0) p.ticket[bh] = 0u;
-  add_pinned(p, b, h, kvh, nctx, kb, zref, l_c, o_c, sm.z, sm.scr);
-  if (p.partial_only) {
-    sm.o[tid] = o_c;
-    __syncthreads();
-    float* dst = p.partial_out + static_cast<int64_t>(bh) * (kD + 1);
-    if (tid == 0) dst[0] = l_c;
-    if (tid < kD) dst[1 + tid] = sm.o[tid] + sm.o[tid + kD];
-    __syncthreads();
-    return;
-  }
-  finalize_head(p, b, h, kvh, nctx, zref, l_c, o_c, sm.z, sm.scr, sm.o);
-  __syncthreads();
-}
-}  // namespace
 
 // List mode (sharded partial): the selected (idx, score) list is given.
 __global__ void __launch_bounds__(NT) attend_kernel(AttendParams p) {

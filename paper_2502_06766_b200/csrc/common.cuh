@@ -274,4 +274,41 @@ __device__ __forceinline__ void find_bucket(const uint32_t* hist, uint32_t need,
   __syncthreads();
 }
 
+// ---------------------------------------------------------------- generic radix select
+// Radix select of the `need` largest composites among the elements accepted by `load`
+// (load(i, c) -> bool), MSB first with 8-bit digits. Result: selected ⇔ (c >> shift) >= prefix.
+template <int T, typename Load>
+__device__ void radix_select_u64(Load load, int64_t n, uint32_t need, uint32_t* hist, uint32_t* scr,
+                                 uint32_t* out, int& shift_out, uint64_t& prefix_out) {
+  int shift = 64;
+  uint64_t prefix = 0;
+  while (shift > 0) {
+    const int nshift = shift - 8;
+    for (int i = threadIdx.x; i < 256; i += T) hist[i] = 0u;
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < n; i += T) {
+      uint64_t c;
+      if (load(i, c) && (shift == 64 || (c >> shift) == prefix))
+        hist_add_aggregated(hist, static_cast<uint32_t>(c >> nshift) & 255u);
+    }
+    __syncthreads();
+    find_bucket<T, 256>(hist, need, out, scr);
+    const uint32_t d = out[0];
+    need -= out[1];
+    prefix = (prefix << 8) | d;
+    shift = nshift;
+    const bool done = hist[d] == need;
+    __syncthreads();
+    if (done) break;
+  }
+  shift_out = shift;
+  prefix_out = prefix;
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
 }  // namespace tkv

@@ -140,6 +140,27 @@ struct AppendParams {
   int advance;
 };
 
+// Fused persistent layer-step kernel (fused.cu): `a` carries the problem, the caches, the
+// outputs and the attention workspace; the rest is the selection state and the schedule.
+struct FusedParams {
+  AttendParams a;
+  HeadState hs;
+  uint32_t* samp;  // [B*Hq*kSamples]
+  uint32_t* ctl;   // control block (zero at launch; the last CTA to exit re-zeroes it)
+  int64_t max_ctx;
+  int no_filter;
+  int NS;          // sample items per (b, kv head)
+  int T;           // scan tiles per (b, kv head)
+  int tile_iters;  // 256-row iterations per scan tile
+  int KS;          // k-th slices per head
+  int KA;          // attend items per head
+  uint64_t* trace;  // optional per-item timeline (tkv_debug_trace): [n][4] = t0, t1, type|cta, item
+  uint32_t trace_cap;
+};
+constexpr int kFusedKS = 4;
+__host__ __device__ inline int fused_ctl_words(int NG, int NH) { return 8 + 2 * NG + 5 * NH; }
+
+cudaError_t launch_fused(const FusedParams& p, cudaStream_t s);
 cudaError_t launch_sample(const SampleParams& p, cudaStream_t s);
 cudaError_t launch_scan(const ScanParams& p, cudaStream_t s);
 cudaError_t launch_select(const SelectParams& p, cudaStream_t s);
