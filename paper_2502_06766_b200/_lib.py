@@ -8,12 +8,15 @@ DeviceError (the product path never silently runs anything else).
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
 from .errors import DeviceError, raise_for_status
 
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libtkv.so"
+if os.environ.get("TKV_LIB_PATH"):  # A/B experiments with an alternative build
+    LIB_PATH = Path(os.environ["TKV_LIB_PATH"]).resolve()
 
 # symbols the header declares (checked by tests/test_boundary.py against include/tkv.h)
 EXPORTS = (

@@ -20,6 +20,7 @@ CSRC = PKG / "csrc"
 OUT_DIR = PKG / "_lib"
 LIB = OUT_DIR / "libtkv.so"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+RDC_SOURCES = {"select.cu"}
 
 
 def nvcc() -> str:
@@ -41,7 +42,7 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > t for p in deps if p.exists())
 
 
-def build(force: bool = False, verbose: bool = False, out: Path | None = None) -> Path:
+def build(force: bool = False, verbose: bool = False, out: Path | None = None, rdc: bool = True) -> Path:
     lib = Path(out) if out else LIB
     if not force and not _stale() and out is None:
         return LIB
@@ -50,18 +51,32 @@ def build(force: bool = False, verbose: bool = False, out: Path | None = None) -
     flags = ARCH + [
         "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
         "-I", str(ROOT / "include"), "-Xptxas", "-v" if verbose else "-O3",
-    ] + os.environ.get("TKV_NVCC_FLAGS", "").split()
+    ] + ([] if rdc else ["-DTKV_NO_CDP"]) + os.environ.get("TKV_NVCC_FLAGS", "").split()
+    rdc_objs = []
     for src in sources():
         obj = OUT_DIR / (src.stem + ".o")
-        cmd = [nvcc(), "-c", str(src), "-o", str(obj)] + flags
+        # only select.cu (k-th kernel + tail-launched fallback) needs relocatable device code;
+        # the hot kernels stay whole-program compiled
+        extra = ["-rdc=true"] if (rdc and src.name in RDC_SOURCES) else []
+        if extra:
+            rdc_objs.append(str(obj))
+        cmd = [nvcc(), "-c", str(src), "-o", str(obj)] + flags + extra
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src.name}:\n{r.stdout}\n{r.stderr}")
         if verbose and r.stderr:
             print(r.stderr, file=sys.stderr)
         objs.append(str(obj))
+    if rdc:
+        # device link: the k-th kernel tail-launches the exactness fallback (dynamic parallelism)
+        dlink = OUT_DIR / "dlink.o"
+        cmd = [nvcc(), "-dlink", "-o", str(dlink)] + rdc_objs + ARCH + ["-Xcompiler", "-fPIC", "-lcudadevrt"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc device link failed:\n{r.stdout}\n{r.stderr}")
+        objs.append(str(dlink))
     tmp = OUT_DIR / "libtkv.so.tmp"
-    cmd = [nvcc(), "-shared", "-o", str(tmp)] + objs + ARCH + ["-lcudart"]
+    cmd = [nvcc(), "-shared", "-o", str(tmp)] + objs + ARCH + ["-lcudadevrt", "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc link failed:\n{r.stdout}\n{r.stderr}")

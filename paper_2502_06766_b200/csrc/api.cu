@@ -45,7 +45,7 @@ int fail(int code, const char* fmt, ...) {
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct Layout {
-  size_t ticket_g, ticket_k, flag, gflag, fctl, ctrl_end;
+  size_t ticket_g, ticket_k, flag, gflag, fctl, fbl, ctrl_end;
   size_t maxc, bktc, bkt, outc;
   size_t cnt, thr, hshift, hist, mmax, mkth, mkb, samp, cand, sidx, sscore, pl, po, total;
   int64_t cap;
@@ -67,6 +67,7 @@ Layout make_layout(const tkv_problem* p) {
   L.flag = take(BH * 4);
   L.gflag = take(BK * 4);
   L.fctl = take(static_cast<size_t>(fused_ctl_words(static_cast<int>(BK), static_cast<int>(BH))) * 4);
+  L.fbl = take(4);
   L.ctrl_end = off;
   L.cnt = take(BH * 4);
   L.thr = take(BH * 4);
@@ -163,6 +164,7 @@ HeadState head_state(void* ws, const Layout& L) {
   hs.bkt = at<uint64_t>(ws, L.bkt);
   hs.kth_ticket = at<uint32_t>(ws, L.ticket_k);
   hs.out_cnt = at<uint32_t>(ws, L.outc);
+  hs.fb_launched = at<uint32_t>(ws, L.fbl);
   return hs;
 }
 
@@ -221,12 +223,11 @@ int run_select(const tkv_problem* p, const void* q, const void* k_cache, const i
   sl.meta_kb = at<int32_t>(ws, L.mkb);
   sl.hs = hs;
   sl.pass = kPassMain;
-  TKV_LAUNCH(launch_kth(sl, st));
-
-  // exactness fallback: heads whose sampled threshold let fewer than k rows through
+  // exactness fallback (heads whose sampled threshold let fewer than k rows through): the
+  // k-th kernel tail-launches a re-scan with threshold 0 and a fallback k-th pass on device
   cp.fallback = 1;
-  TKV_LAUNCH(launch_scan(cp, st));
-  sl.pass = kPassFallback;
+  sl.fb_scan = cp;
+  scan_launch_shape(cp, &sl.fb_scan_grid, &sl.fb_scan_smem);
   TKV_LAUNCH(launch_kth(sl, st));
   return TKV_OK;
 }

@@ -38,6 +38,7 @@ struct HeadState {
   uint64_t* bkt;         // [B*Hq][kSelectBucketCap] threshold-bucket candidates
   uint32_t* kth_ticket;  // [B*Hq] kth_kernel CTAs done (self-resetting)
   uint32_t* out_cnt;     // [B*Hq] selected rows written so far (reset by threshold_kernel)
+  uint32_t* fb_launched; // [1] the exactness fallback has been tail-launched for this call
 };
 
 struct SampleParams {
@@ -82,7 +83,14 @@ struct SelectParams {
   HeadState hs;
   uint64_t* packed_out;  // optional [B*Hq*k] composites (shard candidates)
   int pass;
+  // exactness fallback, tail-launched by kth_kernel (main pass) when a head failed
+  ScanParams fb_scan;
+  int fb_scan_grid;
+  int fb_scan_smem;
 };
+
+// host-side preparation of the device-tail-launched fallback kernels (select.cu)
+void prepare_fallback_kernels();
 
 struct SortParams {
   int32_t* idx;
@@ -163,6 +171,7 @@ __host__ __device__ inline int fused_ctl_words(int NG, int NH) { return 8 + 2 * 
 cudaError_t launch_fused(const FusedParams& p, cudaStream_t s);
 cudaError_t launch_sample(const SampleParams& p, cudaStream_t s);
 cudaError_t launch_scan(const ScanParams& p, cudaStream_t s);
+void scan_launch_shape(const ScanParams& p, int* grid, int* smem_bytes);
 cudaError_t launch_select(const SelectParams& p, cudaStream_t s);
 cudaError_t launch_kth(const SelectParams& p, cudaStream_t s);
 cudaError_t launch_attend_cand(const AttendParams& p, cudaStream_t s);

@@ -21,8 +21,7 @@
 // candidates gathered from every shard; histogram built here from the candidates' range).
 #include <math.h>
 
-#include "common.cuh"
-#include "internal.h"
+#include "scan_dev.cuh"
 
 namespace tkv {
 
@@ -60,7 +59,7 @@ __device__ __forceinline__ void emit_sel(bool sel, uint64_t c, uint32_t* counter
 
 __global__ void __launch_bounds__(NT) select_kernel(SelectParams p) {
   extern __shared__ uint64_t s_bkt[];  // [kSelectBucketCap]
-  __shared__ uint32_t s_hist[kHistBins];
+  __shared__ __align__(16) uint32_t s_hist[kHistBins];
   __shared__ uint32_t s_scr[32];
   __shared__ uint32_t s_out[2];
   __shared__ uint32_t s_nout, s_nbkt, s_nvalid;
@@ -302,6 +301,17 @@ __global__ void __launch_bounds__(NT) select_kernel(SelectParams p) {
   }
 }
 
+// ---------------------------------------------------------------- exactness fallback scan
+// Same loop as scan.cu's scan_kernel; this translation unit is compiled with -rdc=true so the
+// k-th kernel can tail-launch it (the hot scan_kernel stays whole-program compiled).
+#ifndef TKV_NO_CDP
+__global__ void __launch_bounds__(kScanWarps * 32, 2) fb_scan_kernel(ScanParams p) {
+  extern __shared__ uint64_t s_buf[];  // [G][kScanStage]
+  __shared__ uint32_t s_cnt[8];
+  scan_body(p, s_buf, s_cnt);
+}
+#endif
+
 // ---------------------------------------------------------------- k-th threshold only
 // kth_kernel: grid (kKthCtas, B*Hq). Finds the composite threshold T of each head such that
 // { c >= T } is exactly the top-kb candidate set, without writing the set itself (the
@@ -313,7 +323,7 @@ __global__ void __launch_bounds__(NT) select_kernel(SelectParams p) {
 __global__ void __launch_bounds__(kKthThreads) kth_kernel(SelectParams p) {
   constexpr int KT = kKthThreads, KW = KT / 32;
   extern __shared__ uint64_t s_bkt[];  // [kSelectBucketCap]
-  __shared__ uint32_t s_hist[kHistBins];
+  __shared__ __align__(16) uint32_t s_hist[kHistBins];
   __shared__ uint32_t s_scr[32];
   __shared__ uint32_t s_out[2];
   __shared__ uint64_t s_rmax[KW];
@@ -341,6 +351,20 @@ __global__ void __launch_bounds__(kKthThreads) kth_kernel(SelectParams p) {
         p.hs.cand_cnt[bh] = 0u;
         p.hs.thr[bh] = 0u;
         p.hs.hshift[bh] = kNoFilterShift;
+        __threadfence();
+        // First failing head of this call: tail-launch the exact re-scan and its k-th pass.
+        // Tail launches start when this grid (and so every other head's flagging) is done, and
+        // the next kernel of the caller's stream waits for them — no host round trip, and no
+        // cost at all when no head fails.
+#ifndef TKV_NO_CDP
+        if (atomicExch(p.hs.fb_launched, 1u) == 0u) {
+          fb_scan_kernel<<<p.fb_scan_grid, kScanWarps * 32, p.fb_scan_smem, cudaStreamTailLaunch>>>(p.fb_scan);
+          SelectParams f = p;
+          f.pass = kPassFallback;
+          kth_kernel<<<dim3(kKthCtas, p.B * p.Hq), kKthThreads,
+                       kSelectBucketCap * static_cast<int>(sizeof(uint64_t)), cudaStreamTailLaunch>>>(f);
+        }
+#endif
       }
     }
     return;
@@ -353,6 +377,7 @@ __global__ void __launch_bounds__(kKthThreads) kth_kernel(SelectParams p) {
       if (p.pass == kPassFallback) {
         p.hs.flag_fail[bh] = 0u;
         p.hs.group_fail[b * p.Hkv + h / p.G] = 0u;
+        *p.hs.fb_launched = 0u;
       }
     }
     return;
@@ -463,11 +488,24 @@ __global__ void __launch_bounds__(kKthThreads) kth_kernel(SelectParams p) {
     if (p.pass == kPassFallback) {
       p.hs.flag_fail[bh] = 0u;
       p.hs.group_fail[b * p.Hkv + h / p.G] = 0u;
+      *p.hs.fb_launched = 0u;
     }
   }
 }
 
+void prepare_fallback_kernels() {
+#ifndef TKV_NO_CDP
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute(fb_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         8 * kScanStage * static_cast<int>(sizeof(uint64_t)));
+    done = true;
+  }
+#endif
+}
+
 cudaError_t launch_kth(const SelectParams& p, cudaStream_t s) {
+  prepare_fallback_kernels();
   const int smem = kSelectBucketCap * static_cast<int>(sizeof(uint64_t));
   static bool attr = false;
   if (!attr) {
