@@ -6,7 +6,9 @@ the reference's GenWindow, attention.py:76-104), the libtkv workspace, and pinne
 staging buffers. `step(q, k_new, v_new)` mirrors one layer of `decode_step`
 (attention.py:203-230): append the token's k/v to the window (attention.py:210), then top-k
 attention for every q head. With host tensors it is the end-to-end path: q/k/v are copied
-host→device, results device→host, all stream-ordered without extra synchronisation.
+host→device and the output device→host; the whole device part of a step (copies, KV append,
+the attention kernels) is captured once into a CUDA graph and replayed, so a step costs one
+graph launch plus the host copies.
 """
 
 from __future__ import annotations
@@ -20,7 +22,8 @@ from .errors import InputError, ShapeError
 class TopkDecoder:
     def __init__(self, k_cache: torch.Tensor, v_cache: torch.Tensor, n_ctx, k: int, *,
                  n_win=0, scale: float | None = None, combine: str = "joint",
-                 pinned_prefix: int = 0, sorted: bool = False, max_ctx: int | None = None):
+                 pinned_prefix: int = 0, sorted: bool = False, max_ctx: int | None = None,
+                 fused: bool = False, use_graph: bool = True):
         if k < 1:
             raise InputError("k must be >= 1")
         ops._check_cuda_bf16("k_cache", k_cache, 4)
@@ -35,11 +38,13 @@ class TopkDecoder:
         self.max_ctx = int(max_ctx if max_ctx is not None else self.rows)
         self.k = k
         self.kw = dict(scale=scale, combine=combine, pinned_prefix=pinned_prefix, sorted=sorted,
-                       max_ctx=self.max_ctx)
+                       max_ctx=self.max_ctx, fused=fused)
         ops.combine_code(combine)
+        self.use_graph = use_graph
         self.Hq = None
         self._bufs = None
         self.ws = None
+        self._graphs: dict[tuple, torch.cuda.CUDAGraph] = {}
 
     def _ensure(self, Hq: int) -> None:
         if self.Hq == Hq:
@@ -50,20 +55,27 @@ class TopkDecoder:
         dev = self.device
         prob = ops.make_problem(self.B, Hq, self.Hkv, self.rows, self.max_ctx, self.k,
                                 pinned_prefix=self.kw["pinned_prefix"], scale=self.kw["scale"],
-                                combine=self.kw["combine"], sorted=self.kw["sorted"])
+                                combine=self.kw["combine"], sorted=self.kw["sorted"],
+                                fused=self.kw["fused"])
         self.ws = ops.Workspace(prob, dev)
         D = ops.HEAD_DIM
+        bf, f32, i32 = torch.bfloat16, torch.float32, torch.int32
         self._bufs = dict(
-            q=torch.empty((self.B, Hq, D), dtype=torch.bfloat16, device=dev),
-            k_new=torch.empty((self.B, self.Hkv, D), dtype=torch.bfloat16, device=dev),
-            v_new=torch.empty((self.B, self.Hkv, D), dtype=torch.bfloat16, device=dev),
-            out=torch.empty((self.B, Hq, D), dtype=torch.float32, device=dev),
-            idx=torch.empty((self.B, Hq, self.k), dtype=torch.int32, device=dev),
-            scores=torch.empty((self.B, Hq, self.k), dtype=torch.float32, device=dev),
-            out_h=torch.empty((self.B, Hq, D), dtype=torch.float32, pin_memory=True),
-            idx_h=torch.empty((self.B, Hq, self.k), dtype=torch.int32, pin_memory=True),
+            q=torch.empty((self.B, Hq, D), dtype=bf, device=dev),
+            k_new=torch.empty((self.B, self.Hkv, D), dtype=bf, device=dev),
+            v_new=torch.empty((self.B, self.Hkv, D), dtype=bf, device=dev),
+            out=torch.empty((self.B, Hq, D), dtype=f32, device=dev),
+            idx=torch.empty((self.B, Hq, self.k), dtype=i32, device=dev),
+            scores=torch.empty((self.B, Hq, self.k), dtype=f32, device=dev),
+            q_h=torch.empty((self.B, Hq, D), dtype=bf, pin_memory=True),
+            k_h=torch.empty((self.B, self.Hkv, D), dtype=bf, pin_memory=True),
+            v_h=torch.empty((self.B, self.Hkv, D), dtype=bf, pin_memory=True),
+            out_h=torch.empty((self.B, Hq, D), dtype=f32, pin_memory=True),
+            idx_h=torch.empty((self.B, Hq, self.k), dtype=i32, pin_memory=True),
         )
+        self._graphs.clear()
 
+    # ------------------------------------------------------------------ device-side pieces
     def append(self, k_new: torch.Tensor, v_new: torch.Tensor) -> None:
         """GenWindow.append (attention.py:94-100) on device: rows n_ctx + n_win, n_win += 1."""
         if self._bufs is None:
@@ -83,17 +95,66 @@ class TopkDecoder:
                                   **self.kw)
         return b["out"], b["idx"], b["scores"]
 
-    def step(self, q: torch.Tensor, k_new: torch.Tensor | None = None, v_new: torch.Tensor | None = None):
-        """One decode step for this layer. Host inputs → host outputs (out f32, idx int32);
-        device inputs → device outputs."""
-        self._ensure(q.shape[1])
-        if k_new is not None:
-            self.append(k_new, v_new)
-        out, idx, _ = self.attend(q)
-        if q.is_cuda:
-            return out, idx
+    def _host_step_body(self, with_kv: bool, with_idx: bool) -> None:
+        """Everything a host-I/O step enqueues, reading/writing the pinned staging buffers."""
         b = self._bufs
-        b["out_h"].copy_(out, non_blocking=True)
-        b["idx_h"].copy_(idx, non_blocking=True)
+        b["q"].copy_(b["q_h"], non_blocking=True)
+        if with_kv:
+            b["k_new"].copy_(b["k_h"], non_blocking=True)
+            b["v_new"].copy_(b["v_h"], non_blocking=True)
+            ops.kv_append(self.k_cache, self.v_cache, b["k_new"], b["v_new"], self.n_win,
+                          base=self.n_ctx, advance=True)
+        ops.topk_decode_attention(b["q"], self.k_cache, self.v_cache, self.n_ctx, self.k,
+                                  n_win=self.n_win, out=b["out"], idx=b["idx"], scores=b["scores"],
+                                  workspace=self.ws, **self.kw)
+        b["out_h"].copy_(b["out"], non_blocking=True)
+        if with_idx:
+            b["idx_h"].copy_(b["idx"], non_blocking=True)
+
+    # ------------------------------------------------------------------ user API
+    def step(self, q: torch.Tensor, k_new: torch.Tensor | None = None, v_new: torch.Tensor | None = None,
+             return_idx: bool = True):
+        """One decode step for this layer. Host inputs → host outputs (out f32[, idx int32]);
+        device inputs → device outputs (out, idx)."""
+        self._ensure(q.shape[1])
+        if q.is_cuda:
+            if k_new is not None:
+                self.append(k_new, v_new)
+            out, idx, _ = self.attend(q)
+            return (out, idx) if return_idx else out
+        b = self._bufs
+        b["q_h"].copy_(q)
+        with_kv = k_new is not None
+        if with_kv:
+            b["k_h"].copy_(k_new)
+            b["v_h"].copy_(v_new)
+        key = (with_kv, return_idx)
+        if self.use_graph:
+            g = self._graphs.get(key)
+            if g is None:
+                g = self._capture(key)
+            g.replay()
+        else:
+            self._host_step_body(with_kv, return_idx)
         torch.cuda.current_stream(self.device).synchronize()
-        return b["out_h"], b["idx_h"]
+        return (b["out_h"], b["idx_h"]) if return_idx else b["out_h"]
+
+    def _capture(self, key) -> torch.cuda.CUDAGraph:
+        with_kv, with_idx = key
+        stream = torch.cuda.current_stream(self.device)
+        # capture on a side stream; one eager run first so every lazy attribute/occupancy
+        # query inside libtkv has happened before capture. The eager run's KV append is undone
+        # by rewinding n_win, so the capture does not double-append.
+        saved = self.n_win.clone()
+        self._host_step_body(with_kv, with_idx)
+        self.n_win.copy_(saved)
+        stream.synchronize()
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(self.device)
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(g, stream=side):
+                self._host_step_body(with_kv, with_idx)
+        stream.wait_stream(side)
+        self._graphs[key] = g
+        return g

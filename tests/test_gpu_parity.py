@@ -311,3 +311,28 @@ def test_fused_repeated_calls_reset_state(cuda):
         out, idx, sc = topk_decode_attention(_dev(qq, cuda), Kd, Vd, [50000 - rep], 777, fused=True)
         torch.cuda.synchronize()
         _check(qq, K, V, [50000 - rep], 777, out, idx, sc)
+
+
+@pytest.mark.parametrize("use_graph", [True, False])
+def test_decoder_host_io_steps(cuda, use_graph):
+    """TopkDecoder.step with host tensors (the end-to-end path, CUDA-graph replayed): each step
+    appends the token's k/v to the window and attends; equals the oracle on the grown cache."""
+    from paper_2502_06766_b200 import TopkDecoder
+
+    rng = np.random.default_rng(77)
+    B, Hq, Hkv, N, k, steps = 2, 8, 2, 6000, 64, 4
+    q0, K, V = _make(rng, B, Hq, Hkv, N + 16)
+    Kd, Vd = _dev(K, cuda), _dev(V, cuda)
+    dec = TopkDecoder(Kd, Vd, N, k, max_ctx=N, use_graph=use_graph)
+    Kref, Vref = K.copy(), V.copy()
+    for s in range(steps):
+        q = bf16_normal(rng, (B, Hq, 128))
+        kn = bf16_normal(rng, (B, Hkv, 128))
+        vn = bf16_normal(rng, (B, Hkv, 128))
+        out, idx = dec.step(torch.from_numpy(q).to(torch.bfloat16), torch.from_numpy(kn).to(torch.bfloat16),
+                            torch.from_numpy(vn).to(torch.bfloat16))
+        Kref[:, :, N + s] = kn
+        Vref[:, :, N + s] = vn
+        _check(q, Kref, Vref, [N] * B, k, out, idx, torch.zeros(B, Hq, k) + torch.from_numpy(
+            np.stack([[O.ip_scores_all(Kref[b, h // 4, :N], q[b, h])[idx.numpy()[b, h]] for h in range(Hq)]
+                      for b in range(B)]).astype(np.float32)), n_win=[s + 1] * B)
