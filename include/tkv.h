@@ -149,6 +149,14 @@ int tkv_shard_finalize(const tkv_problem* p, const void* q, const void* k_cache,
                        const float* partial, float* out, void* workspace,
                        size_t workspace_bytes, void* stream);
 
+/*
+ * TKKV cache loading (reference on-disk format, cache.py:1-13, 120-257): convert `rows` rows
+ * of one f32 section (row-major, d <= 128 floats per row, device memory) into bf16 cache rows
+ * of 128 values (zero-padded) at dst (16-byte aligned), stream-ordered. The host side
+ * (header validation, section offsets, staging) is paper_2502_06766_b200/cache.py.
+ */
+int tkv_convert_rows_f32(const float* src, int64_t rows, int32_t d, void* dst, void* stream);
+
 /* Number of kernels the last compute call on this thread enqueued (for launch accounting). */
 int tkv_last_launch_count(void);
 

@@ -35,6 +35,7 @@ EXPORTS = (
     "tkv_last_launch_count",
     "tkv_profile_scan_events",
     "tkv_debug_trace",
+    "tkv_convert_rows_f32",
 )
 
 COMBINE_JOINT = 0
@@ -75,6 +76,7 @@ _SIG = {
     "tkv_last_launch_count": ([], _I),
     "tkv_profile_scan_events": ([_P, _P], _I),
     "tkv_debug_trace": ([_P, ctypes.c_uint32], _I),
+    "tkv_convert_rows_f32": ([_P, ctypes.c_int64, ctypes.c_int32, _P, _P], _I),
     "tkv_workspace_bytes": ([ctypes.POINTER(Problem), ctypes.POINTER(ctypes.c_size_t)], _I),
     "tkv_workspace_init": ([ctypes.POINTER(Problem), _P, ctypes.c_size_t, _P], _I),
     "tkv_topk_decode_attention": (

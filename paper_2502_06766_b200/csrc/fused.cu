@@ -144,7 +144,7 @@ __device__ void do_sample(const FusedParams& p, const Ctl& ctl, int g, int part)
   const int gg = lane >> 2, c = lane & 3;
   const int64_t N = a.n_ctx[b];
   if (N > 0) {
-    const int64_t stride = (N + kSamples - 1) / kSamples;
+    const int64_t stride = sample_stride(N);
     const int Sb = static_cast<int>((N + stride - 1) / stride);
     QFrag f;
     load_qfrag(f, a.q + (static_cast<int64_t>(b) * a.Hq + kvh * a.G) * kD, a.G, lane);
@@ -184,7 +184,7 @@ __device__ void do_thresh(const FusedParams& p, const Ctl& ctl, int bh, unsigned
   const int64_t kb = N < a.k ? N : a.k;
   int Sb = 0;
   if (N > 0) {
-    const int64_t stride = (N + kSamples - 1) / kSamples;
+    const int64_t stride = sample_stride(N);
     Sb = static_cast<int>((N + stride - 1) / stride);
   }
   const double mu = N > 0 ? static_cast<double>(kb) * Sb / static_cast<double>(N) : 0.0;

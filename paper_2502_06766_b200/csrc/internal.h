@@ -24,6 +24,13 @@ constexpr int kAttendChunk = 512;    // selected rows per gather CTA (list mode)
 constexpr int kCandChunk = 1024;     // candidates per work item (candidate mode)
 constexpr int kSortMax = 16384;      // sorted output supported up to this k
 constexpr uint32_t kNoFilterShift = 20;  // histogram shift when every score is a candidate
+constexpr int kMinSampleStride = 8;      // small contexts sample at most every 8th row
+
+// rows between two sampled rows: up to kSamples samples, never denser than 1 in 8
+__host__ __device__ inline int64_t sample_stride(int64_t n) {
+  const int64_t s = (n + kSamples - 1) / kSamples;
+  return s > kMinSampleStride ? s : kMinSampleStride;
+}
 
 // per-(b, q head) state shared by the kernels of one call, in the workspace
 struct HeadState {

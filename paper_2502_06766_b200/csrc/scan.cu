@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(kSampleThreads) sample_kernel(SampleParams p) 
   const int g = lane >> 2, c = lane & 3;
   const int64_t N = p.n_ctx[b];
   if (N <= 0) return;
-  const int64_t stride = (N + kSamples - 1) / kSamples;
+  const int64_t stride = sample_stride(N);
   const int Sb = static_cast<int>((N + stride - 1) / stride);
   QFrag f;
   load_qfrag(f, p.q + (static_cast<int64_t>(b) * p.Hq + kvh * p.G) * kD, p.G, lane);
@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(kThrThreads) threshold_kernel(SampleParams p) 
   const int64_t kb = N < p.k ? N : p.k;
   int Sb = 0;
   if (N > 0) {
-    const int64_t stride = (N + kSamples - 1) / kSamples;
+    const int64_t stride = sample_stride(N);
     Sb = static_cast<int>((N + stride - 1) / stride);
   }
   const double mu = N > 0 ? static_cast<double>(kb) * Sb / static_cast<double>(N) : 0.0;

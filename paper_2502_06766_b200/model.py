@@ -1,0 +1,213 @@
+"""Decode-step integration: a random-init Llama-3-8B-shaped decoder whose attention is the
+B200 top-k decode attention (SURVEY §8f "next" #2, BASELINE cfg4).
+
+Mirrors the reference's `decode_step` (attention.py:170-236) layer by layer — RMSNorm, Q/K/V
+projections, RoPE at the token's absolute position (model.py:178-191), append of the token's
+k/v to the generation window (attention.py:210), top-k attention of every head jointly with
+the window (here ONE libtkv call per layer instead of the per-head loop, attention.py:213-230),
+W_O, residual, RMSNorm, MLP, residual; final norm and logits. Differences to the desk-scale
+reference model, as SURVEY §8f notes: GQA (32 q / 8 kv heads), and the Llama SwiGLU MLP
+instead of the reference's non-gated SiLU (model.py:263). Weights and the prefilled KV cache
+are random (no checkpoints offline). The dense projections are plain cuBLAS GEMMs through
+torch; the whole step is captured in one CUDA graph.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import ops
+from .errors import InputError
+
+
+@dataclass(frozen=True)
+class LlamaShape:
+    n_layers: int = 32
+    d_model: int = 4096
+    n_heads: int = 32
+    n_kv_heads: int = 8
+    head_dim: int = 128
+    ffn: int = 14336
+    vocab: int = 128256
+    rope_theta: float = 500000.0
+    eps: float = 1e-5
+
+
+LLAMA3_8B = LlamaShape()
+
+
+def rope_tables(shape: LlamaShape, max_pos: int, device) -> tuple[torch.Tensor, torch.Tensor]:
+    inv = 1.0 / (shape.rope_theta ** (torch.arange(0, shape.head_dim, 2, device=device, dtype=torch.float64)
+                                      / shape.head_dim))
+    pos = torch.arange(max_pos, device=device, dtype=torch.float64)
+    ang = torch.outer(pos, inv)
+    return torch.cos(ang).float(), torch.sin(ang).float()
+
+
+def apply_rope(x: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor) -> torch.Tensor:
+    """Rotate-half RoPE of x [..., H, 128] (f32) with cos/sin [64] for one position."""
+    x1, x2 = x[..., 0::2], x[..., 1::2]
+    out = torch.empty_like(x)
+    out[..., 0::2] = x1 * cos - x2 * sin
+    out[..., 1::2] = x1 * sin + x2 * cos
+    return out
+
+
+def rmsnorm(x: torch.Tensor, w: torch.Tensor, eps: float) -> torch.Tensor:
+    xf = x.float()
+    return (xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + eps) * w).to(torch.bfloat16)
+
+
+class TopkLlamaDecoder:
+    """Batch-1 decode with every layer's KV cache resident in HBM ([1, Hkv, rows, 128] bf16)."""
+
+    def __init__(self, shape: LlamaShape, n_ctx: int, k: int, *, device="cuda", seed: int = 0,
+                 window_capacity: int = 256, init_std: float = 0.02):
+        if shape.head_dim != ops.HEAD_DIM:
+            raise InputError(f"head_dim must be {ops.HEAD_DIM}")
+        self.shape, self.n, self.k = shape, n_ctx, k
+        self.device = torch.device(device)
+        dev, s = self.device, shape
+        g = torch.Generator(device=dev).manual_seed(seed)
+        bf = torch.bfloat16
+
+        def w(*dims):
+            return (torch.randn(dims, generator=g, device=dev) * init_std).to(bf)
+
+        self.embed = w(s.vocab, s.d_model)
+        self.lm_head = w(s.d_model, s.vocab)
+        self.norm_f = torch.ones(s.d_model, device=dev)
+        qkv = (s.n_heads + 2 * s.n_kv_heads) * s.head_dim
+        self.layers = []
+        rows = n_ctx + window_capacity
+        self.rows = rows
+        for layer in range(s.n_layers):
+            lw = dict(wqkv=w(s.d_model, qkv), wo=w(s.n_heads * s.head_dim, s.d_model),
+                      wgu=w(s.d_model, 2 * s.ffn), wd=w(s.ffn, s.d_model),
+                      n1=torch.ones(s.d_model, device=dev), n2=torch.ones(s.d_model, device=dev))
+            # prefilled context: random post-RoPE keys / values, generated in row chunks
+            K = torch.empty((1, s.n_kv_heads, rows, s.head_dim), dtype=bf, device=dev)
+            V = torch.empty_like(K)
+            for r0 in range(0, rows, 1 << 16):
+                r1 = min(rows, r0 + (1 << 16))
+                K[:, :, r0:r1] = torch.randn((1, s.n_kv_heads, r1 - r0, s.head_dim), generator=g, device=dev).to(bf)
+                V[:, :, r0:r1] = torch.randn((1, s.n_kv_heads, r1 - r0, s.head_dim), generator=g, device=dev).to(bf)
+            lw["K"], lw["V"] = K, V
+            self.layers.append(lw)
+        self.n_ctx = torch.tensor([n_ctx], dtype=torch.int32, device=dev)
+        self.n_win = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.pos = torch.zeros(1, dtype=torch.int64, device=dev)  # absolute position of the token
+        self.cos, self.sin = rope_tables(s, rows, dev)
+        prob = ops.make_problem(1, s.n_heads, s.n_kv_heads, rows, n_ctx, k)
+        self.ws = ops.Workspace(prob, dev)
+        self.token = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.next_token = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.attn_out = torch.empty((1, s.n_heads, s.head_dim), dtype=torch.float32, device=dev)
+        self.idx = torch.empty((1, s.n_heads, k), dtype=torch.int32, device=dev)
+        self.scores = torch.empty((1, s.n_heads, k), dtype=torch.float32, device=dev)
+        self.graph = None
+        self.pos.fill_(n_ctx)
+
+    def _layer(self, x: torch.Tensor, lw: dict) -> torch.Tensor:
+        s = self.shape
+        h = rmsnorm(x, lw["n1"], s.eps)
+        qkv = (h @ lw["wqkv"]).float()
+        nq, nk = s.n_heads * s.head_dim, s.n_kv_heads * s.head_dim
+        q = qkv[:, :nq].view(1, s.n_heads, s.head_dim)
+        kk = qkv[:, nq:nq + nk].view(1, s.n_kv_heads, s.head_dim)
+        v = qkv[:, nq + nk:].view(1, s.n_kv_heads, s.head_dim)
+        cos = self.cos.index_select(0, self.pos)
+        sin = self.sin.index_select(0, self.pos)
+        q = apply_rope(q, cos, sin).to(torch.bfloat16)
+        kk = apply_rope(kk, cos, sin).to(torch.bfloat16).contiguous()
+        v = v.to(torch.bfloat16).contiguous()
+        # window append (attention.py:210) — advance n_win once per step, after the last layer
+        ops.kv_append(lw["K"], lw["V"], kk, v, self.n_win, base=self.n_ctx, advance=False)
+        ops.topk_decode_attention(q.contiguous(), lw["K"], lw["V"], self.n_ctx, self.k, n_win=self._n_win_next,
+                                  out=self.attn_out, idx=self.idx, scores=self.scores, workspace=self.ws,
+                                  max_ctx=self.n)
+        x = x + self.attn_out.view(1, -1).to(torch.bfloat16) @ lw["wo"]
+        h2 = rmsnorm(x, lw["n2"], s.eps)
+        gu = h2 @ lw["wgu"]
+        gate, up = gu[:, :s.ffn], gu[:, s.ffn:]
+        x = x + (torch.nn.functional.silu(gate.float()) * up.float()).to(torch.bfloat16) @ lw["wd"]
+        return x
+
+    def _step_body(self) -> None:
+        x = self.embed.index_select(0, self.token)
+        self._n_win_next = self.n_win + 1  # the token attends to itself (attention.py:210)
+        for lw in self.layers:
+            x = self._layer(x, lw)
+        logits = rmsnorm(x, self.norm_f, self.shape.eps) @ self.lm_head
+        self.next_token.copy_(logits.argmax(-1))
+        self.n_win.add_(1)
+        self.pos.add_(1)
+
+    def step(self, token: int | None = None) -> torch.Tensor:
+        """One decode step for every layer; returns the greedy next token (device tensor)."""
+        if token is not None:
+            self.token.fill_(token)
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self._step_body()
+        self.token.copy_(self.next_token)
+        return self.next_token
+
+    def capture(self) -> None:
+        """Capture one step into a CUDA graph (window and position advance on device)."""
+        torch.cuda.synchronize(self.device)
+        saved = (self.n_win.clone(), self.pos.clone(), self.token.clone())
+        self._step_body()  # warm-up: lazy libtkv / cuBLAS setup outside the capture
+        self.n_win.copy_(saved[0])
+        self.pos.copy_(saved[1])
+        self.token.copy_(saved[2])
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._step_body()
+        self.graph = g
+
+    @staticmethod
+    def memory_bytes(shape: LlamaShape, n_ctx: int, window_capacity: int = 256) -> int:
+        s = shape
+        per_layer_w = (s.d_model * (s.n_heads + 2 * s.n_kv_heads) * s.head_dim + s.n_heads * s.head_dim * s.d_model
+                       + 3 * s.d_model * s.ffn) * 2
+        kv = 2 * s.n_kv_heads * (n_ctx + window_capacity) * s.head_dim * 2
+        return s.n_layers * (per_layer_w + kv) + 2 * s.vocab * s.d_model * 2
+
+
+def dense_reference_step(dec: TopkLlamaDecoder, token: int) -> torch.Tensor:
+    """fp32 reference of the same step with DENSE attention over context + window (k = N is the
+    exact-equivalence case). Test helper: does not touch the decoder's state."""
+    s = dec.shape
+    x = dec.embed[token].float()[None]
+    pos = dec.pos.clone()
+    nwin = int(dec.n_win.item())
+    for lw in dec.layers:
+        h = rmsnorm(x, lw["n1"], s.eps).float()
+        qkv = h @ lw["wqkv"].float()
+        nq, nk = s.n_heads * s.head_dim, s.n_kv_heads * s.head_dim
+        q = qkv[:, :nq].view(1, s.n_heads, s.head_dim)
+        kk = qkv[:, nq:nq + nk].view(1, s.n_kv_heads, s.head_dim)
+        v = qkv[:, nq + nk:].view(1, s.n_kv_heads, s.head_dim)
+        cos, sin = dec.cos.index_select(0, pos), dec.sin.index_select(0, pos)
+        q = apply_rope(q, cos, sin).to(torch.bfloat16).float()
+        kk = apply_rope(kk, cos, sin).to(torch.bfloat16).float()
+        v = v.to(torch.bfloat16).float()
+        rows = dec.n + nwin
+        K = torch.cat([lw["K"][0, :, :rows].float(), kk.transpose(0, 1)], dim=1)  # [Hkv, rows+1, d]
+        V = torch.cat([lw["V"][0, :, :rows].float(), v.transpose(0, 1)], dim=1)
+        G = s.n_heads // s.n_kv_heads
+        Kq = K.repeat_interleave(G, 0)
+        Vq = V.repeat_interleave(G, 0)
+        sc = torch.einsum("hd,hnd->hn", q[0], Kq) / math.sqrt(s.head_dim)
+        attn = torch.einsum("hn,hnd->hd", torch.softmax(sc, -1), Vq)
+        x = x + attn.reshape(1, -1).to(torch.bfloat16).float() @ lw["wo"].float()
+        h2 = rmsnorm(x, lw["n2"], s.eps).float()
+        gu = h2 @ lw["wgu"].float()
+        x = x + (torch.nn.functional.silu(gu[:, :s.ffn]) * gu[:, s.ffn:]) @ lw["wd"].float()
+    return rmsnorm(x, dec.norm_f, s.eps).float() @ dec.lm_head.float()

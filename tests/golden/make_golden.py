@@ -124,6 +124,45 @@ def main() -> None:
     save_attend("dense_equiv_n256_d128", rnd(rng, (128,)), rnd(rng, (256, 128)), rnd(rng, (256, 128)),
                 rnd(rng, (2, 128)), rnd(rng, (2, 128)), 256)
 
+    # ---- TKKV cache file (cache.py:1-13) + header mutations with the reference's verdicts
+    from topk_kv.cache import CacheFile, CacheMeta, KvCache, write_cache  # noqa: E402
+    from topk_kv.errors import FormatError as RefFormatError  # noqa: E402
+
+    meta = CacheMeta(2, 3, 50, 16, "f32", "golden-tiny")
+    kv_rng = np.random.default_rng(7)
+    cache = KvCache(meta, rnd(kv_rng, (2, 3, 50, 16)), rnd(kv_rng, (2, 3, 50, 16)))
+    tk_path = OUT / "tkkv_small.tkkv"
+    write_cache(cache, tk_path)
+    blob = tk_path.read_bytes()
+    mutations = []
+    spots = [(0, b"XKKV"), (4, b"\x02"), (8, b"\x00"), (16, b"\x00"), (24, b"\x00"), (32, b"\x00"),
+             (40, b"\x31"), (48, b"\x07"), (49, b"\xff\xff"), (53, b"\xff"), (49 + 4 + 11, b"\x01"),
+             (49 + 4 + 11 + 8, b"\x00"), (len(blob) - 1, None), (len(blob), b"\x00"), (16, b"\x03"),
+             (24, b"\x33"), (40, b"\x00\x01"), (49, b"\x00\x00\x00\x00"), (49 + 4 + 11 + 16, b"\x10"),
+             (0, b"\x00")]
+    for i, (at, new) in enumerate(spots):
+        b2 = bytearray(blob)
+        if new is None:
+            b2 = b2[:at]
+        elif at >= len(b2):
+            b2 += new
+        else:
+            b2[at:at + len(new)] = new
+        mp = OUT / f"tkkv_mut_{i:02d}.bin"
+        mp.write_bytes(bytes(b2))
+        try:
+            with CacheFile(mp) as cf:
+                verdict = {"ok": True, "meta_hash": cf.meta.meta_hash().hex()}
+        except RefFormatError as e:
+            verdict = {"ok": False, "error": "FormatError", "offset": e.offset}
+        except Exception as e:  # noqa: BLE001
+            verdict = {"ok": False, "error": type(e).__name__, "offset": None}
+        mp.unlink()
+        mutations.append({"at": at, "new": None if new is None else new.hex(), "verdict": verdict})
+    index.append({"name": "tkkv_small", "kind": "tkkv", "meta_hash": meta.meta_hash().hex(),
+                  "mutations": mutations})
+    np.savez_compressed(OUT / "tkkv_small_values.npz", keys=bf16_bits(cache.keys), values=bf16_bits(cache.values))
+
     (OUT.parent / "index.json").write_text(json.dumps({"reference": str(REF), "cases": index}, indent=1))
     print(f"wrote {len(index)} cases to {OUT}")
 

@@ -18,7 +18,7 @@ HEADER = Path(__file__).resolve().parents[1] / "include" / "tkv.h"
 def header_functions() -> list[str]:
     text = HEADER.read_text()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"\b(tkv_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(tkv_[a-z0-9_]+)\s*\(", text)))
 
 
 def test_library_loads_and_exports_header_symbols():
