@@ -21,6 +21,7 @@
 // candidates survived (then the true top-k ⊆ candidates, since every top-k key >= the k-th
 // key >= t_h); if not, the head is re-scanned with t_h = 0 (scan_kernel fallback pass).
 #include <math.h>
+#include <stdlib.h>
 
 #include "scan_dev.cuh"
 
@@ -184,6 +185,11 @@ static int scan_grid(int G, size_t smem) {
     int sms = 0, per = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, scan_kernel, kScanWarps * 32, smem);
+    static const int cap = [] {
+      const char* e = getenv("TKV_SCAN_CTAS_PER_SM");
+      return e ? atoi(e) : 0;
+    }();
+    if (cap > 0 && per > cap) per = cap;
     cached[G] = sms * (per > 0 ? per : 1);
   }
   return cached[G];
