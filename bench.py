@@ -59,6 +59,12 @@ def peaks():
     return 6650.0, "fallback"
 
 
+# the dominant kernel: the TMA + tcgen05 key scan unless TKV_SCAN=hmma selects the mma.sync scan
+SCAN_KERNEL = "scan_kernel" if os.environ.get("TKV_SCAN", "") == "hmma" else "scan_tc_kernel"
+SCAN_DESC = {"scan_kernel": "scan_kernel (mma.sync GQA key scan + candidate emit)",
+             "scan_tc_kernel": "scan_tc_kernel (TMA + tcgen05 GQA key scan + candidate emit)"}
+
+
 def scan_traffic(config: str, world: int):
     """dram__bytes_read.sum + dram__bytes_write.sum of the scan kernel per launch, from the
     committed ncu --set full capture (profiles/r*_summary.json); None when not captured."""
@@ -68,7 +74,7 @@ def scan_traffic(config: str, world: int):
     if not caps:
         return None
     j = json.loads(caps[-1].read_text())
-    return j.get("scan_kernel", {}).get("traffic_bytes")
+    return j.get(SCAN_KERNEL, {}).get("traffic_bytes")
 
 
 class ClockSampler:
@@ -331,7 +337,7 @@ def main():
                    "head_dim": D, "parallelism": f"token-shard{world}" if world > 1 else "single",
                    "l2": "inputs larger than L2 (K cache %.2f GB per GPU, L2 126 MB): no flush" % (kbytes / 1e9),
                    "seed": args.seed},
-        "roofline": {"bound": "hbm", "kernel": "scan_kernel (GQA key scan + candidate emit)",
+        "roofline": {"bound": "hbm", "kernel": SCAN_DESC[SCAN_KERNEL],
                      "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": scan_traffic(args.config, world),
                      "algorithmic_bytes_per_launch": kbytes, "kernel_us": round(scan_ms * 1e3, 2)},

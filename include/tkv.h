@@ -23,7 +23,8 @@
  *   v_cache  [B, Hkv, cache_rows, d] bf16   rows [n_ctx[b], n_ctx[b]+n_win[b]) = generation
  *                                            window, always attended, never retrieved —
  *                                            reference GenWindow, attention.py:76-104)
- *   n_ctx, n_win [B]               int32  device arrays
+ *   n_ctx, n_win [B]               int32  device arrays, n_ctx[b] + n_win[b] <= cache_rows
+ *                                          (n_ctx[b] <= max_ctx; a window past the cache is clamped)
  *   out      [B, Hq, d]            f32
  *   idx      [B, Hq, k]            int32  global row ids (row_offset + local row); -1 pads
  *                                          when k > n_ctx[b] (reference clamps, attention.py:147-149)
@@ -60,6 +61,8 @@ extern "C" {
 #define TKV_F_SORTED 1u    /* idx/scores ordered score-desc, id-asc (TopKResult order, ann.py:166) */
 #define TKV_F_NO_FILTER 2u /* disable the sampled-threshold pre-filter (emit every score)       */
 #define TKV_F_FUSED 4u     /* run the layer step as one persistent work-queue kernel (fused.cu)   */
+#define TKV_F_SCAN_HMMA 8u /* key scan on register-staged mma.sync (scan.cu) instead of the TMA +  
+                              tcgen05 pipeline (scan_tc.cu, the default)                         */
 
 typedef struct tkv_problem {
   int32_t batch;         /* B                                                                  */
@@ -163,7 +166,8 @@ int tkv_last_launch_count(void);
 /*
  * Measurement hook: when both events are non-NULL (cudaEvent_t as void*), subsequent compute
  * calls on this thread record `start` / `stop` on their stream immediately before / after the
- * dominant kernel launch (the fused layer-step kernel; with TKV_F_UNFUSED the key-scan kernel),
+ * dominant kernel launch (the key-scan kernel: scan_tc_kernel, or scan_kernel with
+ * TKV_F_SCAN_HMMA; with TKV_F_FUSED the fused layer-step kernel),
  * so a caller can time it with CUDA events on the stream it runs on. Pass NULLs to disable.
  */
 int tkv_profile_scan_events(void* start, void* stop);

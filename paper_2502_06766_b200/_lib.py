@@ -43,6 +43,7 @@ COMBINE_ADDITIVE = 1
 F_SORTED = 1
 F_NO_FILTER = 2
 F_FUSED = 4
+F_SCAN_HMMA = 8
 
 
 class Problem(ctypes.Structure):

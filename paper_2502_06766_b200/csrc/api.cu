@@ -206,7 +206,10 @@ int run_select(const tkv_problem* p, const void* q, const void* k_cache, const i
   cp.hs = hs;
   cp.fallback = 0;
   if (g_scan_start && g_scan_stop) cudaEventRecord(g_scan_start, st);
-  TKV_LAUNCH(launch_scan(cp, st));
+  if (!(p->flags & TKV_F_SCAN_HMMA) && scan_tc_supported(cp))
+    TKV_LAUNCH(launch_scan_tc(cp, st));
+  else
+    TKV_LAUNCH(launch_scan(cp, st));
   if (g_scan_start && g_scan_stop) cudaEventRecord(g_scan_stop, st);
 
   SelectParams sl{};

@@ -96,7 +96,10 @@ __device__ void finalize_head(const AttendParams& p, int b, int h, int kvh, int6
                               float l_c, float o_c, float* s_z, float* s_scr, float* s_o) {
   const int tid = threadIdx.x;
   const int bh = b * p.Hq + h;
-  const int64_t nwin = p.n_win ? p.n_win[b] : 0;
+  // precondition n_ctx + n_win <= cache_rows (tkv.h); a window past the cache is clamped
+  // rather than read from the next head's rows
+  int64_t nwin = p.n_win ? p.n_win[b] : 0;
+  if (nwin > p.cache_rows - nctx) nwin = p.cache_rows - nctx;
   float m_w = -INFINITY, l_w = 0.f, o_w = 0.f;
   if (nwin > 0) accumulate_rows(p, b, h, kvh, nctx, nctx + nwin, false, 0ull, m_w, l_w, o_w, s_z, s_scr);
   float val;

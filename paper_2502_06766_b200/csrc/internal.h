@@ -178,6 +178,8 @@ __host__ __device__ inline int fused_ctl_words(int NG, int NH) { return 8 + 2 * 
 cudaError_t launch_fused(const FusedParams& p, cudaStream_t s);
 cudaError_t launch_sample(const SampleParams& p, cudaStream_t s);
 cudaError_t launch_scan(const ScanParams& p, cudaStream_t s);
+cudaError_t launch_scan_tc(const ScanParams& p, cudaStream_t s);
+bool scan_tc_supported(const ScanParams& p);
 void scan_launch_shape(const ScanParams& p, int* grid, int* smem_bytes);
 cudaError_t launch_select(const SelectParams& p, cudaStream_t s);
 cudaError_t launch_kth(const SelectParams& p, cudaStream_t s);

@@ -172,10 +172,12 @@ def test_fallback_when_sample_overestimates(cuda, fused):
     out, idx, sc = _run(q, K, V, [N], k, cuda, fused=fused)
     torch.cuda.synchronize()
     _check(q, K, V, [N], k, out, idx, sc)
-    # the filtered and unfiltered paths agree exactly on the set
-    out2, idx2, _ = _run(q, K, V, [N], k, cuda, no_filter=True)
-    for h in range(Hq):
-        assert set(idx[0, h].tolist()) == set(idx2[0, h].tolist())
+    # the unfiltered path (every score a candidate, no fallback) is exact as well; the two may
+    # differ only on near-ties, since the fallback re-scan uses the mma.sync scan and the main
+    # pass the tcgen05 scan (fp32 accumulation orders differ)
+    out2, idx2, sc2 = _run(q, K, V, [N], k, cuda, no_filter=True)
+    torch.cuda.synchronize()
+    _check(q, K, V, [N], k, out2, idx2, sc2)
 
 
 def test_no_filter_equals_filter(cuda):
