@@ -61,6 +61,9 @@ extern "C" {
 #define TKV_F_SORTED 1u    /* idx/scores ordered score-desc, id-asc (TopKResult order, ann.py:166) */
 #define TKV_F_NO_FILTER 2u /* disable the sampled-threshold pre-filter (emit every score)       */
 #define TKV_F_FUSED 4u     /* run the layer step as one persistent work-queue kernel (fused.cu)   */
+#define TKV_F_PARTS(n) ((uint32_t)(n) << 8) /* pipeline parts: scan of part i+1 overlaps the  \
+                              k-th selection + V gather of part i (1..15; 0 = automatic)         */
+#define TKV_F_PARTS_MASK 0xF00u
 #define TKV_F_SCAN_HMMA 8u /* key scan on register-staged mma.sync (scan.cu) instead of the TMA +  
                               tcgen05 pipeline (scan_tc.cu, the default)                         */
 

@@ -44,6 +44,7 @@ F_SORTED = 1
 F_NO_FILTER = 2
 F_FUSED = 4
 F_SCAN_HMMA = 8
+F_PARTS_SHIFT = 8  # TKV_F_PARTS(n): bits 8..11
 
 
 class Problem(ctypes.Structure):

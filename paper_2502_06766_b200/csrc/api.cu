@@ -67,7 +67,7 @@ Layout make_layout(const tkv_problem* p) {
   L.flag = take(BH * 4);
   L.gflag = take(BK * 4);
   L.fctl = take(static_cast<size_t>(fused_ctl_words(static_cast<int>(BK), static_cast<int>(BH))) * 4);
-  L.fbl = take(4);
+  L.fbl = take(4 * kMaxParts);
   L.ctrl_end = off;
   L.cnt = take(BH * 4);
   L.thr = take(BH * 4);
@@ -168,10 +168,9 @@ HeadState head_state(void* ws, const Layout& L) {
   return hs;
 }
 
-// sample → threshold → scan → k-th threshold (+ exactness fallback: re-scan / k-th); the
-// selected set is { candidates c : c >= meta_kth }, materialised by run_emit
-int run_select(const tkv_problem* p, const void* q, const void* k_cache, const int32_t* n_ctx,
-               void* ws, const Layout& L, cudaStream_t st) {
+// sample → threshold for every head; fills the scan / k-th parameter templates
+int run_prefix(const tkv_problem* p, const void* q, const void* k_cache, const int32_t* n_ctx, void* ws,
+               const Layout& L, cudaStream_t st, ScanParams* cp_out, SelectParams* sl_out) {
   const int G = p->n_q_heads / p->n_kv_heads;
   const HeadState hs = head_state(ws, L);
   SampleParams sp{};
@@ -205,12 +204,8 @@ int run_select(const tkv_problem* p, const void* q, const void* k_cache, const i
   cp.cap = L.cap;
   cp.hs = hs;
   cp.fallback = 0;
-  if (g_scan_start && g_scan_stop) cudaEventRecord(g_scan_start, st);
-  if (!(p->flags & TKV_F_SCAN_HMMA) && scan_tc_supported(cp))
-    TKV_LAUNCH(launch_scan_tc(cp, st));
-  else
-    TKV_LAUNCH(launch_scan(cp, st));
-  if (g_scan_start && g_scan_stop) cudaEventRecord(g_scan_stop, st);
+  cp.seg_begin = 0;
+  cp.seg_count = static_cast<int64_t>(p->batch) * p->n_kv_heads;
 
   SelectParams sl{};
   sl.src = cp.cand;
@@ -226,12 +221,88 @@ int run_select(const tkv_problem* p, const void* q, const void* k_cache, const i
   sl.meta_kb = at<int32_t>(ws, L.mkb);
   sl.hs = hs;
   sl.pass = kPassMain;
-  // exactness fallback (heads whose sampled threshold let fewer than k rows through): the
-  // k-th kernel tail-launches a re-scan with threshold 0 and a fallback k-th pass on device
+  *cp_out = cp;
+  *sl_out = sl;
+  return TKV_OK;
+}
+
+bool use_tc_scan(const tkv_problem* p, const ScanParams& cp) {
+  return !(p->flags & TKV_F_SCAN_HMMA) && scan_tc_supported(cp);
+}
+
+// key scan of segments [s0, s1) on stream `st`
+int run_scan_part(const tkv_problem* p, ScanParams cp, int64_t s0, int64_t s1, cudaStream_t st) {
+  cp.seg_begin = s0;
+  cp.seg_count = s1 - s0;
+  if (use_tc_scan(p, cp))
+    TKV_LAUNCH(launch_scan_tc(cp, st));
+  else
+    TKV_LAUNCH(launch_scan(cp, st));
+  return TKV_OK;
+}
+
+// exact k-th threshold of the heads of segments [s0, s1) (+ the exactness fallback: re-scan /
+// k-th of failing heads, tail-launched on device); the selected set of a head is
+// { candidates c : c >= meta_kth }, materialised by run_emit
+int run_kth_part(const tkv_problem* p, ScanParams cp, SelectParams sl, int64_t s0, int64_t s1, int part,
+                 cudaStream_t st) {
+  const int G = p->n_q_heads / p->n_kv_heads;
+  cp.seg_begin = s0;
+  cp.seg_count = s1 - s0;
   cp.fallback = 1;
+  sl.bh_begin = static_cast<int>(s0 * G);
+  sl.bh_count = static_cast<int>((s1 - s0) * G);
+  sl.hs.fb_launched += part;
   sl.fb_scan = cp;
   scan_launch_shape(cp, &sl.fb_scan_grid, &sl.fb_scan_smem);
   TKV_LAUNCH(launch_kth(sl, st));
+  return TKV_OK;
+}
+
+// Parts of the overlapped pipeline: the scan of part i+1 runs on the caller's stream while
+// the k-th selection and the V gather of part i run on a side stream beside it (both fit on
+// an SM next to the tcgen05 scan CTA). One part when the scan is too short to hide them.
+int pipeline_parts(const tkv_problem* p, bool tc) {
+  static const int env = [] {
+    const char* e = getenv("TKV_PARTS");
+    return e ? atoi(e) : 0;
+  }();
+  const int64_t nseg = static_cast<int64_t>(p->batch) * p->n_kv_heads;
+  int P;
+  const int forced = static_cast<int>((p->flags & TKV_F_PARTS_MASK) >> 8);
+  if (forced > 0) {
+    P = forced;
+  } else if (env > 0) {
+    P = env;
+  } else {
+    // measured on cfg3 (2.1 GB of keys): each extra scan launch costs ~12 us of fill/drain, more
+    // than the overlap hides, so one part; four parts only for very long scans (cfg5: 8.6 GB)
+    const double kbytes = static_cast<double>(nseg) * static_cast<double>(p->max_ctx) * kD * 2;
+    P = tc && !(p->flags & TKV_F_FUSED) && kbytes >= 4e9 ? 4 : 1;
+  }
+  if (P > nseg) P = static_cast<int>(nseg);
+  if (P > kMaxParts) P = kMaxParts;
+  return P < 1 ? 1 : P;
+}
+
+// per-thread, per-device side stream and fork/join events of the overlapped pipeline
+struct PipeRes {
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev[kMaxParts + 1] = {};
+};
+thread_local PipeRes g_pipe[16];
+
+int pipe_res(PipeRes** out) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 16) return fail(TKV_ECUDA, "device ordinal %d unsupported", dev);
+  PipeRes& r = g_pipe[dev];
+  if (!r.side) {
+    cudaError_t e = cudaStreamCreateWithFlags(&r.side, cudaStreamNonBlocking);
+    for (int i = 0; e == cudaSuccess && i <= kMaxParts; ++i) e = cudaEventCreateWithFlags(&r.ev[i], cudaEventDisableTiming);
+    if (e != cudaSuccess) return fail(TKV_ECUDA, "side stream / events: %s", cudaGetErrorString(e));
+  }
+  *out = &r;
   return TKV_OK;
 }
 
@@ -274,8 +345,11 @@ AttendParams make_attend(const tkv_problem* p, const void* q, const void* k_cach
 // gather + softmax fused when gather != 0; then the optional TopKResult-order sort.
 int run_emit(const tkv_problem* p, const void* q, const void* k_cache, const void* v_cache,
              const int32_t* n_ctx, const int32_t* n_win, int32_t* idx, float* scores,
-             uint64_t* packed, float* out, int gather, void* ws, const Layout& L, cudaStream_t st) {
+             uint64_t* packed, float* out, int gather, void* ws, const Layout& L, cudaStream_t st,
+             int bh_begin, int bh_count) {
   AttendParams a = make_attend(p, q, k_cache, v_cache, n_ctx, n_win, idx, scores, ws, L);
+  a.bh_begin = bh_begin;
+  a.bh_count = bh_count;
   a.idx_out = idx;
   a.scores_out = scores;
   a.packed_out = packed;
@@ -284,8 +358,8 @@ int run_emit(const tkv_problem* p, const void* q, const void* k_cache, const voi
   a.partial_only = 0;
   TKV_LAUNCH(launch_attend_cand(a, st));
   if (p->flags & TKV_F_SORTED) {
-    SortParams so{idx, scores, at<int32_t>(ws, L.mkb), p->k};
-    TKV_LAUNCH(launch_sort(so, p->batch * p->n_q_heads, st));
+    SortParams so{idx, scores, at<int32_t>(ws, L.mkb), p->k, bh_begin};
+    TKV_LAUNCH(launch_sort(so, bh_count, st));
   }
   return TKV_OK;
 }
@@ -296,8 +370,53 @@ int run_layer(const tkv_problem* p, const void* q, const void* k_cache, const vo
               const int32_t* n_ctx, const int32_t* n_win, int32_t* idx, float* scores,
               uint64_t* packed, float* out, int gather, void* ws, const Layout& L, cudaStream_t st) {
   if (!(p->flags & TKV_F_FUSED)) {
-    TRY(run_select(p, q, k_cache, n_ctx, ws, L, st));
-    return run_emit(p, q, k_cache, v_cache, n_ctx, n_win, idx, scores, packed, out, gather, ws, L, st);
+    ScanParams cp;
+    SelectParams sl;
+    TRY(run_prefix(p, q, k_cache, n_ctx, ws, L, st, &cp, &sl));
+    const int G = p->n_q_heads / p->n_kv_heads;
+    const int64_t nseg = static_cast<int64_t>(p->batch) * p->n_kv_heads;
+    const int P = pipeline_parts(p, use_tc_scan(p, cp));
+    const bool prof = g_scan_start && g_scan_stop;
+    if (P == 1) {
+      if (prof) cudaEventRecord(g_scan_start, st);
+      TRY(run_scan_part(p, cp, 0, nseg, st));
+      if (prof) cudaEventRecord(g_scan_stop, st);
+      TRY(run_kth_part(p, cp, sl, 0, nseg, 0, st));
+      return run_emit(p, q, k_cache, v_cache, n_ctx, n_win, idx, scores, packed, out, gather, ws, L, st, 0,
+                      static_cast<int>(nseg * G));
+    }
+    PipeRes* r = nullptr;
+    TRY(pipe_res(&r));
+    static const bool serial = [] {  // diagnostics: split scans, no overlap
+      const char* e = getenv("TKV_PIPE_SERIAL");
+      return e && atoi(e) != 0;
+    }();
+    if (serial) {
+      if (prof) cudaEventRecord(g_scan_start, st);
+      for (int part = 0; part < P; ++part) TRY(run_scan_part(p, cp, nseg * part / P, nseg * (part + 1) / P, st));
+      if (prof) cudaEventRecord(g_scan_stop, st);
+      for (int part = 0; part < P; ++part) {
+        const int64_t s0 = nseg * part / P, s1 = nseg * (part + 1) / P;
+        TRY(run_kth_part(p, cp, sl, s0, s1, part, st));
+        TRY(run_emit(p, q, k_cache, v_cache, n_ctx, n_win, idx, scores, packed, out, gather, ws, L, st,
+                     static_cast<int>(s0 * G), static_cast<int>((s1 - s0) * G)));
+      }
+      return TKV_OK;
+    }
+    if (prof) cudaEventRecord(g_scan_start, st);
+    for (int part = 0; part < P; ++part) {
+      const int64_t s0 = nseg * part / P, s1 = nseg * (part + 1) / P;
+      TRY(run_scan_part(p, cp, s0, s1, st));
+      if (cudaEventRecord(r->ev[part], st) != cudaSuccess || cudaStreamWaitEvent(r->side, r->ev[part], 0) != cudaSuccess)
+        return fail(TKV_ECUDA, "pipeline fork failed");
+      TRY(run_kth_part(p, cp, sl, s0, s1, part, r->side));
+      TRY(run_emit(p, q, k_cache, v_cache, n_ctx, n_win, idx, scores, packed, out, gather, ws, L, r->side,
+                   static_cast<int>(s0 * G), static_cast<int>((s1 - s0) * G)));
+    }
+    if (prof) cudaEventRecord(g_scan_stop, st);
+    if (cudaEventRecord(r->ev[P], r->side) != cudaSuccess || cudaStreamWaitEvent(st, r->ev[P], 0) != cudaSuccess)
+      return fail(TKV_ECUDA, "pipeline join failed");
+    return TKV_OK;
   }
   FusedParams f{};
   f.a = make_attend(p, q, k_cache, v_cache, n_ctx, n_win, idx, scores, ws, L);
@@ -338,7 +457,7 @@ int run_layer(const tkv_problem* p, const void* q, const void* k_cache, const vo
   TKV_LAUNCH(launch_fused(f, st));
   if (g_scan_start && g_scan_stop) cudaEventRecord(g_scan_stop, st);
   if (p->flags & TKV_F_SORTED) {
-    SortParams so{idx, scores, at<int32_t>(ws, L.mkb), p->k};
+    SortParams so{idx, scores, at<int32_t>(ws, L.mkb), p->k, 0};
     TKV_LAUNCH(launch_sort(so, p->batch * p->n_q_heads, st));
   }
   return TKV_OK;

@@ -54,9 +54,9 @@ __global__ void __launch_bounds__(NT) attend_cand_kernel(AttendParams p) {
   __shared__ AttSmem sm;
   extern __shared__ uint32_t s_pref[];  // [B*Hq + 1] work-item prefix over heads
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int BH = p.B * p.Hq;
-  auto nslots_of = [&](int bh) -> int {
-    int64_t n = p.cand_cnt[bh];
+  const int BH = p.bh_count ? p.bh_count : p.B * p.Hq;  // heads [bh_begin, bh_begin + BH)
+  auto nslots_of = [&](int lh) -> int {
+    int64_t n = p.cand_cnt[p.bh_begin + lh];
     if (n > p.cap) n = p.cap;
     const int c = static_cast<int>((n + kCandChunk - 1) / kCandChunk);
     return c > 0 ? c : 1;  // every head gets >= 1 item so its output is always finalized
@@ -93,14 +93,14 @@ __global__ void __launch_bounds__(NT) attend_cand_kernel(AttendParams p) {
   const uint32_t total = s_pref[BH];
   const float zs = p.scale * kLog2e;
   for (uint32_t item = blockIdx.x; item < total; item += gridDim.x) {
-    int lo = 0, hi = BH;  // largest bh with s_pref[bh] <= item
+    int lo = 0, hi = BH;  // largest local head with s_pref[lh] <= item
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
       if (s_pref[mid] <= item) lo = mid; else hi = mid;
     }
-    const int bh = lo;
-    const int slot = static_cast<int>(item - s_pref[bh]);
-    const int nslots = static_cast<int>(s_pref[bh + 1] - s_pref[bh]);
+    const int bh = p.bh_begin + lo;
+    const int slot = static_cast<int>(item - s_pref[lo]);
+    const int nslots = static_cast<int>(s_pref[lo + 1] - s_pref[lo]);
     const int b = bh / p.Hq;
     int64_t n = p.cand_cnt[bh];
     if (n > p.cap) n = p.cap;
@@ -218,14 +218,17 @@ cudaError_t launch_attend(const AttendParams& p, cudaStream_t s) {
 cudaError_t launch_attend_cand(const AttendParams& p, cudaStream_t s) {
   static int grid = 0;
   if (!grid) {
+    // same shared-memory carveout as the scan, so both can share an SM (parts pipeline)
+    cudaFuncSetAttribute(attend_cand_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, attend_cand_kernel, NT, 8192);
     grid = sms * (per > 0 ? per : 1);
   }
-  const size_t smem = (static_cast<size_t>(p.B) * p.Hq + 1) * sizeof(uint32_t);
-  attend_cand_kernel<<<grid, NT, smem, s>>>(p);
+  const size_t nbh = p.bh_count ? static_cast<size_t>(p.bh_count) : static_cast<size_t>(p.B) * p.Hq;
+  attend_cand_kernel<<<grid, NT, (nbh + 1) * sizeof(uint32_t), s>>>(p);
   return cudaGetLastError();
 }
 

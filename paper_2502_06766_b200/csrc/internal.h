@@ -19,12 +19,15 @@ constexpr int kSelectThreads = 1024;
 constexpr int kSelectBucketCap = 8192;  // threshold-bucket candidates refined in shared memory
 constexpr int kKthThreads = 512;        // kth_kernel CTA
 constexpr int kKthCtas = 4;             // kth_kernel CTAs per (b, q head)
+constexpr int kKthSmemBucket = 2048;    // threshold-bucket members rank-selected in shared memory
+constexpr int kKthSmem = kKthSmemBucket * 8;  // kth_kernel dynamic shared memory (fits beside the scan)
 constexpr int kAttendThreads = 256;
 constexpr int kAttendChunk = 512;    // selected rows per gather CTA (list mode)
 constexpr int kCandChunk = 1024;     // candidates per work item (candidate mode)
 constexpr int kSortMax = 16384;      // sorted output supported up to this k
 constexpr uint32_t kNoFilterShift = 20;  // histogram shift when every score is a candidate
 constexpr int kMinSampleStride = 8;      // small contexts sample at most every 8th row
+constexpr int kMaxParts = 16;            // KV-group parts of the overlapped layer pipeline
 
 // rows between two sampled rows: up to kSamples samples, never denser than 1 in 8
 __host__ __device__ inline int64_t sample_stride(int64_t n) {
@@ -45,7 +48,8 @@ struct HeadState {
   uint64_t* bkt;         // [B*Hq][kSelectBucketCap] threshold-bucket candidates
   uint32_t* kth_ticket;  // [B*Hq] kth_kernel CTAs done (self-resetting)
   uint32_t* out_cnt;     // [B*Hq] selected rows written so far (reset by threshold_kernel)
-  uint32_t* fb_launched; // [1] the exactness fallback has been tail-launched for this call
+  uint32_t* fb_launched; // the exactness fallback has been tail-launched for this call (one flag
+                         // per pipeline part; the part's SelectParams points at its own)
 };
 
 struct SampleParams {
@@ -71,6 +75,7 @@ struct ScanParams {
   int64_t cap;
   HeadState hs;
   int fallback;
+  int64_t seg_begin, seg_count;  // (b, kv head) segments to scan; seg_count 0 = all B*Hkv
 };
 
 enum SelectPass { kPassMain = 0, kPassFallback = 1, kPassMerge = 2 };
@@ -90,6 +95,7 @@ struct SelectParams {
   HeadState hs;
   uint64_t* packed_out;  // optional [B*Hq*k] composites (shard candidates)
   int pass;
+  int bh_begin, bh_count;  // heads handled (kth_kernel); bh_count 0 = all B*Hq
   // exactness fallback, tail-launched by kth_kernel (main pass) when a head failed
   ScanParams fb_scan;
   int fb_scan_grid;
@@ -104,6 +110,7 @@ struct SortParams {
   float* scores;
   const int32_t* meta_kb;
   int k;
+  int bh_begin;
 };
 
 struct AttendParams {
@@ -141,6 +148,7 @@ struct AttendParams {
   float* scores_out;
   uint64_t* packed_out;
   int gather;  // 0: only write the selected rows (no attention)
+  int bh_begin, bh_count;  // heads handled by attend_cand_kernel; bh_count 0 = all B*Hq
 };
 
 struct AppendParams {

@@ -206,7 +206,7 @@ void scan_launch_shape(const ScanParams& p, int* grid, int* smem_bytes) {
     attr_set = true;
   }
   const int64_t tps = (p.max_ctx + kScanRows - 1) / kScanRows;
-  const int64_t total = static_cast<int64_t>(p.B) * p.Hkv * tps;
+  const int64_t total = (p.seg_count ? p.seg_count : static_cast<int64_t>(p.B) * p.Hkv) * tps;
   int g = scan_grid(p.G, smem);
   if (total < g) g = static_cast<int>(total > 0 ? total : 1);
   *grid = g;
@@ -222,7 +222,7 @@ cudaError_t launch_scan(const ScanParams& p, cudaStream_t s) {
     attr_set = true;
   }
   const int64_t tps = (p.max_ctx + kScanRows - 1) / kScanRows;
-  const int64_t total = static_cast<int64_t>(p.B) * p.Hkv * tps;
+  const int64_t total = (p.seg_count ? p.seg_count : static_cast<int64_t>(p.B) * p.Hkv) * tps;
   if (total == 0) return cudaSuccess;
   int grid = scan_grid(p.G, smem);
   if (total < grid) grid = static_cast<int>(total);

@@ -48,7 +48,8 @@ __device__ __forceinline__ void scan_body(const ScanParams& p, uint64_t* s_buf, 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, c = lane & 3;
   const int64_t tps = (p.max_ctx + kScanRows - 1) / kScanRows;
-  const int64_t total = static_cast<int64_t>(p.B) * p.Hkv * tps;
+  const int64_t nseg = p.seg_count ? p.seg_count : static_cast<int64_t>(p.B) * p.Hkv;
+  const int64_t total = nseg * tps;
   const int64_t t0 = total * blockIdx.x / gridDim.x;
   const int64_t t1 = total * (blockIdx.x + 1) / gridDim.x;
   if (tid < 8) s_cnt[tid] = 0u;
@@ -63,7 +64,8 @@ __device__ __forceinline__ void scan_body(const ScanParams& p, uint64_t* s_buf, 
   const int col0 = 2 * c, col1 = 2 * c + 1;
 
   for (int64_t t = t0; t < t1; ++t) {
-    const int64_t seg = t / tps;
+    const int64_t lseg = t / tps;  // segment index inside [seg_begin, seg_begin + nseg)
+    const int64_t seg = p.seg_begin + lseg;
     if (seg != st.seg) {
       if (st.seg >= 0) scan_flush(p, st, s_buf, s_cnt, warp, lane);
       since = 0;
@@ -73,7 +75,7 @@ __device__ __forceinline__ void scan_body(const ScanParams& p, uint64_t* s_buf, 
       st.nctx = p.n_ctx[st.b];
       st.active = !p.fallback || p.hs.group_fail[seg] != 0u;
       if (!st.active) {
-        t = (seg + 1) * tps - 1;  // skip the rest of this segment (CTA-uniform)
+        t = (lseg + 1) * tps - 1;  // skip the rest of this segment (CTA-uniform)
         continue;
       }
       load_qfrag(f, p.q + (static_cast<int64_t>(st.b) * p.Hq + st.kvh * p.G) * kD, p.G, lane);
@@ -84,7 +86,7 @@ __device__ __forceinline__ void scan_body(const ScanParams& p, uint64_t* s_buf, 
       thr0 = col0 < p.G ? p.hs.thr[bh0 + col0] : 0u;
       thr1 = col1 < p.G ? p.hs.thr[bh0 + col1] : 0u;
     }
-    const int64_t tile = t - seg * tps;
+    const int64_t tile = t - lseg * tps;
     const int64_t rbase = tile * kScanRows + warp * 16 * kScanU;
     if (rbase < st.nctx) {  // warp-uniform
       uint4 a[kScanU][2][4];

@@ -49,7 +49,7 @@ constexpr int kTcQBytes = kTcN * kD * 2;           // 2 KB: one 8-row swizzle at
 constexpr int kTcEpiWarps = 4;
 constexpr int kTcThreads = 64 + 32 * kTcEpiWarps;
 constexpr int kTcWarpRows = kTcUnit / 4;           // rows per unit one epilogue warp handles
-constexpr int kTcMaxFlush = 8;                     // units between a warp's flushes (measured flat from 4 to 16)
+constexpr int kTcMaxFlush = 4;  // units between a warp's flushes (flat from 4 to 16; 4 leaves room beside the CTA)
 constexpr int kTcSmemLimit = 227 * 1024 - 512;     // opt-in maximum minus the static barriers
 
 static_assert(kTcTmemCols >= kTcAcc * kTcAccCols, "TMEM allocation too small");
@@ -276,9 +276,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) scan_tc_kernel(const __grid_con
   const uint32_t tmem = s_tmem;
 
   const int64_t ups = (p.max_ctx + kTcUnit - 1) / kTcUnit;
-  const int64_t total = static_cast<int64_t>(p.B) * p.Hkv * ups;
+  const int64_t total = (p.seg_count ? p.seg_count : static_cast<int64_t>(p.B) * p.Hkv) * ups;
+  const int64_t ubase = p.seg_begin * ups;  // units of the segment range [seg_begin, +seg_count)
   UnitWalk w;
-  w.init(p, total * blockIdx.x / gridDim.x, total * (blockIdx.x + 1) / gridDim.x, ups);
+  w.init(p, ubase + total * blockIdx.x / gridDim.x, ubase + total * (blockIdx.x + 1) / gridDim.x, ups);
   bool new_seg = false;
 
   if (warp == 0) {
@@ -437,7 +438,7 @@ bool scan_tc_supported(const ScanParams& p) {
 
 cudaError_t launch_scan_tc(const ScanParams& p, cudaStream_t s) {
   const int64_t ups = (p.max_ctx + kTcUnit - 1) / kTcUnit;
-  const int64_t total = static_cast<int64_t>(p.B) * p.Hkv * ups;
+  const int64_t total = (p.seg_count ? p.seg_count : static_cast<int64_t>(p.B) * p.Hkv) * ups;
   if (total == 0) return cudaSuccess;
   CUtensorMap map;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(kD),
@@ -473,7 +474,10 @@ cudaError_t launch_scan_tc(const ScanParams& p, cudaStream_t s) {
   const size_t smem = tc_smem_bytes(p.G, sh);
   static bool attr_set = false;
   if (!attr_set) {
-    const cudaError_t e = cudaFuncSetAttribute(scan_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmemLimit);
+    cudaError_t e = cudaFuncSetAttribute(scan_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmemLimit);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(scan_tc_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }

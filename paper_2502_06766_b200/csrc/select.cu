@@ -322,14 +322,14 @@ __global__ void __launch_bounds__(kScanWarps * 32, 2) fb_scan_kernel(ScanParams 
 //   8-bit radix over the 64-bit composites → exact lower-id tie resolution).
 __global__ void __launch_bounds__(kKthThreads) kth_kernel(SelectParams p) {
   constexpr int KT = kKthThreads, KW = KT / 32;
-  extern __shared__ uint64_t s_bkt[];  // [kSelectBucketCap]
+  extern __shared__ uint64_t s_bkt[];  // [kKthSmemBucket]
   __shared__ __align__(16) uint32_t s_hist[kHistBins];
   __shared__ uint32_t s_scr[32];
   __shared__ uint32_t s_out[2];
   __shared__ uint64_t s_rmax[KW];
   __shared__ int s_last;
 
-  const int bh = blockIdx.y, part = blockIdx.x, P = gridDim.x;
+  const int bh = p.bh_begin + blockIdx.y, part = blockIdx.x, P = gridDim.x;
   const int b = bh / p.Hq, h = bh % p.Hq;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (p.pass == kPassFallback && p.hs.flag_fail[bh] == 0u) return;
@@ -361,8 +361,8 @@ __global__ void __launch_bounds__(kKthThreads) kth_kernel(SelectParams p) {
           fb_scan_kernel<<<p.fb_scan_grid, kScanWarps * 32, p.fb_scan_smem, cudaStreamTailLaunch>>>(p.fb_scan);
           SelectParams f = p;
           f.pass = kPassFallback;
-          kth_kernel<<<dim3(kKthCtas, p.B * p.Hq), kKthThreads,
-                       kSelectBucketCap * static_cast<int>(sizeof(uint64_t)), cudaStreamTailLaunch>>>(f);
+          kth_kernel<<<dim3(kKthCtas, p.bh_count ? p.bh_count : p.B * p.Hq), kKthThreads, kKthSmem,
+                       cudaStreamTailLaunch>>>(f);
         }
 #endif
       }
@@ -455,15 +455,15 @@ __global__ void __launch_bounds__(kKthThreads) kth_kernel(SelectParams p) {
     uint64_t cp = 0;
     if (!big) {
       const int64_t nb = __ldcg(&p.hs.bkt_cnt[bh]);
-      for (int64_t i = tid; i < nb; i += KT) s_bkt[i] = __ldcg(&gbkt[i]);
-      __syncthreads();
-      if (nb <= 2048) {  // typical: a few hundred → rank counting, two barriers
+      if (nb <= kKthSmemBucket) {  // typical: a few hundred → rank counting in shared memory
+        for (int64_t i = tid; i < nb; i += KT) s_bkt[i] = __ldcg(&gbkt[i]);
+        __syncthreads();
         __shared__ uint64_t s_res;
         cp = block_rank_select<KT>(s_bkt, static_cast<int>(nb), static_cast<int>(need), &s_res);
         cs = 0;
-      } else {
+      } else {  // large bucket: radix passes over the global copy
         auto ld = [&](int64_t i, uint64_t& c) {
-          c = s_bkt[i];
+          c = __ldcg(&gbkt[i]);
           return true;
         };
         radix_select_u64<KT>(ld, nb, need, s_hist, s_scr, s_out, cs, cp);
@@ -506,13 +506,12 @@ void prepare_fallback_kernels() {
 
 cudaError_t launch_kth(const SelectParams& p, cudaStream_t s) {
   prepare_fallback_kernels();
-  const int smem = kSelectBucketCap * static_cast<int>(sizeof(uint64_t));
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
+  static bool carve = false;
+  if (!carve) {  // same shared-memory carveout as the scan, so both can share an SM (parts pipeline)
+    cudaFuncSetAttribute(kth_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    carve = true;
   }
-  kth_kernel<<<dim3(kKthCtas, p.B * p.Hq), kKthThreads, smem, s>>>(p);
+  kth_kernel<<<dim3(kKthCtas, p.bh_count ? p.bh_count : p.B * p.Hq), kKthThreads, kKthSmem, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -521,7 +520,7 @@ cudaError_t launch_kth(const SelectParams& p, cudaStream_t s) {
 // of the kb selected rows in shared memory.
 __global__ void __launch_bounds__(NT) sort_kernel(SortParams p) {
   extern __shared__ uint64_t s_c[];
-  const int bh = blockIdx.x;
+  const int bh = p.bh_begin + blockIdx.x;
   const int kb = p.meta_kb[bh];
   if (kb <= 1) return;
   int P = 1;

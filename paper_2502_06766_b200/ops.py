@@ -44,7 +44,7 @@ def make_problem(B: int, Hq: int, Hkv: int, cache_rows: int, max_ctx: int, k: in
                  pinned_prefix: int = 0, scale: float | None = None, combine: str = "joint",
                  sorted: bool = False, no_filter: bool = False, row_offset: int = 0,
                  head_dim: int = HEAD_DIM, fused: bool = False,
-                 tc_scan: bool | None = None) -> _lib.Problem:
+                 tc_scan: bool | None = None, parts: int = 0) -> _lib.Problem:
     p = _lib.Problem()
     p.batch, p.n_q_heads, p.n_kv_heads, p.head_dim = B, Hq, Hkv, head_dim
     p.cache_rows, p.max_ctx, p.k = cache_rows, max_ctx, k
@@ -57,6 +57,9 @@ def make_problem(B: int, Hq: int, Hkv: int, cache_rows: int, max_ctx: int, k: in
         tc_scan = os.environ.get("TKV_SCAN", "") != "hmma"
     if not tc_scan:
         p.flags |= _lib.F_SCAN_HMMA
+    if not 0 <= parts <= 15:
+        raise ConfigError("parts must be in 0..15 (0 = automatic)")
+    p.flags |= parts << _lib.F_PARTS_SHIFT
     p.row_offset = row_offset
     return p
 
@@ -148,7 +151,7 @@ def topk_decode_attention(q, k_cache, v_cache, n_ctx, k: int, *, n_win=None, sca
                           combine: str = "joint", pinned_prefix: int = 0, sorted: bool = False,
                           max_ctx: int | None = None, no_filter: bool = False, row_offset: int = 0,
                           out=None, idx=None, scores=None, workspace: Workspace | None = None,
-                          fused: bool = False, tc_scan: bool | None = None):
+                          fused: bool = False, tc_scan: bool | None = None, parts: int = 0):
     """Exact top-k decode attention for every (batch, q head) of one layer.
 
     q [B, Hq, 128] bf16; k_cache/v_cache [B, Hkv, rows, 128] bf16 with the context in rows
@@ -166,7 +169,7 @@ def topk_decode_attention(q, k_cache, v_cache, n_ctx, k: int, *, n_win=None, sca
         max_ctx = s.cache_rows if isinstance(n_ctx, torch.Tensor) else int(n_ctx_t.max().item())
     prob = make_problem(s.B, s.Hq, s.Hkv, s.cache_rows, max_ctx, k, pinned_prefix=pinned_prefix,
                         scale=scale, combine=combine, sorted=sorted, no_filter=no_filter,
-                        row_offset=row_offset, fused=fused, tc_scan=tc_scan)
+                        row_offset=row_offset, fused=fused, tc_scan=tc_scan, parts=parts)
     ws = workspace or workspace_for(prob, dev)
     out = out if out is not None else torch.empty((s.B, s.Hq, HEAD_DIM), dtype=torch.float32, device=dev)
     idx = idx if idx is not None else torch.empty((s.B, s.Hq, k), dtype=torch.int32, device=dev)
@@ -179,7 +182,7 @@ def topk_decode_attention(q, k_cache, v_cache, n_ctx, k: int, *, n_win=None, sca
 
 def topk_search(q, k_cache, n_ctx, k: int, *, sorted: bool = True, max_ctx: int | None = None,
                 no_filter: bool = False, row_offset: int = 0, workspace: Workspace | None = None,
-                fused: bool = False, tc_scan: bool | None = None):
+                fused: bool = False, tc_scan: bool | None = None, parts: int = 0):
     """Exact top-k rows per (batch, q head) without attention (knn_search flat, ann.py:203-218).
 
     Returns (idx [B, Hq, k] int32, scores [B, Hq, k] f32), TopKResult-ordered when sorted.
@@ -192,7 +195,8 @@ def topk_search(q, k_cache, n_ctx, k: int, *, sorted: bool = True, max_ctx: int 
     if max_ctx is None:
         max_ctx = s.cache_rows if isinstance(n_ctx, torch.Tensor) else int(n_ctx_t.max().item())
     prob = make_problem(s.B, s.Hq, s.Hkv, s.cache_rows, max_ctx, k, sorted=sorted,
-                        no_filter=no_filter, row_offset=row_offset, fused=fused, tc_scan=tc_scan)
+                        no_filter=no_filter, row_offset=row_offset, fused=fused, tc_scan=tc_scan,
+                        parts=parts)
     ws = workspace or workspace_for(prob, dev)
     idx = torch.empty((s.B, s.Hq, k), dtype=torch.int32, device=dev)
     scores = torch.empty((s.B, s.Hq, k), dtype=torch.float32, device=dev)

@@ -100,3 +100,63 @@ def test_tc_scan_repeated_and_graph(cuda):
         g.replay()
     torch.cuda.synchronize()
     assert same(idx_g, ref[1]) and float((out_g - ref[0]).abs().max()) < 1e-5
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,N,k,parts", [
+    (1, 32, 8, 16384, 256, 4),
+    (2, 8, 4, 5000, 300, 3),     # uneven split of 8 segments, ragged below
+    (1, 16, 2, 5000, 1, 2),
+])
+def test_overlapped_parts_parity(cuda, B, Hq, Hkv, N, k, parts):
+    """The part-overlapped pipeline (scan of part i+1 beside k-th + gather of part i on a side
+    stream) is exact, for every head range, also with sorted output and a window."""
+    rng = np.random.default_rng(4000 + N + parts)
+    q, K, V = _make(rng, B, Hq, Hkv, N + 8)
+    n_ctx = [N] + [N - 777] * (B - 1)
+    n_win = [3] * B
+    out, idx, sc = _run(q, K, V, n_ctx, k, cuda, n_win=n_win, parts=parts, sorted=True)
+    torch.cuda.synchronize()
+    _check(q, K, V, n_ctx, k, out, idx, sc, n_win=n_win)
+    out1, idx1, _ = _run(q, K, V, n_ctx, k, cuda, n_win=n_win, parts=1, sorted=True)
+    torch.cuda.synchronize()
+    assert torch.equal(idx, idx1)  # sorted: identical order
+    assert float((out - out1).abs().max()) < 1e-5
+
+
+def test_overlapped_parts_fallback_and_graph(cuda):
+    """A failing head in a later part triggers that part's own device-side fallback; the whole
+    overlapped layer is capturable in a CUDA graph (fork/join events)."""
+    from oracle import oracle as O
+    from paper_2502_06766_b200 import ops
+
+    rng = np.random.default_rng(19)
+    B, Hq, Hkv, N, k = 1, 16, 4, 65536, 2048
+    q, K, V = _make(rng, B, Hq, Hkv, N)
+    K = O.to_bf16_f32(K * 0.01)
+    stride = -(-N // 4096)
+    # adversarial sample for kv head 3 only (the last part)
+    K[0, 3, ::stride] = O.to_bf16_f32(np.sign(q[0, 12])[None, :] * 2.0 + K[0, 3, ::stride])
+    out, idx, sc = _run(q, K, V, [N], k, cuda, parts=4)
+    torch.cuda.synchronize()
+    _check(q, K, V, [N], k, out, idx, sc)
+    qd, Kd, Vd = _dev(q, cuda), _dev(K, cuda), _dev(V, cuda)
+    n = torch.tensor([N], dtype=torch.int32, device=cuda)
+    prob = ops.make_problem(B, Hq, Hkv, N, N, k, parts=4)
+    ws = ops.Workspace(prob, cuda)
+    out_g = torch.empty_like(out)
+    idx_g = torch.empty_like(idx)
+    sc_g = torch.empty_like(sc)
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        ops.topk_decode_attention(qd, Kd, Vd, n, k, workspace=ws, max_ctx=N, parts=4, out=out_g, idx=idx_g,
+                                  scores=sc_g)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g):
+            ops.topk_decode_attention(qd, Kd, Vd, n, k, workspace=ws, max_ctx=N, parts=4, out=out_g,
+                                      idx=idx_g, scores=sc_g)
+    for _ in range(3):
+        out_g.zero_()
+        g.replay()
+    torch.cuda.synchronize()
+    _check(q, K, V, [N], k, out_g, idx_g, sc_g)
