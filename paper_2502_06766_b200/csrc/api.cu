@@ -449,12 +449,24 @@ int run_layer(const tkv_problem* p, const void* q, const void* k_cache, const vo
     f.tile_iters >>= 1;
   f.T = static_cast<int>((p->max_ctx + f.tile_iters * kScanRows - 1) / (f.tile_iters * kScanRows));
   f.KS = kFusedKS;
+  f.scan_target = f.T;
+  f.scan_flush_iters = 4;
   int ka = (2 * grid + NH - 1) / NH;
+  static const int ka_env = [] {  // experiments: attend items per head
+    const char* e = getenv("TKV_KA");
+    return e ? atoi(e) : 0;
+  }();
+  const bool tc_fused = !(p->flags & TKV_F_SCAN_HMMA) && fused_tc_supported(f);
+  if (tc_fused) ka = (256 + NH - 1) / NH;  // tc kernel: 8 per head at NH = 32 (measured 8 > 4, 16)
+  if (ka_env > 0) ka = ka_env;
   f.KA = ka < 1 ? 1 : (ka > 16 ? 16 : ka);
   f.trace = g_trace;
   f.trace_cap = g_trace_cap;
   if (g_scan_start && g_scan_stop) cudaEventRecord(g_scan_start, st);
-  TKV_LAUNCH(launch_fused(f, st));
+  if (tc_fused)
+    TKV_LAUNCH(launch_fused_tc(f, st));
+  else
+    TKV_LAUNCH(launch_fused(f, st));
   if (g_scan_start && g_scan_stop) cudaEventRecord(g_scan_stop, st);
   if (p->flags & TKV_F_SORTED) {
     SortParams so{idx, scores, at<int32_t>(ws, L.mkb), p->k, 0};

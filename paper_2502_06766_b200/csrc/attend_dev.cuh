@@ -16,10 +16,11 @@ constexpr int NW = NT / 32;
 // h. State (m, l, o) in the log2-scaled domain; thread t accumulates o for d = t % 128 over rows
 // of parity t / 128. With `pinned`, a row is skipped when it is among the selected top-k
 // (composite >= kth).
+template <class Gp = CtaGrp>
 __device__ void accumulate_rows(const AttendParams& p, int b, int h, int kvh, int64_t r_begin,
                                 int64_t r_end, bool pinned, uint64_t kth, float& m, float& l,
                                 float& o, float* s_z, float* s_scr) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = Gp::tid(), lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, c = lane & 3;
   const int n = h - kvh * p.G;
   const float zs = p.scale * kLog2e;
@@ -47,11 +48,11 @@ __device__ void accumulate_rows(const AttendParams& p, int b, int h, int kvh, in
         s_z[warp * 16 + g + 8] = okB ? sB * zs : -INFINITY;
       }
     }
-    __syncthreads();
+    Gp::sync();
     float v = tid < 128 ? s_z[tid] : -INFINITY;
     v = warp_max(v);
     if (lane == 0) s_scr[warp] = v;
-    __syncthreads();
+    Gp::sync();
     float cm = -INFINITY;
 #pragma unroll
     for (int w = 0; w < 4; ++w) cm = fmaxf(cm, s_scr[w]);
@@ -70,12 +71,13 @@ __device__ void accumulate_rows(const AttendParams& p, int b, int h, int kvh, in
       o = o * fold + osum;
       m = mn;
     }
-    __syncthreads();
+    Gp::sync();
   }
 }
 
 // Pinned-prefix rows [0, p) that the top-k did not select join the context softmax
 // (attention.py:152-154 unions them into the retrieved ids). Local rows of this shard only.
+template <class Gp = CtaGrp>
 __device__ void add_pinned(const AttendParams& p, int b, int h, int kvh, int64_t nctx, int kb,
                            float zref, float& l, float& o, float* s_z, float* s_scr) {
   if (p.pinned <= 0 || kb <= 0) return;
@@ -86,22 +88,23 @@ __device__ void add_pinned(const AttendParams& p, int b, int h, int kvh, int64_t
   if (hi <= lo) return;
   const int bh = b * p.Hq + h;
   float m = zref;
-  accumulate_rows(p, b, h, kvh, lo, hi, true, __ldcg(&p.meta_kth[bh]), m, l, o, s_z, s_scr);
+  accumulate_rows<Gp>(p, b, h, kvh, lo, hi, true, __ldcg(&p.meta_kth[bh]), m, l, o, s_z, s_scr);
   // every unselected row scores <= the k-th selected score <= M, so m stays zref
 }
 
 // Window rows + normalisation. Inputs: context state (zref, l_c, o_c) where o_c is this
 // thread's share (d = tid % 128, parity tid / 128). Writes out[bh, :].
+template <class Gp = CtaGrp>
 __device__ void finalize_head(const AttendParams& p, int b, int h, int kvh, int64_t nctx, float zref,
                               float l_c, float o_c, float* s_z, float* s_scr, float* s_o) {
-  const int tid = threadIdx.x;
+  const int tid = Gp::tid();
   const int bh = b * p.Hq + h;
   // precondition n_ctx + n_win <= cache_rows (tkv.h); a window past the cache is clamped
   // rather than read from the next head's rows
   int64_t nwin = p.n_win ? p.n_win[b] : 0;
   if (nwin > p.cache_rows - nctx) nwin = p.cache_rows - nctx;
   float m_w = -INFINITY, l_w = 0.f, o_w = 0.f;
-  if (nwin > 0) accumulate_rows(p, b, h, kvh, nctx, nctx + nwin, false, 0ull, m_w, l_w, o_w, s_z, s_scr);
+  if (nwin > 0) accumulate_rows<Gp>(p, b, h, kvh, nctx, nctx + nwin, false, 0ull, m_w, l_w, o_w, s_z, s_scr);
   float val;
   if (p.combine == 0) {  // joint (attention.py:109-114)
     const float mm = fmaxf(l_c > 0.f ? zref : -INFINITY, m_w);
@@ -113,7 +116,7 @@ __device__ void finalize_head(const AttendParams& p, int b, int h, int kvh, int6
     val = (l_c > 0.f ? o_c / l_c : 0.f) + (l_w > 0.f ? o_w / l_w : 0.f);
   }
   s_o[tid] = val;
-  __syncthreads();
+  Gp::sync();
   if (tid < kD) p.out[static_cast<int64_t>(bh) * kD + tid] = s_o[tid] + s_o[tid + kD];
 }
 
@@ -132,9 +135,10 @@ struct AttSmem {
 
 // Gather the V rows listed in sm.row (local rows, -1 = skip) weighted by sm.w and reduce them
 // into the head's partial slot (l, o[128]). Ends with a barrier (smem reusable).
+template <class Gp = CtaGrp>
 __device__ void gather_partial(const AttendParams& p, int bh, int slot, int nrows, AttSmem& sm) {
   const int b = bh / p.Hq, h = bh % p.Hq, kvh = h / p.G;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = Gp::tid(), lane = tid & 31, warp = tid >> 5;
   const int half = lane >> 4, part = lane & 15;
   const __nv_bfloat16* vb =
       p.vc + (static_cast<int64_t>(b) * p.Hkv + kvh) * p.cache_rows * kD + part * 8;
@@ -174,7 +178,7 @@ __device__ void gather_partial(const AttendParams& p, int bh, int slot, int nrow
   for (int i = tid; i < nrows; i += NT) lw += sm.w[i];
   lw = warp_sum(lw);
   if (lane == 0) sm.l[warp] = lw;
-  __syncthreads();
+  Gp::sync();
   if (tid < kD) {
     float o = 0.f;
 #pragma unroll
@@ -187,15 +191,16 @@ __device__ void gather_partial(const AttendParams& p, int bh, int slot, int nrow
     for (int w2 = 0; w2 < NW; ++w2) l += sm.l[w2];
     p.part_l[static_cast<int64_t>(bh) * p.nchunks + slot] = l;
   }
-  __syncthreads();
+  Gp::sync();
 }
 
 // The last CTA of a head (caller decided, after a __threadfence): combine the nslots partials
 // in slot order (deterministic), add the unselected pinned-prefix rows and the window, write out
 // (or the (l, o) partial in sharded mode).
+template <class Gp = CtaGrp>
 __device__ void head_finish(const AttendParams& p, int bh, int nslots, AttSmem& sm) {
   const int b = bh / p.Hq, h = bh % p.Hq, kvh = h / p.G;
-  const int tid = threadIdx.x;
+  const int tid = Gp::tid();
   const int kb = __ldcg(&p.meta_kb[bh]);
   const float zref = kb > 0 ? __ldcg(&p.meta_max[bh]) * p.scale * kLog2e : 0.f;
   const int64_t nctx = p.n_ctx[b];
@@ -204,31 +209,32 @@ __device__ void head_finish(const AttendParams& p, int bh, int nslots, AttSmem& 
     if (tid < kD) o_c += __ldcg(&p.part_o[(static_cast<int64_t>(bh) * p.nchunks + c2) * kD + tid]);
     l_c += __ldcg(&p.part_l[static_cast<int64_t>(bh) * p.nchunks + c2]);
   }
-  add_pinned(p, b, h, kvh, nctx, kb, zref, l_c, o_c, sm.z, sm.scr);
+  add_pinned<Gp>(p, b, h, kvh, nctx, kb, zref, l_c, o_c, sm.z, sm.scr);
   if (p.partial_only) {
     sm.o[tid] = o_c;
-    __syncthreads();
+    Gp::sync();
     float* dst = p.partial_out + static_cast<int64_t>(bh) * (kD + 1);
     if (tid == 0) dst[0] = l_c;
     if (tid < kD) dst[1 + tid] = sm.o[tid] + sm.o[tid + kD];
-    __syncthreads();
+    Gp::sync();
     return;
   }
-  finalize_head(p, b, h, kvh, nctx, zref, l_c, o_c, sm.z, sm.scr, sm.o);
-  __syncthreads();
+  finalize_head<Gp>(p, b, h, kvh, nctx, zref, l_c, o_c, sm.z, sm.scr, sm.o);
+  Gp::sync();
 }
 
 // gather_partial + per-head ticket; the last CTA of the head finishes it.
+template <class Gp = CtaGrp>
 __device__ void chunk_body(const AttendParams& p, int bh, int slot, int nslots, int nrows, AttSmem& sm) {
-  gather_partial(p, bh, slot, nrows, sm);
+  gather_partial<Gp>(p, bh, slot, nrows, sm);
   __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) sm.last = (atomicAdd(&p.ticket[bh], 1u) == static_cast<unsigned>(nslots - 1));
-  __syncthreads();
+  Gp::sync();
+  if (Gp::tid() == 0) sm.last = (atomicAdd(&p.ticket[bh], 1u) == static_cast<unsigned>(nslots - 1));
+  Gp::sync();
   if (!sm.last) return;
   __threadfence();
-  if (threadIdx.x == 0) p.ticket[bh] = 0u;
-  head_finish(p, bh, nslots, sm);
+  if (Gp::tid() == 0) p.ticket[bh] = 0u;
+  head_finish<Gp>(p, bh, nslots, sm);
 }
 }  // namespace
 

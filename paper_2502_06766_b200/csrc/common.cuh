@@ -150,20 +150,35 @@ __device__ __forceinline__ void hist_add_aggregated(uint32_t* hist, uint32_t dig
   if ((threadIdx.x & 31) == static_cast<unsigned>(__ffs(peers) - 1)) atomicAdd(&hist[digit], __popc(peers));
 }
 
+// ---------------------------------------------------------------- thread groups
+// Block-wide helpers run on a thread group: the whole CTA (default), or a contiguous range of
+// warps synchronised by a named barrier (the work-queue warps of the warp-specialised layer
+// kernel run beside the tcgen05 scan warps, which must not take part in their barriers).
+struct CtaGrp {
+  __device__ static __forceinline__ int tid() { return static_cast<int>(threadIdx.x); }
+  __device__ static __forceinline__ void sync() { __syncthreads(); }
+};
+template <int kBase, int kCount, int kBarId>
+struct WarpGrp {
+  static_assert(kBase % 32 == 0 && kCount % 32 == 0 && kBarId > 0 && kBarId < 16, "warp-aligned group");
+  __device__ static __forceinline__ int tid() { return static_cast<int>(threadIdx.x) - kBase; }
+  __device__ static __forceinline__ void sync() { asm volatile("bar.sync %0, %1;" ::"n"(kBarId), "n"(kCount) : "memory"); }
+};
+
 // Copy n (multiple of 4, 16-byte aligned) u32 words global → shared with every load of a
 // thread issued before its first store (one memory round trip instead of n / NT). L2 path.
-template <int NT, int MAXN>
+template <int NT, int MAXN, class Gp = CtaGrp>
 __device__ __forceinline__ void copy_g2s_u32(uint32_t* dst, const uint32_t* src, int n) {
   constexpr int PER = (MAXN / 4 + NT - 1) / NT;
   uint4 v[PER];
 #pragma unroll
   for (int u = 0; u < PER; ++u) {
-    const int i = (u * NT + threadIdx.x) * 4;
+    const int i = (u * NT + Gp::tid()) * 4;
     v[u] = i < n ? __ldcg(reinterpret_cast<const uint4*>(src + i)) : make_uint4(0, 0, 0, 0);
   }
 #pragma unroll
   for (int u = 0; u < PER; ++u) {
-    const int i = (u * NT + threadIdx.x) * 4;
+    const int i = (u * NT + Gp::tid()) * 4;
     if (i < n) *reinterpret_cast<uint4*>(dst + i) = v[u];
   }
 }
@@ -173,9 +188,9 @@ __device__ __forceinline__ void copy_g2s_u32(uint32_t* dst, const uint32_t* src,
 // O(m^2 / NT) compares, two barriers — for the few hundred elements of a threshold bucket
 // this beats any multi-pass radix. Duplicates allowed: returns the value v with
 // #{> v} < need <= #{>= v}. Result broadcast through *out. Block-wide call.
-template <int NT, typename T>
+template <int NT, typename T, class Gp = CtaGrp>
 __device__ __forceinline__ T block_rank_select(const T* vals, int m, int need, T* out) {
-  for (int i = threadIdx.x; i < m; i += NT) {
+  for (int i = Gp::tid(); i < m; i += NT) {
     const T v = vals[i];
     int gt = 0, ge = 0;
     for (int j = 0; j < m; ++j) {
@@ -185,9 +200,9 @@ __device__ __forceinline__ T block_rank_select(const T* vals, int m, int need, T
     }
     if (gt < need && need <= ge) *out = v;  // all qualifying threads hold the same value
   }
-  __syncthreads();
+  Gp::sync();
   const T r = *out;
-  __syncthreads();
+  Gp::sync();
   return r;
 }
 
@@ -224,11 +239,11 @@ __device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
 // that above(d*) < need <= above(d*) + hist[d*], where above(d) = sum of hist over buckets > d.
 // Requires 1 <= need <= sum(hist). Result in out[0] = d*, out[1] = above(d*). Block-wide;
 // every thread must call it. scratch: >= NT/32 words.
-template <int NT, int NB>
+template <int NT, int NB, class Gp = CtaGrp>
 __device__ __forceinline__ void find_bucket(const uint32_t* hist, uint32_t need, uint32_t* out,
                                             uint32_t* scratch) {
   constexpr int PER = (NB + NT - 1) / NT;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = Gp::tid(), lane = tid & 31, warp = tid >> 5;
   uint32_t local[PER];
   uint32_t sum = 0;
 #pragma unroll
@@ -245,7 +260,7 @@ __device__ __forceinline__ void find_bucket(const uint32_t* hist, uint32_t need,
     if (lane >= o) incl += t;
   }
   if (lane == 31) scratch[warp] = incl;
-  __syncthreads();
+  Gp::sync();
   if (warp == 0) {
     constexpr int NW = NT / 32;
     uint32_t w = lane < NW ? scratch[lane] : 0u;
@@ -257,7 +272,7 @@ __device__ __forceinline__ void find_bucket(const uint32_t* hist, uint32_t need,
     }
     if (lane < NW) scratch[lane] = wi - w;  // exclusive warp offsets
   }
-  __syncthreads();
+  Gp::sync();
   const uint32_t excl = scratch[warp] + incl - sum;
   if (excl < need && need <= excl + sum) {
     uint32_t cum = excl;
@@ -271,34 +286,34 @@ __device__ __forceinline__ void find_bucket(const uint32_t* hist, uint32_t need,
       cum += local[j];
     }
   }
-  __syncthreads();
+  Gp::sync();
 }
 
 // ---------------------------------------------------------------- generic radix select
 // Radix select of the `need` largest composites among the elements accepted by `load`
 // (load(i, c) -> bool), MSB first with 8-bit digits. Result: selected ⇔ (c >> shift) >= prefix.
-template <int T, typename Load>
+template <int T, typename Load, class Gp = CtaGrp>
 __device__ void radix_select_u64(Load load, int64_t n, uint32_t need, uint32_t* hist, uint32_t* scr,
                                  uint32_t* out, int& shift_out, uint64_t& prefix_out) {
   int shift = 64;
   uint64_t prefix = 0;
   while (shift > 0) {
     const int nshift = shift - 8;
-    for (int i = threadIdx.x; i < 256; i += T) hist[i] = 0u;
-    __syncthreads();
-    for (int64_t i = threadIdx.x; i < n; i += T) {
+    for (int i = Gp::tid(); i < 256; i += T) hist[i] = 0u;
+    Gp::sync();
+    for (int64_t i = Gp::tid(); i < n; i += T) {
       uint64_t c;
       if (load(i, c) && (shift == 64 || (c >> shift) == prefix))
         hist_add_aggregated(hist, static_cast<uint32_t>(c >> nshift) & 255u);
     }
-    __syncthreads();
-    find_bucket<T, 256>(hist, need, out, scr);
+    Gp::sync();
+    find_bucket<T, 256, Gp>(hist, need, out, scr);
     const uint32_t d = out[0];
     need -= out[1];
     prefix = (prefix << 8) | d;
     shift = nshift;
     const bool done = hist[d] == need;
-    __syncthreads();
+    Gp::sync();
     if (done) break;
   }
   shift_out = shift;

@@ -11,7 +11,7 @@
 //   ATT(h, a)         KA per head                     — filter c >= T, V gather, softmax
 //
 // ordered so that the selection and the V gather of group g-1 are claimed while the tiles of
-// group g are being scanned:   SAMPLE(*) THRESH(*) | for g: SCAN(g)[0,T/2) KTH(g-1)
+// group g are being scanned:   SAMPLE(g) THRESH(g) for every g | for g: SCAN(g)[0,T/2) KTH(g-1)
 // SCAN(g)[T/2,T) ATT(g-1) | KTH(last) ATT(last).
 // An item only ever waits (spin on a flag) for items with a SMALLER index; the smallest
 // unfinished item therefore always has its inputs ready and is being processed (a CTA holds a
@@ -28,6 +28,7 @@
 #include <cstdio>
 
 #include "attend_dev.cuh"
+#include "scan_tc_dev.cuh"
 
 namespace tkv {
 
@@ -38,6 +39,13 @@ static_assert(FT == kAttendThreads && FT == kScanWarps * 32, "one CTA shape for 
 constexpr int kFStage = kScanRows * 4;  // staged candidates per head: up to 4 iterations/tile
 constexpr int kFBkt = 2048;             // bucket refinement held in shared memory
 constexpr uint32_t kNoItem = 0xffffffffu;
+
+// diagnostics: time an item's dependency wait ended (set by KTH / ATT items when tracing)
+__shared__ uint64_t s_item_ready;
+
+__device__ __forceinline__ void stamp_ready(const FusedParams& p, int tid) {
+  if (p.trace && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(s_item_ready));
+}
 
 enum ItemType : int { kItSample, kItThresh, kItScan, kItKth, kItAtt, kItFbScan, kItFbKth, kItFbAtt, kItNop };
 
@@ -78,19 +86,21 @@ __device__ __forceinline__ void spin_pause(uint32_t& n) {
 }
 
 // thread 0 spins until *f >= target; the barrier then releases the whole CTA
+template <class Gp>
 __device__ __forceinline__ void wait_geq(const uint32_t* f, uint32_t target) {
-  if (threadIdx.x == 0) {
+  if (Gp::tid() == 0) {
     uint32_t n = 0;
     while (ld_acquire(f) < target) spin_pause(n);
   }
-  __syncthreads();
+  Gp::sync();
 }
 
 // every thread's prior writes are made visible before *f is bumped
+template <class Gp>
 __device__ __forceinline__ void publish_add(uint32_t* f, uint32_t v) {
   __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) atomicAdd(f, v);
+  Gp::sync();
+  if (Gp::tid() == 0) atomicAdd(f, v);
 }
 
 __device__ __forceinline__ int group_of(const FusedParams& p, int bh) {
@@ -116,8 +126,12 @@ struct Sched {
 };
 
 __device__ Item decode(const Sched& s, const uint32_t* blk, uint32_t it) {
-  if (it < static_cast<uint32_t>(s.NS * s.NG)) return {kItSample, static_cast<int>(it / s.NS), static_cast<int>(it % s.NS)};
-  if (it < s.pre) return {kItThresh, static_cast<int>(it - s.NS * s.NG), 0};
+  if (it < s.pre) {  // group by group: SAMPLE(g, 0..NS) THRESH(heads of g), so g's threshold is early
+    const int per = s.NS + s.G;
+    const int g = static_cast<int>(it / per), o = static_cast<int>(it % per);
+    if (o < s.NS) return {kItSample, g, o};
+    return {kItThresh, g * s.G + (o - s.NS), 0};  // head index b·Hq + kvh·G + n = g·G + n
+  }
   const uint32_t j = it - s.pre;
   int lo = 0, hi = s.nblocks();  // largest g with blk[g] <= j
   while (hi - lo > 1) {
@@ -137,10 +151,11 @@ __device__ Item decode(const Sched& s, const uint32_t* blk, uint32_t it) {
 }
 
 // ------------------------------------------------------------------------- SAMPLE
+template <class Gp>
 __device__ void do_sample(const FusedParams& p, const Ctl& ctl, int g, int part) {
   const AttendParams& a = p.a;
   const int b = g / a.Hkv, kvh = g % a.Hkv;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = Gp::tid() & 31, warp = Gp::tid() >> 5;
   const int gg = lane >> 2, c = lane & 3;
   const int64_t N = a.n_ctx[b];
   if (N > 0) {
@@ -167,10 +182,11 @@ __device__ void do_sample(const FusedParams& p, const Ctl& ctl, int g, int part)
       }
     }
   }
-  publish_add(ctl.samp_done(g), 1u);
+  publish_add<Gp>(ctl.samp_done(g), 1u);
 }
 
 // ------------------------------------------------------------------------- THRESH
+template <class Gp>
 __device__ void do_thresh(const FusedParams& p, const Ctl& ctl, int bh, unsigned char* smem) {
   const AttendParams& a = p.a;
   uint32_t* s_keys = reinterpret_cast<uint32_t*>(smem);          // [kSamples]
@@ -178,7 +194,7 @@ __device__ void do_thresh(const FusedParams& p, const Ctl& ctl, int bh, unsigned
   uint32_t* s_scr = s_hist + 2048;                                // [32]
   uint32_t* s_out = s_scr + 32;                                   // [4]
   uint32_t* s_max = s_out + 4;                                    // [FW]
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = Gp::tid(), lane = tid & 31, warp = tid >> 5;
   const int b = bh / a.Hq;
   const int64_t N = a.n_ctx[b];
   const int64_t kb = N < a.k ? N : a.k;
@@ -192,15 +208,15 @@ __device__ void do_thresh(const FusedParams& p, const Ctl& ctl, int bh, unsigned
   const bool filter = !p.no_filter && kb > 0 && rr < static_cast<double>(Sb);
   uint32_t thr = 0u, shift = kNoFilterShift;
   if (filter) {
-    wait_geq(ctl.samp_done(group_of(p, bh)), static_cast<uint32_t>(p.NS));
-    copy_g2s_u32<FT, kSamples>(s_keys, p.samp + static_cast<int64_t>(bh) * kSamples, (Sb + 3) & ~3);
-    __syncthreads();
+    wait_geq<Gp>(ctl.samp_done(group_of(p, bh)), static_cast<uint32_t>(p.NS));
+    copy_g2s_u32<FT, kSamples, Gp>(s_keys, p.samp + static_cast<int64_t>(bh) * kSamples, (Sb + 3) & ~3);
+    Gp::sync();
     uint32_t mx = 0u;
     for (int i = tid; i < Sb; i += FT) mx = max(mx, s_keys[i]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(kFull, mx, o));
     if (lane == 0) s_max[warp] = mx;
-    __syncthreads();
+    Gp::sync();
     uint32_t prefix = 0, need = static_cast<uint32_t>(rr);
     int sh = 32;
     bool exact = false;
@@ -209,32 +225,32 @@ __device__ void do_thresh(const FusedParams& p, const Ctl& ctl, int bh, unsigned
       const int nsh = sh - w;
       const uint32_t mask = (1u << w) - 1u;
       for (int i = tid; i <= static_cast<int>(mask); i += FT) s_hist[i] = 0u;
-      __syncthreads();
+      Gp::sync();
       for (int i = tid; i < Sb; i += FT) {
         const uint32_t k = s_keys[i];
         if (sh == 32 || (k >> sh) == prefix) hist_add_aggregated(s_hist, (k >> nsh) & mask);
       }
-      __syncthreads();
+      Gp::sync();
       if (w == 11)
-        find_bucket<FT, 2048>(s_hist, need, s_out, s_scr);
+        find_bucket<FT, 2048, Gp>(s_hist, need, s_out, s_scr);
       else
-        find_bucket<FT, 1024>(s_hist, need, s_out, s_scr);
+        find_bucket<FT, 1024, Gp>(s_hist, need, s_out, s_scr);
       need -= s_out[1];
       prefix = (prefix << w) | s_out[0];
       sh = nsh;
       const uint32_t bc = s_hist[s_out[0]];
       const bool done = bc == need;
-      __syncthreads();
+      Gp::sync();
       if (done) break;
       if (bc <= 2048u) {
         if (tid == 0) s_out[2] = 0u;
-        __syncthreads();
+        Gp::sync();
         for (int i = tid; i < Sb; i += FT) {
           const uint32_t k = s_keys[i];
           if ((k >> sh) == prefix) s_hist[atomicAdd(&s_out[2], 1u)] = k;
         }
-        __syncthreads();
-        thr = block_rank_select<FT>(s_hist, static_cast<int>(s_out[2]), static_cast<int>(need), &s_out[3]);
+        Gp::sync();
+        thr = block_rank_select<FT, uint32_t, Gp>(s_hist, static_cast<int>(s_out[2]), static_cast<int>(need), &s_out[3]);
         exact = true;
         break;
       }
@@ -256,18 +272,21 @@ __device__ void do_thresh(const FusedParams& p, const Ctl& ctl, int bh, unsigned
     p.hs.bkt_cnt[bh] = 0u;
     p.hs.out_cnt[bh] = 0u;
   }
-  publish_add(ctl.thr_ready(bh), 1u);
+  publish_add<Gp>(ctl.thr_ready(bh), 1u);
 }
 
 // ------------------------------------------------------------------------- SCAN
 // Scores rows [tile*TR, (tile+1)*TR) of group g for its G heads (or, fallback, for fb_head
 // only) and appends every row whose key passes the head's threshold to the candidates.
+template <class Gp>
 __device__ void do_scan(const FusedParams& p, const Ctl& ctl, int g, int tile, int fb_head,
                         unsigned char* smem, int& ready_group) {
   const AttendParams& a = p.a;
-  uint64_t* s_buf = reinterpret_cast<uint64_t*>(smem);                          // [G][kFStage]
-  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_buf + a.G * kFStage);         // [8]
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int fl = p.scan_flush_iters;                                            // iterations per flush
+  const int stage = kScanRows * fl;                                              // staged per head
+  uint64_t* s_buf = reinterpret_cast<uint64_t*>(smem);                          // [G][stage]
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_buf + a.G * stage);           // [8]
+  const int tid = Gp::tid(), lane = tid & 31, warp = tid >> 5;
   const int gg = lane >> 2, c = lane & 3;
   const int b = g / a.Hkv, kvh = g % a.Hkv;
   const int bh0 = b * a.Hq + kvh * a.G;
@@ -280,7 +299,7 @@ __device__ void do_scan(const FusedParams& p, const Ctl& ctl, int g, int tile, i
     ready_group = g;
   }
   if (tid < 8) s_cnt[tid] = 0u;
-  __syncthreads();
+  Gp::sync();
   const int64_t nctx = a.n_ctx[b];
   const int TR = p.tile_iters * kScanRows;
   const int64_t r0 = static_cast<int64_t>(tile) * TR;
@@ -293,7 +312,7 @@ __device__ void do_scan(const FusedParams& p, const Ctl& ctl, int g, int tile, i
   const uint32_t thr1 = col1 < a.G ? __ldcg(&p.hs.thr[bh0 + col1]) : 0u;
   // flush: warp n moves head n's staged candidates to HBM and adds them to its histogram
   auto flush = [&]() {
-    __syncthreads();
+    Gp::sync();
     if (warp < a.G) {
       const uint32_t cnt = s_cnt[warp];
       __syncwarp();
@@ -305,7 +324,7 @@ __device__ void do_scan(const FusedParams& p, const Ctl& ctl, int g, int tile, i
         const uint32_t thr = __ldcg(&p.hs.thr[bh]), shift = __ldcg(&p.hs.hshift[bh]);
         uint32_t* gh = p.hs.hist + static_cast<int64_t>(bh) * kHistBins;
         uint64_t* dst = const_cast<uint64_t*>(a.cand) + static_cast<int64_t>(bh) * a.cap + base;
-        const uint64_t* src = s_buf + warp * kFStage;
+        const uint64_t* src = s_buf + warp * stage;
         for (uint32_t i = lane; i < cnt; i += 32) {
           const uint64_t cc = src[i];
           dst[i] = cc;
@@ -317,7 +336,7 @@ __device__ void do_scan(const FusedParams& p, const Ctl& ctl, int g, int tile, i
       __syncwarp();
       if (lane == 0) s_cnt[warp] = 0u;
     }
-    __syncthreads();
+    Gp::sync();
   };
   if (r0 < r1) {
     QFrag f;
@@ -352,20 +371,21 @@ __device__ void do_scan(const FusedParams& p, const Ctl& ctl, int g, int tile, i
               if (lane == leader) base = atomicAdd(&s_cnt[col], static_cast<uint32_t>(__popc(same)));
               base = __shfl_sync(m, base, leader);
               const uint32_t rank = __popc(same & ((1u << lane) - 1u));
-              s_buf[col * kFStage + base + rank] =
+              s_buf[col * stage + base + rank] =
                   make_comp(key, static_cast<uint32_t>(a.row_offset) + static_cast<uint32_t>(row));
             }
           }
         }
       }
-      if ((it & 3) == 3 && it + 1 < p.tile_iters) flush();  // staging holds 4 iterations per head
+      if (it % fl == fl - 1 && it + 1 < p.tile_iters) flush();  // staging holds fl iterations per head
     }
   }
   flush();
-  publish_add(fb_head < 0 ? ctl.scan_done(g) : ctl.fb_scan_done(fb_head), 1u);
+  publish_add<Gp>(fb_head < 0 ? ctl.scan_done(g) : ctl.fb_scan_done(fb_head), 1u);
 }
 
 // ------------------------------------------------------------------------- KTH
+template <class Gp>
 __device__ void do_kth(const FusedParams& p, const Ctl& ctl, int bh, int slice, bool fb,
                        unsigned char* smem) {
   const AttendParams& a = p.a;
@@ -374,12 +394,13 @@ __device__ void do_kth(const FusedParams& p, const Ctl& ctl, int bh, int slice, 
   uint32_t* s_scr = reinterpret_cast<uint32_t*>(s_bkt + kFBkt);           // [32]
   uint32_t* s_out = s_scr + 32;                                           // [4]
   uint64_t* s_r64 = reinterpret_cast<uint64_t*>(s_out + 4);               // [FW + 2]
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = Gp::tid(), lane = tid & 31, warp = tid >> 5;
   const int b = bh / a.Hq, g = group_of(p, bh);
   if (fb)
-    wait_geq(ctl.fb_scan_done(bh), static_cast<uint32_t>(p.T));
+    wait_geq<Gp>(ctl.fb_scan_done(bh), static_cast<uint32_t>(p.T));
   else
-    wait_geq(ctl.scan_done(g), static_cast<uint32_t>(p.T));
+    wait_geq<Gp>(ctl.scan_done(g), static_cast<uint32_t>(p.scan_target));
+  stamp_ready(p, tid);
   int64_t n = __ldcg(&p.hs.cand_cnt[bh]);
   if (n > a.cap) n = a.cap;
   const int64_t N = a.n_ctx[b];
@@ -402,7 +423,7 @@ __device__ void do_kth(const FusedParams& p, const Ctl& ctl, int bh, int slice, 
         p.hs.flag_fail[bh] = 1u;
       }
       __threadfence();
-      __syncthreads();
+      Gp::sync();
       if (tid == 0) {
         const uint32_t s = atomicAdd(ctl.fb_alloc(), 1u);
         *ctl.fb_head(static_cast<int>(s)) = static_cast<uint32_t>(bh);
@@ -412,7 +433,7 @@ __device__ void do_kth(const FusedParams& p, const Ctl& ctl, int bh, int slice, 
         atomicAdd(ctl.nfb(), 1u);
         atomicExch(ctl.kth_state(bh), 2u);  // static ATT items of this head stand down
       }
-      __syncthreads();
+      Gp::sync();
     }
     return;
   }
@@ -424,7 +445,7 @@ __device__ void do_kth(const FusedParams& p, const Ctl& ctl, int bh, int slice, 
         const_cast<float*>(a.meta_max)[bh] = -INFINITY;
       }
       __threadfence();
-      __syncthreads();
+      Gp::sync();
       if (tid == 0) atomicExch(ctl.kth_state(bh), final_state);
     }
     return;
@@ -435,9 +456,9 @@ __device__ void do_kth(const FusedParams& p, const Ctl& ctl, int bh, int slice, 
   uint32_t dstar = 0, need = 0, bcnt = 0;
   bool whole = true;
   if (!all) {
-    copy_g2s_u32<FT, kHistBins>(s_hist, p.hs.hist + static_cast<int64_t>(bh) * kHistBins, kHistBins);
-    __syncthreads();
-    find_bucket<FT, kHistBins>(s_hist, static_cast<uint32_t>(kb), s_out, s_scr);
+    copy_g2s_u32<FT, kHistBins, Gp>(s_hist, p.hs.hist + static_cast<int64_t>(bh) * kHistBins, kHistBins);
+    Gp::sync();
+    find_bucket<FT, kHistBins, Gp>(s_hist, static_cast<uint32_t>(kb), s_out, s_scr);
     dstar = s_out[0];
     need = static_cast<uint32_t>(kb) - s_out[1];
     bcnt = s_hist[dstar];
@@ -476,16 +497,16 @@ __device__ void do_kth(const FusedParams& p, const Ctl& ctl, int bh, int slice, 
   }
   vmax = warp_max_u64(vmax);
   if (lane == 0) s_r64[warp] = vmax;
-  __syncthreads();
+  Gp::sync();
   if (tid == 0) {
     uint64_t m = 0ull;
     for (int w = 0; w < FW; ++w) m = s_r64[w] > m ? s_r64[w] : m;
     atomicMax(reinterpret_cast<unsigned long long*>(&p.hs.max_comp[bh]), static_cast<unsigned long long>(m));
   }
   __threadfence();
-  __syncthreads();
+  Gp::sync();
   if (tid == 0) s_out[2] = (atomicAdd(&p.hs.kth_ticket[bh], 1u) == static_cast<unsigned>(p.KS - 1)) ? 1u : 0u;
-  __syncthreads();
+  Gp::sync();
   if (!s_out[2]) return;
   __threadfence();
 
@@ -500,21 +521,21 @@ __device__ void do_kth(const FusedParams& p, const Ctl& ctl, int bh, int slice, 
     const int64_t nb = __ldcg(&p.hs.bkt_cnt[bh]);
     if (!big && nb <= kFBkt) {
       for (int64_t i = tid; i < nb; i += FT) s_bkt[i] = __ldcg(&gbkt[i]);
-      __syncthreads();
-      cp = block_rank_select<FT>(s_bkt, static_cast<int>(nb), static_cast<int>(need), &s_r64[FW]);
+      Gp::sync();
+      cp = block_rank_select<FT, uint64_t, Gp>(s_bkt, static_cast<int>(nb), static_cast<int>(need), &s_r64[FW]);
       cs = 0;
     } else if (!big) {
       auto ld = [&](int64_t i, uint64_t& c) {
         c = __ldcg(&gbkt[i]);
         return true;
       };
-      radix_select_u64<FT>(ld, nb, need, s_hist, s_scr, s_out, cs, cp);
+      radix_select_u64<FT, decltype(ld), Gp>(ld, nb, need, s_hist, s_scr, s_out, cs, cp);
     } else {
       auto ld = [&](int64_t i, uint64_t& c) {
         c = __ldcg(&src[i]);
         return c != 0ull && hist_digit(comp_key(c), thr, shift) == dstar;
       };
-      radix_select_u64<FT>(ld, n, need, s_hist, s_scr, s_out, cs, cp);
+      radix_select_u64<FT, decltype(ld), Gp>(ld, n, need, s_hist, s_scr, s_out, cs, cp);
     }
     T = cp << cs;
   }
@@ -527,7 +548,7 @@ __device__ void do_kth(const FusedParams& p, const Ctl& ctl, int bh, int slice, 
     if (fb) p.hs.flag_fail[bh] = 0u;
   }
   __threadfence();
-  __syncthreads();
+  Gp::sync();
   if (tid == 0) atomicExch(ctl.kth_state(bh), final_state);
 }
 
@@ -535,19 +556,21 @@ __device__ void do_kth(const FusedParams& p, const Ctl& ctl, int bh, int slice, 
 // Chunks ai, ai+KA, ... of head bh's candidate list: keep c >= T, append the kept rows to
 // idx/scores, gather their V rows into per-chunk partials; the CTA that completes the head's
 // chunk count combines them, adds pinned-prefix and window rows and writes out.
+template <class Gp>
 __device__ void do_att(const FusedParams& p, const Ctl& ctl, int bh, int ai, bool fb, unsigned char* smem) {
   const AttendParams& a = p.a;
   AttSmem& sm = *reinterpret_cast<AttSmem*>(smem);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = Gp::tid(), lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
     uint32_t st;
     uint32_t spins = 0;
     while ((st = ld_acquire(ctl.kth_state(bh))) == 0u || (fb && st != 3u)) spin_pause(spins);
     sm.base = st;
   }
-  __syncthreads();
+  Gp::sync();
   const uint32_t state = sm.base;
-  __syncthreads();
+  stamp_ready(p, tid);
+  Gp::sync();
   if (!fb && state == 2u) return;  // failed head: its fallback job does the work
 
   int64_t n = __ldcg(&p.hs.cand_cnt[bh]);
@@ -583,14 +606,14 @@ __device__ void do_att(const FusedParams& p, const Ctl& ctl, int bh, int ai, boo
       if (lane >= o) incl += t;
     }
     if (lane == 31) sm.wcnt[warp] = incl;
-    __syncthreads();
+    Gp::sync();
     uint32_t woff = 0, m = 0;
     for (int w = 0; w < FW; ++w) {
       woff += w < warp ? sm.wcnt[w] : 0u;
       m += sm.wcnt[w];
     }
     if (tid == 0) sm.base = m ? atomicAdd(&a.out_cnt[bh], m) : 0u;
-    __syncthreads();
+    Gp::sync();
     const uint32_t obase = sm.base;
     uint32_t pos = woff + incl - my;
 #pragma unroll
@@ -617,21 +640,21 @@ __device__ void do_att(const FusedParams& p, const Ctl& ctl, int bh, int ai, boo
         if (a.packed_out) a.packed_out[static_cast<int64_t>(bh) * a.k + i] = 0ull;
       }
     }
-    __syncthreads();
-    if (a.gather) gather_partial(a, bh, slot, static_cast<int>(m), sm);
+    Gp::sync();
+    if (a.gather) gather_partial<Gp>(a, bh, slot, static_cast<int>(m), sm);
     ++mine;
   }
   if (!a.gather || mine == 0) return;
   __threadfence();
-  __syncthreads();
+  Gp::sync();
   if (tid == 0) {
     const uint32_t old = atomicAdd(ctl.att_ticket(bh), mine);
     sm.last = (old + mine == static_cast<uint32_t>(nch)) ? 1 : 0;
   }
-  __syncthreads();
+  Gp::sync();
   if (!sm.last) return;
   __threadfence();
-  head_finish(a, bh, nch, sm);
+  head_finish<Gp>(a, bh, nch, sm);
 }
 
 __device__ Item decode_dyn(const FusedParams& p, const Ctl& ctl, uint32_t j) {
@@ -642,28 +665,13 @@ __device__ Item decode_dyn(const FusedParams& p, const Ctl& ctl, uint32_t j) {
   if (o < p.T + p.KS) return {kItFbKth, bh, o - p.T};
   return {kItFbAtt, bh, o - p.T - p.KS};
 }
-}  // namespace
 
-__global__ void __launch_bounds__(FT, 2) fused_kernel(FusedParams p) {
-  extern __shared__ __align__(16) unsigned char f_smem[];
-  __shared__ uint32_t s_item;
-  __shared__ int s_last;
-  const int tid = threadIdx.x;
-  const int NG = p.a.B * p.a.Hkv, NH = p.a.B * p.a.Hq;
-  const Ctl ctl{p.ctl, NG, NH};
-  Sched sc{NG, NH, p.a.G, p.NS, p.T, p.KS, p.KA, static_cast<uint32_t>(p.NS * NG + NH)};
-  // block-start table of the interleaved part of the schedule
-  uint32_t* blk = reinterpret_cast<uint32_t*>(f_smem);
-  unsigned char* work = f_smem + ((static_cast<size_t>(NG) + 3) * 4 + 15) / 16 * 16;
-  if (tid == 0) {
-    uint32_t acc = 0;
-    for (int g = 0; g < sc.nblocks(); ++g) {
-      blk[g] = acc;
-      acc += static_cast<uint32_t>(sc.size(g));
-    }
-    blk[sc.nblocks()] = acc;
-  }
-  __syncthreads();
+// The work-queue loop, run by a thread group (the whole CTA in fused_kernel, the eight
+// work-queue warps in fused_tc_kernel). Claims items in order until none is left.
+template <class Gp>
+__device__ void run_queue(const FusedParams& p, const Ctl& ctl, const Sched& sc, const uint32_t* blk,
+                          unsigned char* work, uint32_t* s_item) {
+  const int tid = Gp::tid();
   const uint32_t static_items = sc.pre + blk[sc.nblocks()];
   const uint32_t per_fb = static_cast<uint32_t>(p.T + p.KS + p.KA);
   int ready_group = -1;
@@ -680,16 +688,16 @@ __global__ void __launch_bounds__(FT, 2) fused_kernel(FusedParams p) {
   if (tid == 0) {
     const uint32_t first = atomicAdd(ctl.item(), 1u);
     if (first < static_items) {
-      s_item = first;
+      *s_item = first;
     } else {
       dyn = true;
-      s_item = claim_dyn();
+      *s_item = claim_dyn();
     }
   }
-  __syncthreads();
+  Gp::sync();
   for (;;) {
-    const uint32_t it = s_item;
-    __syncthreads();
+    const uint32_t it = *s_item;
+    Gp::sync();
     if (it == kNoItem) break;
     uint32_t next = kNoItem;
     if (tid == 0 && !dyn) next = atomicAdd(ctl.item(), 1u);  // prefetch the next claim
@@ -705,19 +713,22 @@ __global__ void __launch_bounds__(FT, 2) fused_kernel(FusedParams p) {
              static_items);
 #endif
     uint64_t t_start = 0;
-    if (p.trace && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    if (p.trace && tid == 0) {
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+      s_item_ready = t_start;
+    }
     switch (item.type) {
-      case kItSample: do_sample(p, ctl, item.a, item.b); break;
-      case kItThresh: do_thresh(p, ctl, item.a, work); break;
-      case kItScan: do_scan(p, ctl, item.a, item.b, -1, work, ready_group); break;
-      case kItKth: do_kth(p, ctl, item.a, item.b, false, work); break;
-      case kItAtt: do_att(p, ctl, item.a, item.b, false, work); break;
-      case kItFbScan: do_scan(p, ctl, group_of(p, item.a), item.b, item.a, work, ready_group); break;
-      case kItFbKth: do_kth(p, ctl, item.a, item.b, true, work); break;
-      case kItFbAtt: do_att(p, ctl, item.a, item.b, true, work); break;
+      case kItSample: do_sample<Gp>(p, ctl, item.a, item.b); break;
+      case kItThresh: do_thresh<Gp>(p, ctl, item.a, work); break;
+      case kItScan: do_scan<Gp>(p, ctl, item.a, item.b, -1, work, ready_group); break;
+      case kItKth: do_kth<Gp>(p, ctl, item.a, item.b, false, work); break;
+      case kItAtt: do_att<Gp>(p, ctl, item.a, item.b, false, work); break;
+      case kItFbScan: do_scan<Gp>(p, ctl, group_of(p, item.a), item.b, item.a, work, ready_group); break;
+      case kItFbKth: do_kth<Gp>(p, ctl, item.a, item.b, true, work); break;
+      case kItFbAtt: do_att<Gp>(p, ctl, item.a, item.b, true, work); break;
       default: break;
     }
-    __syncthreads();
+    Gp::sync();
     if (p.trace && tid == 0 && it < p.trace_cap) {
       uint64_t t_end;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
@@ -726,27 +737,206 @@ __global__ void __launch_bounds__(FT, 2) fused_kernel(FusedParams p) {
       r[1] = t_end;
       r[2] = (static_cast<uint64_t>(item.type) << 32) | blockIdx.x;
       r[3] = (static_cast<uint64_t>(static_cast<uint32_t>(item.a)) << 32) | static_cast<uint32_t>(item.b);
+      r[2] |= static_cast<uint64_t>((s_item_ready - t_start) / 64u & 0xFFFFFFu) << 40 >> 0;  // wait (64 ns units)
     }
     if (tid == 0) {
       if (!dyn && next < static_items) {
-        s_item = next;
+        *s_item = next;
       } else {
         dyn = true;
-        s_item = claim_dyn();
+        *s_item = claim_dyn();
       }
     }
-    __syncthreads();
+    Gp::sync();
   }
-  // the last CTA out re-zeroes the control block for the next launch
-  if (tid == 0) {
+}
+
+__device__ __forceinline__ void build_block_table(const Sched& sc, uint32_t* blk) {
+  uint32_t acc = 0;
+  for (int g = 0; g < sc.nblocks(); ++g) {
+    blk[g] = acc;
+    acc += static_cast<uint32_t>(sc.size(g));
+  }
+  blk[sc.nblocks()] = acc;
+}
+
+// the last CTA out re-zeroes the control block for the next launch (block-wide call)
+__device__ __forceinline__ void reset_ctl_if_last(const FusedParams& p, const Ctl& ctl, int* s_last) {
+  if (threadIdx.x == 0) {
     __threadfence();
-    s_last = atomicAdd(ctl.exited(), 1u) == gridDim.x - 1;
+    *s_last = atomicAdd(ctl.exited(), 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (s_last) {
-    const int words = fused_ctl_words(NG, NH);
-    for (int i = tid; i < words; i += FT) p.ctl[i] = 0u;
+  if (*s_last) {
+    const int words = fused_ctl_words(ctl.NG, ctl.NH);
+    for (int i = threadIdx.x; i < words; i += blockDim.x) p.ctl[i] = 0u;
   }
+}
+}  // namespace
+
+__global__ void __launch_bounds__(FT, 2) fused_kernel(FusedParams p) {
+  extern __shared__ __align__(16) unsigned char f_smem[];
+  __shared__ uint32_t s_item;
+  __shared__ int s_last;
+  const int NG = p.a.B * p.a.Hkv, NH = p.a.B * p.a.Hq;
+  const Ctl ctl{p.ctl, NG, NH};
+  Sched sc{NG, NH, p.a.G, p.NS, p.T, p.KS, p.KA, static_cast<uint32_t>(p.NS * NG + NH)};
+  // block-start table of the interleaved part of the schedule
+  uint32_t* blk = reinterpret_cast<uint32_t*>(f_smem);
+  unsigned char* work = f_smem + ((static_cast<size_t>(NG) + 3) * 4 + 15) / 16 * 16;
+  if (threadIdx.x == 0) build_block_table(sc, blk);
+  __syncthreads();
+  run_queue<CtaGrp>(p, ctl, sc, blk, work, &s_item);
+  reset_ctl_if_last(p, ctl, &s_last);
+}
+
+namespace {
+// ------------------------------------------------------------------------- fused_tc_kernel
+// The layer step with the key scan on the tcgen05 pipeline, warp-specialised in one persistent
+// CTA per SM (448 threads):
+//   warps 0–5   the scan roles of scan_tc.cu (TMA producer, MMA issuer, 4 epilogue warps),
+//               walking the KV groups IN ORDER — every CTA scans its share of group 0, then of
+//               group 1, … — so group g's candidates are complete early; each epilogue warp
+//               bumps scan_done(g) after flushing its last candidates of g (target 4 · grid);
+//   warps 6–13  the work queue of fused_kernel without SCAN items: SAMPLE/THRESH of every group
+//               first (group 0 first — the epilogue waits for its thresholds), then KTH(g) and
+//               ATT(g) per group, which wait for scan_done(g) and so run beside the scan of
+//               groups g+1, …; the exactness fallback re-scans on these warps (mma.sync).
+// The scan warps only wait on THRESH items, which never wait on the scan, and every CTA is
+// co-resident (one CTA per SM, grid = #SMs, cooperative launch), so nothing can deadlock.
+constexpr int kFtcThreads = tc::kTcThreads + FT;
+using QueueGrp = WarpGrp<tc::kTcThreads, FT, 1>;
+
+// live units [lo, hi) of group g scanned by this CTA: the group's units split into `grid`
+// contiguous shares, share (cta + g) mod grid — rotating, so the remainder units spread evenly
+__device__ __forceinline__ void group_share(const FusedParams& p, int g, int64_t ups, int64_t& lo, int64_t& hi) {
+  const int grid = static_cast<int>(gridDim.x);
+  const int r = static_cast<int>((static_cast<int64_t>(blockIdx.x) + g) % grid);
+  lo = ups * r / grid;
+  hi = ups * (r + 1) / grid;
+  const int64_t nctx = p.a.n_ctx[g / p.a.Hkv];
+  const int64_t live = (nctx + tc::kTcUnit - 1) / tc::kTcUnit;
+  if (hi > live) hi = live;
+  if (lo > hi) lo = hi;
+}
+}  // namespace
+
+__global__ void __launch_bounds__(kFtcThreads, 1) fused_tc_kernel(const __grid_constant__ CUtensorMap kmap,
+                                                                  FusedParams p, int n_stages, int flush_every,
+                                                                  int tc_bytes) {
+  using namespace tc;
+  extern __shared__ __align__(16) unsigned char f_smem[];  // tc_setup aligns the pipeline to 1024
+  __shared__ __align__(8) uint64_t s_bar[kTcBarWords];
+  __shared__ uint32_t s_tmem;
+  __shared__ uint32_t s_item;
+  __shared__ int s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const AttendParams& a = p.a;
+  const int NG = a.B * a.Hkv, NH = a.B * a.Hq;
+  const Ctl ctl{p.ctl, NG, NH};
+  Sched sc{NG, NH, a.G, p.NS, 0 /* no SCAN items */, p.KS, p.KA, static_cast<uint32_t>(p.NS * NG + NH)};
+  TcPipe t = tc_setup(f_smem, s_bar, &s_tmem, a.G, flush_every, n_stages, &kmap, tid == 0, warp == 1);
+  uint32_t* blk = reinterpret_cast<uint32_t*>(f_smem + tc_bytes);
+  unsigned char* work = f_smem + tc_bytes + ((static_cast<size_t>(NG) + 3) * 4 + 15) / 16 * 16;
+  if (tid == kTcThreads) build_block_table(sc, blk);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  t.tmem = s_tmem;
+  const int64_t ups = (p.max_ctx + kTcUnit - 1) / kTcUnit;
+
+  if (warp == 0) {  // TMA producer
+    uint32_t i = 0;
+    for (int g = 0; g < NG; ++g) {
+      int64_t lo, hi;
+      group_share(p, g, ups, lo, hi);
+      for (int64_t u = lo; u < hi; ++u, ++i)
+        tc_produce(t, i, &kmap, static_cast<int>(g * a.cache_rows + u * kTcUnit), lane, 0);
+    }
+  } else if (warp == 1) {  // MMA issuer
+    uint32_t i = 0;
+    int slot = -1;
+    for (int g = 0; g < NG; ++g) {
+      int64_t lo, hi;
+      group_share(p, g, ups, lo, hi);
+      for (int64_t u = lo; u < hi; ++u, ++i) {
+        tc_mma_acquire(t, i);
+        if (u == lo) {
+          slot = (slot + 1) % kTcQSlots;
+          tc_load_q(t, slot, a.q + static_cast<int64_t>(g) * a.G * kD, a.G, lane);
+        }
+        tc_mma_issue(t, i, slot, lane, 0);
+      }
+    }
+  } else if (warp < kTcThreads / 32) {  // epilogue
+    const int ew = warp - 2;
+    const int quarter = warp & 3;  // TMEM lanes this warp may access: [32·quarter, +32)
+    uint64_t* wbuf = t.s_buf + static_cast<int64_t>(ew) * a.G * t.cap;
+    uint32_t thr[8], shift[8], cnt[8];
+#pragma unroll
+    for (int n = 0; n < 8; ++n) cnt[n] = thr[n] = shift[n] = 0u;
+    uint32_t i = 0;
+    for (int g = 0; g < NG; ++g) {
+      int64_t lo, hi;
+      group_share(p, g, ups, lo, hi);
+      const int64_t bh0 = static_cast<int64_t>(g) * a.G;
+      uint64_t t_start = 0, t_ready = 0;
+      if (p.trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+      if (lo < hi) {
+        // the group's thresholds come from THRESH items of the work queue
+        if (lane < a.G) {
+          uint32_t spins = 0;
+          while (ld_acquire(ctl.thr_ready(static_cast<int>(bh0) + lane)) == 0u) spin_pause(spins);
+        }
+        __syncwarp();
+        if (p.trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_ready));
+#pragma unroll
+        for (int n = 0; n < 8; ++n) {
+          thr[n] = n < a.G ? __ldcg(&p.hs.thr[bh0 + n]) : 0xFFFFFFFFu;
+          shift[n] = n < a.G ? __ldcg(&p.hs.hshift[bh0 + n]) : 0u;
+        }
+        const int64_t nctx = a.n_ctx[g / a.Hkv];
+        int since = 0;
+        for (int64_t u = lo; u < hi; ++u, ++i) {
+          uint32_t v[16];
+          tc_epi_load(t, i, quarter, lane, v, 0);
+          tc_epi_emit(v, u * kTcUnit, nctx, quarter, lane, a.G, static_cast<uint32_t>(a.row_offset), thr, wbuf,
+                      t.cap, cnt, true);
+          if (++since == flush_every) {
+            tc_warp_flush(const_cast<uint64_t*>(a.cand), a.cap, p.hs.cand_cnt, p.hs.hist, a.G, bh0, wbuf, t.cap,
+                          cnt, thr, shift, lane);
+            since = 0;
+          }
+        }
+        tc_warp_flush(const_cast<uint64_t*>(a.cand), a.cap, p.hs.cand_cnt, p.hs.hist, a.G, bh0, wbuf, t.cap, cnt,
+                      thr, shift, lane);
+      }
+      // this warp's share of group g is in HBM: count it towards scan_done(g)
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) atomicAdd(ctl.scan_done(g), 1u);
+      if (p.trace && lane == 0) {  // diagnostics: per (group, CTA, epilogue warp) scan window
+        const uint32_t slot = sc.pre + blk[sc.nblocks()] + 4096u + (static_cast<uint32_t>(g) * gridDim.x + blockIdx.x) * 4u + ew;
+        if (slot < p.trace_cap) {
+          uint64_t t_end;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+          uint64_t* r = p.trace + static_cast<uint64_t>(slot) * 4;
+          r[0] = t_start;
+          r[1] = t_end;
+          r[2] = (static_cast<uint64_t>(kItScan) << 32) | blockIdx.x;
+          r[3] = (static_cast<uint64_t>(static_cast<uint32_t>(g)) << 32) |
+                 static_cast<uint32_t>(t_ready ? (t_ready - t_start) : 0);
+        }
+      }
+    }
+  } else {  // work queue
+    run_queue<QueueGrp>(p, ctl, sc, blk, work, &s_item);
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_teardown(t.tmem, warp == 1);
+  reset_ctl_if_last(p, ctl, &s_last);
 }
 
 cudaError_t launch_fused(const FusedParams& p, cudaStream_t s) {
@@ -773,6 +963,74 @@ cudaError_t launch_fused(const FusedParams& p, cudaStream_t s) {
   }
   fused_kernel<<<grid_cache[1], FT, smem, s>>>(p);
   return cudaGetLastError();
+}
+
+// Work-queue shared memory of the tc layer kernel: the fallback scan flushes every iteration.
+static size_t ftc_work_bytes(int G) {
+  const size_t scan_sm = static_cast<size_t>(G) * kScanRows * 8 + 64;
+  const size_t thr_sm = (kSamples + 2048 + 32 + 4 + FW) * 4;
+  const size_t kth_sm = kHistBins * 4 + kFBkt * 8 + (32 + 4) * 4 + (FW + 2) * 8;
+  const size_t att_sm = sizeof(AttSmem);
+  size_t work = scan_sm;
+  work = thr_sm > work ? thr_sm : work;
+  work = kth_sm > work ? kth_sm : work;
+  work = att_sm > work ? att_sm : work;
+  return work;
+}
+
+bool fused_tc_supported(const FusedParams& p) {
+  const int64_t rows = static_cast<int64_t>(p.a.B) * p.a.Hkv * p.a.cache_rows;
+  return (reinterpret_cast<uintptr_t>(p.a.kc) & 15u) == 0 && rows < (int64_t(1) << 31) && p.a.G <= 8;
+}
+
+cudaError_t launch_fused_tc(FusedParams p, cudaStream_t s) {
+  using namespace tc;
+  CUtensorMap map;
+  if (!make_kmap(p.a.kc, static_cast<int64_t>(p.a.B) * p.a.Hkv * p.a.cache_rows, &map)) return cudaErrorInvalidValue;
+  const int NG = p.a.B * p.a.Hkv;
+  const size_t tbl = ((static_cast<size_t>(NG) + 3) * 4 + 15) / 16 * 16;
+  const size_t work = ftc_work_bytes(p.a.G);
+  // scan pipeline: two stages, the largest flush interval (<= 4 units) that fits beside the queue
+  TcShape sh{2, kTcMaxFlush};
+  size_t tcb = 0;
+  for (; sh.flush >= 1; --sh.flush) {
+    tcb = (tc_smem_bytes(p.a.G, sh) + 15) / 16 * 16;
+    if (tcb + tbl + work <= static_cast<size_t>(kTcSmemLimit)) break;
+  }
+  if (sh.flush < 1) return cudaErrorInvalidConfiguration;
+  const size_t smem = tcb + tbl + work;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(fused_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmemLimit);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(fused_tc_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  int dev = 0, sms = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fused_tc_kernel, kFtcThreads, smem);
+  if (per < 1) return cudaErrorInvalidConfiguration;
+  p.scan_target = 4 * sms;  // every epilogue warp of every CTA reports each group
+  p.scan_flush_iters = 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(sms);
+  cfg.blockDim = dim3(kFtcThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  // every CTA must be resident (the queue warps wait on other CTAs' scan progress): a
+  // cooperative launch guarantees it, or fails instead of hanging; inside stream capture a
+  // plain launch of one CTA per SM (the shared memory allows no more) is used
+  cudaLaunchAttribute attr_coop[1];
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cap);
+  attr_coop[0].id = cudaLaunchAttributeCooperative;
+  attr_coop[0].val.cooperative = 1;
+  cfg.attrs = attr_coop;
+  cfg.numAttrs = cap == cudaStreamCaptureStatusNone ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, fused_tc_kernel, map, p, sh.stages, sh.flush, static_cast<int>(tcb));
 }
 
 }  // namespace tkv

@@ -177,6 +177,8 @@ struct FusedParams {
   int tile_iters;  // 256-row iterations per scan tile
   int KS;          // k-th slices per head
   int KA;          // attend items per head
+  int scan_target;       // scan_done(g) count that completes group g's scan
+  int scan_flush_iters;  // HMMA scan items: 256-row iterations per staging flush
   uint64_t* trace;  // optional per-item timeline (tkv_debug_trace): [n][4] = t0, t1, type|cta, item
   uint32_t trace_cap;
 };
@@ -184,6 +186,8 @@ constexpr int kFusedKS = 4;
 __host__ __device__ inline int fused_ctl_words(int NG, int NH) { return 8 + 2 * NG + 5 * NH; }
 
 cudaError_t launch_fused(const FusedParams& p, cudaStream_t s);
+cudaError_t launch_fused_tc(FusedParams p, cudaStream_t s);
+bool fused_tc_supported(const FusedParams& p);
 cudaError_t launch_sample(const SampleParams& p, cudaStream_t s);
 cudaError_t launch_scan(const ScanParams& p, cudaStream_t s);
 cudaError_t launch_scan_tc(const ScanParams& p, cudaStream_t s);

@@ -28,14 +28,14 @@ def main():
     dev = torch.device("cuda", 0)
     q, K, V, n = bench.make_inputs(cfg, cfg["N"] + 8, 0, dev)
     for _ in range(3):
-        tkv.topk_decode_attention(q, K, V, n, cfg["k"], max_ctx=n)
+        tkv.topk_decode_attention(q, K, V, n, cfg["k"], max_ctx=n, fused=True)
     cap = 1 << 16
     buf = torch.zeros(cap * 4, dtype=torch.int64, device=dev)
     lib = _lib.load()
     lib.tkv_debug_trace(ctypes.c_void_p(buf.data_ptr()), cap)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    tkv.topk_decode_attention(q, K, V, n, cfg["k"], max_ctx=n)
+    tkv.topk_decode_attention(q, K, V, n, cfg["k"], max_ctx=n, fused=True)
     e1.record()
     torch.cuda.synchronize()
     lib.tkv_debug_trace(None, 0)
@@ -44,7 +44,8 @@ def main():
     t0 = r[:, 0].min()
     start = (r[:, 0] - t0) / 1e3
     end = (r[:, 1] - t0) / 1e3
-    typ = (r[:, 2] >> 32).astype(int)
+    typ = ((r[:, 2] >> 32) & 0xFF).astype(int)
+    ready = start + ((r[:, 2] >> 40).astype(float) * 64) / 1e3  # dependency wait end (KTH / ATT)
     cta = (r[:, 2] & 0xffffffff).astype(int)
     print(f"event time {e0.elapsed_time(e1) * 1e3:.1f} us; traced span {end.max():.1f} us; items {len(r)}; "
           f"CTAs {len(set(cta.tolist()))}")
@@ -57,6 +58,25 @@ def main():
     busy = (end - start).sum()
     ncta = len(set(cta.tolist()))
     print(f"  CTA occupancy {busy / (span * ncta):.3f}  (idle = waiting / claiming / tail)")
+    # tc kernel: per-group scan windows of the epilogue warps (type SCAN, a = group, b = thr wait ns)
+    m = typ == 2
+    if m.any():
+        grp = (r[:, 3] >> 32).astype(int)
+        wait = (r[:, 3] & 0xffffffff).astype(float) / 1e3
+        for g in sorted(set(grp[m].tolist())):
+            mg = m & (grp == g)
+            print(f"    group {g:3d}: start {start[mg].min():7.1f}..{start[mg].max():7.1f}  end "
+                  f"{end[mg].min():7.1f}..{end[mg].max():7.1f}  thr wait max {wait[mg].max():6.1f} us")
+        for t in (3, 4):
+            mt = typ == t
+            if mt.any():
+                ga = (r[:, 3] >> 32).astype(int) // 4  # head → group (G = 4)
+                for g in sorted(set(ga[mt].tolist()))[:16]:
+                    mg = mt & (ga == g)
+                    work = end[mg] - ready[mg]
+                    print(f"    {NAMES[t]} group {g:3d}: claimed {start[mg].min():7.1f}  ready {ready[mg].min():7.1f}"
+                          f"..{ready[mg].max():7.1f}  end {end[mg].max():7.1f}  work mean {work.mean():6.1f} "
+                          f"max {work.max():6.1f} us")
     # scan throughput over time windows
     m = typ == 2
     w = 20.0
