@@ -223,10 +223,9 @@ __device__ void head_finish(const AttendParams& p, int bh, int nslots, AttSmem& 
   Gp::sync();
 }
 
-// gather_partial + per-head ticket; the last CTA of the head finishes it.
+// Per-head ticket after a partial slot was written; the last CTA of the head finishes it.
 template <class Gp = CtaGrp>
-__device__ void chunk_body(const AttendParams& p, int bh, int slot, int nslots, int nrows, AttSmem& sm) {
-  gather_partial<Gp>(p, bh, slot, nrows, sm);
+__device__ void ticket_finish(const AttendParams& p, int bh, int nslots, AttSmem& sm) {
   __threadfence();
   Gp::sync();
   if (Gp::tid() == 0) sm.last = (atomicAdd(&p.ticket[bh], 1u) == static_cast<unsigned>(nslots - 1));
@@ -235,6 +234,13 @@ __device__ void chunk_body(const AttendParams& p, int bh, int slot, int nslots, 
   __threadfence();
   if (Gp::tid() == 0) p.ticket[bh] = 0u;
   head_finish<Gp>(p, bh, nslots, sm);
+}
+
+// gather_partial + per-head ticket; the last CTA of the head finishes it.
+template <class Gp = CtaGrp>
+__device__ void chunk_body(const AttendParams& p, int bh, int slot, int nslots, int nrows, AttSmem& sm) {
+  gather_partial<Gp>(p, bh, slot, nrows, sm);
+  ticket_finish<Gp>(p, bh, nslots, sm);
 }
 }  // namespace
 

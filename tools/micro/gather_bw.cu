@@ -1,0 +1,59 @@
+// Microbenchmark: bandwidth of gathering random 256-byte rows (bf16 V rows, d = 128) from a
+// 2 GiB cache, 16 lanes per row, U rows in flight per half-warp, grid = 148 × CTAs/SM.
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <vector>
+#include <random>
+#include <algorithm>
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+template <int U>
+__global__ void __launch_bounds__(256) gather(const uint4* V, const int* rows, int n, float* out) {
+  const int lane = threadIdx.x & 31, half = lane >> 4, part = lane & 15;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  float acc = 0.f;
+  for (int r0 = (gw * 2 + half) * U; r0 < n; r0 += nw * 2 * U) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int r = r0 + u;
+      v[u] = r < n ? ldg_stream(V + static_cast<int64_t>(rows[r]) * 16 + part) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc += __uint_as_float(v[u].x) + __uint_as_float(v[u].w);
+  }
+  if (acc == 12345.f) out[0] = acc;
+}
+template <int U>
+void run(const uint4* V, const int* rows, int n, float* out, int per_sm) {
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  const int grid = 148 * per_sm;
+  gather<U><<<grid, 256>>>(V, rows, n, out);
+  cudaEventRecord(a);
+  for (int i = 0; i < 10; ++i) gather<U><<<grid, 256>>>(V, rows, n, out);
+  cudaEventRecord(b); cudaEventSynchronize(b);
+  float ms; cudaEventElapsedTime(&ms, a, b);
+  const double bytes = double(n) * 256 * 10;
+  printf("U=%2d ctas/sm=%d: %.1f us per gather of %d rows -> %.0f GB/s\n", U, per_sm, ms * 100, n, bytes / (ms * 1e-3) / 1e9);
+}
+int main() {
+  const int64_t nrows = (2LL << 30) / 256;  // 2 GiB of V rows
+  uint4* V; cudaMalloc(&V, nrows * 256); cudaMemset(V, 0, nrows * 256);
+  const int n = 32 * 16384;  // cfg3: 32 heads × k
+  std::vector<int> h(n); std::mt19937 g(1);
+  for (int i = 0; i < n; ++i) h[i] = int(g() % nrows);
+  int* rows; cudaMalloc(&rows, n * 4); cudaMemcpy(rows, h.data(), n * 4, cudaMemcpyHostToDevice);
+  float* out; cudaMalloc(&out, 4);
+  run<4>(V, rows, n, out, 4); run<8>(V, rows, n, out, 4); run<16>(V, rows, n, out, 4); run<8>(V, rows, n, out, 8);
+  run<16>(V, rows, n, out, 8); run<32>(V, rows, n, out, 4);
+  // sorted rows (ascending ids within each head, like a selection in row order)
+  for (int hh = 0; hh < 32; ++hh) std::sort(h.begin() + hh * 16384, h.begin() + (hh + 1) * 16384);
+  cudaMemcpy(rows, h.data(), n * 4, cudaMemcpyHostToDevice);
+  printf("sorted per head:\n"); run<8>(V, rows, n, out, 4); run<16>(V, rows, n, out, 8);
+  return 0;
+}
