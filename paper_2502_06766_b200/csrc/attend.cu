@@ -23,7 +23,7 @@ namespace tkv {
 
 
 // List mode (sharded partial): the selected (idx, score) list is given.
-__global__ void __launch_bounds__(NT) attend_kernel(AttendParams p) {
+__global__ void __launch_bounds__(NT, 4) attend_kernel(AttendParams p) {
   __shared__ AttSmem sm;
   const int ch = blockIdx.x, bh = blockIdx.y;
   const int b = bh / p.Hq;
@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(NT) attend_kernel(AttendParams p) {
 // work items; a candidate is selected iff its composite >= meta_kth (kth_kernel), which is
 // exactly the top-kb set. Selected rows are appended to idx/scores (order unspecified) and,
 // with p.gather, their V rows are gathered in the same pass.
-__global__ void __launch_bounds__(NT) attend_cand_kernel(AttendParams p) {
+__global__ void __launch_bounds__(NT, 4) attend_cand_kernel(AttendParams p) {
   __shared__ AttSmem sm;
   extern __shared__ uint32_t s_pref[];  // [B*Hq + 1] work-item prefix over heads
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -177,6 +177,7 @@ __global__ void __launch_bounds__(NT) finalize_kernel(AttendParams p) {
   __shared__ float s_z[128];
   __shared__ float s_scr[32];
   __shared__ float s_o[NT];
+  __shared__ float s_red[NW * kD];
   const int bh = blockIdx.x;
   const int b = bh / p.Hq, h = bh % p.Hq, kvh = h / p.G;
   const int tid = threadIdx.x;
@@ -186,7 +187,7 @@ __global__ void __launch_bounds__(NT) finalize_kernel(AttendParams p) {
   const float* src = p.partial_in + static_cast<int64_t>(bh) * (kD + 1);
   const float l_c = kb > 0 ? src[0] : 0.f;
   const float o_c = (kb > 0 && tid < kD) ? src[1 + tid] : 0.f;
-  finalize_head(p, b, h, kvh, p.n_ctx[b], zref, l_c, o_c, s_z, s_scr, s_o);
+  finalize_head(p, b, h, kvh, p.n_ctx[b], zref, l_c, o_c, s_z, s_scr, s_o, s_red);
 }
 
 // K4: KV append (GenWindow.append, attention.py:94-100) — one CTA per batch entry.

@@ -13,32 +13,38 @@ constexpr int NT = kAttendThreads;
 constexpr int NW = NT / 32;
 
 // Online softmax accumulation over local rows [r_begin, r_end) of kv head (b, kvh) for q head
-// h. State (m, l, o) in the log2-scaled domain; thread t accumulates o for d = t % 128 over rows
-// of parity t / 128. With `pinned`, a row is skipped when it is among the selected top-k
-// (composite >= kth).
+// h. State (m, l, o) in the log2-scaled domain; thread t holds o for d = t % 128 (the two
+// halves t / 128 are summed by the caller). With `pinned`, a row is skipped when it is among
+// the selected top-k (composite >= kth). Per 128-row block: the rows are scored with the scan's
+// HMMA tile (bit-identical scores), weighted once per row, and their V rows gathered 16 bytes
+// per lane with 8 rows in flight per half-warp; s_red: NW × 128 floats.
 template <class Gp = CtaGrp>
 __device__ void accumulate_rows(const AttendParams& p, int b, int h, int kvh, int64_t r_begin,
                                 int64_t r_end, bool pinned, uint64_t kth, float& m, float& l,
-                                float& o, float* s_z, float* s_scr) {
+                                float& o, float* s_z, float* s_scr, float* s_red) {
   const int tid = Gp::tid(), lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, c = lane & 3;
+  const int half = lane >> 4, part = lane & 15;
   const int n = h - kvh * p.G;
   const float zs = p.scale * kLog2e;
   QFrag f;
   load_qfrag(f, p.q + (static_cast<int64_t>(b) * p.Hq + kvh * p.G) * kD, p.G, lane);
   const int64_t head_off = (static_cast<int64_t>(b) * p.Hkv + kvh) * p.cache_rows * kD;
   const __nv_bfloat16* kb = p.kc + head_off;
-  const __nv_bfloat16* vb = p.vc + head_off;
-  const int d = tid & (kD - 1), par = tid >> 7;
+  const __nv_bfloat16* vb = p.vc + head_off + part * 8;
+  float acc[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+  float mrun = m, lrun = 0.f;  // acc and lrun are relative to mrun (rows of this call only)
   for (int64_t base = r_begin; base < r_end; base += 8 * 16) {
     {
       const int64_t rA = base + warp * 16 + g, rB = rA + 8;
       uint4 a[2][4];
       load_tile(a, kb + rA * kD, rA < r_end, kb + rB * kD, rB < r_end, c);
-      float acc[4];
-      score_tile(acc, a, f);
+      float sc[4];
+      score_tile(sc, a, f);
       if (c == (n >> 1)) {
-        const float sA = acc[n & 1], sB = acc[2 + (n & 1)];
+        const float sA = sc[n & 1], sB = sc[2 + (n & 1)];
         bool okA = rA < r_end, okB = rB < r_end;
         if (pinned) {
           okA = okA && make_comp(score_key(sA), static_cast<uint32_t>(p.row_offset + rA)) < kth;
@@ -56,30 +62,71 @@ __device__ void accumulate_rows(const AttendParams& p, int b, int h, int kvh, in
     float cm = -INFINITY;
 #pragma unroll
     for (int w = 0; w < 4; ++w) cm = fmaxf(cm, s_scr[w]);
-    const float mn = fmaxf(m, cm);
-    if (mn != -INFINITY) {
-      const float fold = (m == -INFINITY) ? 0.f : exp2f(m - mn);
-      float lsum = 0.f, osum = 0.f;
-      for (int r = 0; r < 128; ++r) {
-        const float z = s_z[r];
-        if (z == -INFINITY) continue;
-        const float w = exp2f(z - mn);
-        lsum += w;
-        if ((r & 1) == par) osum += w * __bfloat162float(vb[(base + r) * kD + d]);
+    const float mn = fmaxf(mrun, cm);
+    if (mn != -INFINITY) {  // block-uniform
+      const float fold = (mrun == -INFINITY) ? 0.f : exp2f(mrun - mn);
+      if (tid < 128) {  // weights, once per row, in place
+        const float z = s_z[tid];
+        const float w = z == -INFINITY ? 0.f : exp2f(z - mn);
+        s_z[tid] = w;
+        const float ws = warp_sum(w);
+        if (lane == 0) s_scr[8 + warp] = ws;
       }
-      l = l * fold + lsum;
-      o = o * fold + osum;
-      m = mn;
+      Gp::sync();
+      const float lsum = s_scr[8] + s_scr[9] + s_scr[10] + s_scr[11];
+      uint4 vv[8];
+      float wt[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int r = warp * 16 + 2 * u + half;
+        wt[u] = s_z[r];
+        vv[u] = wt[u] != 0.f ? ldg_stream(vb + (base + r) * kD) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] *= fold;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        acc[0] = fmaf(wt[u], bf16lo(vv[u].x), acc[0]);
+        acc[1] = fmaf(wt[u], bf16hi(vv[u].x), acc[1]);
+        acc[2] = fmaf(wt[u], bf16lo(vv[u].y), acc[2]);
+        acc[3] = fmaf(wt[u], bf16hi(vv[u].y), acc[3]);
+        acc[4] = fmaf(wt[u], bf16lo(vv[u].z), acc[4]);
+        acc[5] = fmaf(wt[u], bf16hi(vv[u].z), acc[5]);
+        acc[6] = fmaf(wt[u], bf16lo(vv[u].w), acc[6]);
+        acc[7] = fmaf(wt[u], bf16hi(vv[u].w), acc[7]);
+      }
+      lrun = lrun * fold + lsum;
+      mrun = mn;
     }
     Gp::sync();
   }
+  if (mrun == -INFINITY) return;  // no row of the range contributes
+  // per-lane partial sums → per-dimension totals (thread d of parity 0 takes the whole sum)
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j] += __shfl_xor_sync(kFull, acc[j], 16);
+  if (half == 0) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s_red[warp * kD + part * 8 + j] = acc[j];
+  }
+  Gp::sync();
+  const int d = tid & (kD - 1);
+  float tot = 0.f;
+  if (tid < kD) {
+#pragma unroll
+    for (int w = 0; w < NW; ++w) tot += s_red[w * kD + d];
+  }
+  const float F = (m == -INFINITY) ? 0.f : exp2f(m - mrun);
+  o = o * F + tot;
+  l = l * F + lrun;
+  m = mrun;
+  Gp::sync();
 }
 
 // Pinned-prefix rows [0, p) that the top-k did not select join the context softmax
 // (attention.py:152-154 unions them into the retrieved ids). Local rows of this shard only.
 template <class Gp = CtaGrp>
 __device__ void add_pinned(const AttendParams& p, int b, int h, int kvh, int64_t nctx, int kb,
-                           float zref, float& l, float& o, float* s_z, float* s_scr) {
+                           float zref, float& l, float& o, float* s_z, float* s_scr, float* s_red) {
   if (p.pinned <= 0 || kb <= 0) return;
   int64_t lo = -p.row_offset;
   if (lo < 0) lo = 0;
@@ -88,7 +135,7 @@ __device__ void add_pinned(const AttendParams& p, int b, int h, int kvh, int64_t
   if (hi <= lo) return;
   const int bh = b * p.Hq + h;
   float m = zref;
-  accumulate_rows<Gp>(p, b, h, kvh, lo, hi, true, __ldcg(&p.meta_kth[bh]), m, l, o, s_z, s_scr);
+  accumulate_rows<Gp>(p, b, h, kvh, lo, hi, true, __ldcg(&p.meta_kth[bh]), m, l, o, s_z, s_scr, s_red);
   // every unselected row scores <= the k-th selected score <= M, so m stays zref
 }
 
@@ -96,7 +143,7 @@ __device__ void add_pinned(const AttendParams& p, int b, int h, int kvh, int64_t
 // thread's share (d = tid % 128, parity tid / 128). Writes out[bh, :].
 template <class Gp = CtaGrp>
 __device__ void finalize_head(const AttendParams& p, int b, int h, int kvh, int64_t nctx, float zref,
-                              float l_c, float o_c, float* s_z, float* s_scr, float* s_o) {
+                              float l_c, float o_c, float* s_z, float* s_scr, float* s_o, float* s_red) {
   const int tid = Gp::tid();
   const int bh = b * p.Hq + h;
   // precondition n_ctx + n_win <= cache_rows (tkv.h); a window past the cache is clamped
@@ -104,7 +151,8 @@ __device__ void finalize_head(const AttendParams& p, int b, int h, int kvh, int6
   int64_t nwin = p.n_win ? p.n_win[b] : 0;
   if (nwin > p.cache_rows - nctx) nwin = p.cache_rows - nctx;
   float m_w = -INFINITY, l_w = 0.f, o_w = 0.f;
-  if (nwin > 0) accumulate_rows<Gp>(p, b, h, kvh, nctx, nctx + nwin, false, 0ull, m_w, l_w, o_w, s_z, s_scr);
+  if (nwin > 0)
+    accumulate_rows<Gp>(p, b, h, kvh, nctx, nctx + nwin, false, 0ull, m_w, l_w, o_w, s_z, s_scr, s_red);
   float val;
   if (p.combine == 0) {  // joint (attention.py:109-114)
     const float mm = fmaxf(l_c > 0.f ? zref : -INFINITY, m_w);
@@ -209,7 +257,7 @@ __device__ void head_finish(const AttendParams& p, int bh, int nslots, AttSmem& 
     if (tid < kD) o_c += __ldcg(&p.part_o[(static_cast<int64_t>(bh) * p.nchunks + c2) * kD + tid]);
     l_c += __ldcg(&p.part_l[static_cast<int64_t>(bh) * p.nchunks + c2]);
   }
-  add_pinned<Gp>(p, b, h, kvh, nctx, kb, zref, l_c, o_c, sm.z, sm.scr);
+  add_pinned<Gp>(p, b, h, kvh, nctx, kb, zref, l_c, o_c, sm.z, sm.scr, &sm.red[0][0]);
   if (p.partial_only) {
     sm.o[tid] = o_c;
     Gp::sync();
@@ -219,7 +267,7 @@ __device__ void head_finish(const AttendParams& p, int bh, int nslots, AttSmem& 
     Gp::sync();
     return;
   }
-  finalize_head<Gp>(p, b, h, kvh, nctx, zref, l_c, o_c, sm.z, sm.scr, sm.o);
+  finalize_head<Gp>(p, b, h, kvh, nctx, zref, l_c, o_c, sm.z, sm.scr, sm.o, &sm.red[0][0]);
   Gp::sync();
 }
 

@@ -60,16 +60,25 @@ class TopkDecoder:
         self.ws = ops.Workspace(prob, dev)
         D = ops.HEAD_DIM
         bf, f32, i32 = torch.bfloat16, torch.float32, torch.int32
+        # q, k_new and v_new share one staging buffer on each side, so a step moves its inputs
+        # with a single host→device copy
+        nq, nkv = self.B * Hq * D, self.B * self.Hkv * D
+        in_d = torch.empty(nq + 2 * nkv, dtype=bf, device=dev)
+        in_h = torch.empty(nq + 2 * nkv, dtype=bf, pin_memory=True)
+
+        def views(buf):
+            return (buf[:nq].view(self.B, Hq, D), buf[nq:nq + nkv].view(self.B, self.Hkv, D),
+                    buf[nq + nkv:].view(self.B, self.Hkv, D))
+
+        q_d, k_d, v_d = views(in_d)
+        q_h, k_h, v_h = views(in_h)
         self._bufs = dict(
-            q=torch.empty((self.B, Hq, D), dtype=bf, device=dev),
-            k_new=torch.empty((self.B, self.Hkv, D), dtype=bf, device=dev),
-            v_new=torch.empty((self.B, self.Hkv, D), dtype=bf, device=dev),
+            in_d=in_d, in_h=in_h, nq=nq,
+            q=q_d, k_new=k_d, v_new=v_d,
             out=torch.empty((self.B, Hq, D), dtype=f32, device=dev),
             idx=torch.empty((self.B, Hq, self.k), dtype=i32, device=dev),
             scores=torch.empty((self.B, Hq, self.k), dtype=f32, device=dev),
-            q_h=torch.empty((self.B, Hq, D), dtype=bf, pin_memory=True),
-            k_h=torch.empty((self.B, self.Hkv, D), dtype=bf, pin_memory=True),
-            v_h=torch.empty((self.B, self.Hkv, D), dtype=bf, pin_memory=True),
+            q_h=q_h, k_h=k_h, v_h=v_h,
             out_h=torch.empty((self.B, Hq, D), dtype=f32, pin_memory=True),
             idx_h=torch.empty((self.B, Hq, self.k), dtype=i32, pin_memory=True),
         )
@@ -98,10 +107,11 @@ class TopkDecoder:
     def _host_step_body(self, with_kv: bool, with_idx: bool) -> None:
         """Everything a host-I/O step enqueues, reading/writing the pinned staging buffers."""
         b = self._bufs
-        b["q"].copy_(b["q_h"], non_blocking=True)
+        if with_kv:  # one copy: q | k_new | v_new
+            b["in_d"].copy_(b["in_h"], non_blocking=True)
+        else:
+            b["q"].copy_(b["q_h"], non_blocking=True)
         if with_kv:
-            b["k_new"].copy_(b["k_h"], non_blocking=True)
-            b["v_new"].copy_(b["v_h"], non_blocking=True)
             ops.kv_append(self.k_cache, self.v_cache, b["k_new"], b["v_new"], self.n_win,
                           base=self.n_ctx, advance=True)
         ops.topk_decode_attention(b["q"], self.k_cache, self.v_cache, self.n_ctx, self.k,
