@@ -226,14 +226,29 @@ int run_prefix(const tkv_problem* p, const void* q, const void* k_cache, const i
   return TKV_OK;
 }
 
+}  // namespace
+
+// Programmatic dependent launch between sample → threshold → scan → k-th (default on;
+// TKV_PDL=0 disables it, e.g. for A/B timing).
+bool tkv::pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TKV_PDL");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
+namespace {
+
 bool use_tc_scan(const tkv_problem* p, const ScanParams& cp) {
   return !(p->flags & TKV_F_SCAN_HMMA) && scan_tc_supported(cp);
 }
 
 // key scan of segments [s0, s1) on stream `st`
-int run_scan_part(const tkv_problem* p, ScanParams cp, int64_t s0, int64_t s1, cudaStream_t st) {
+int run_scan_part(const tkv_problem* p, ScanParams cp, int64_t s0, int64_t s1, cudaStream_t st, bool pdl) {
   cp.seg_begin = s0;
   cp.seg_count = s1 - s0;
+  cp.pdl = pdl ? 1 : 0;
   if (use_tc_scan(p, cp))
     TKV_LAUNCH(launch_scan_tc(cp, st));
   else
@@ -245,11 +260,13 @@ int run_scan_part(const tkv_problem* p, ScanParams cp, int64_t s0, int64_t s1, c
 // k-th of failing heads, tail-launched on device); the selected set of a head is
 // { candidates c : c >= meta_kth }, materialised by run_emit
 int run_kth_part(const tkv_problem* p, ScanParams cp, SelectParams sl, int64_t s0, int64_t s1, int part,
-                 cudaStream_t st) {
+                 cudaStream_t st, bool pdl) {
   const int G = p->n_q_heads / p->n_kv_heads;
   cp.seg_begin = s0;
   cp.seg_count = s1 - s0;
   cp.fallback = 1;
+  cp.pdl = 0;  // the device-launched fallback scan
+  sl.pdl = pdl ? 1 : 0;
   sl.bh_begin = static_cast<int>(s0 * G);
   sl.bh_count = static_cast<int>((s1 - s0) * G);
   sl.hs.fb_launched += part;
@@ -379,9 +396,11 @@ int run_layer(const tkv_problem* p, const void* q, const void* k_cache, const vo
     const bool prof = g_scan_start && g_scan_stop;
     if (P == 1) {
       if (prof) cudaEventRecord(g_scan_start, st);
-      TRY(run_scan_part(p, cp, 0, nseg, st));
+      // with the profiling events in the stream the launches stay ordinary (an event record
+      // between two kernels would hide the overlap anyway)
+      TRY(run_scan_part(p, cp, 0, nseg, st, pdl_enabled() && !prof));
       if (prof) cudaEventRecord(g_scan_stop, st);
-      TRY(run_kth_part(p, cp, sl, 0, nseg, 0, st));
+      TRY(run_kth_part(p, cp, sl, 0, nseg, 0, st, pdl_enabled() && !prof));
       return run_emit(p, q, k_cache, v_cache, n_ctx, n_win, idx, scores, packed, out, gather, ws, L, st, 0,
                       static_cast<int>(nseg * G));
     }
@@ -393,11 +412,12 @@ int run_layer(const tkv_problem* p, const void* q, const void* k_cache, const vo
     }();
     if (serial) {
       if (prof) cudaEventRecord(g_scan_start, st);
-      for (int part = 0; part < P; ++part) TRY(run_scan_part(p, cp, nseg * part / P, nseg * (part + 1) / P, st));
+      for (int part = 0; part < P; ++part)
+        TRY(run_scan_part(p, cp, nseg * part / P, nseg * (part + 1) / P, st, false));
       if (prof) cudaEventRecord(g_scan_stop, st);
       for (int part = 0; part < P; ++part) {
         const int64_t s0 = nseg * part / P, s1 = nseg * (part + 1) / P;
-        TRY(run_kth_part(p, cp, sl, s0, s1, part, st));
+        TRY(run_kth_part(p, cp, sl, s0, s1, part, st, false));
         TRY(run_emit(p, q, k_cache, v_cache, n_ctx, n_win, idx, scores, packed, out, gather, ws, L, st,
                      static_cast<int>(s0 * G), static_cast<int>((s1 - s0) * G)));
       }
@@ -406,10 +426,10 @@ int run_layer(const tkv_problem* p, const void* q, const void* k_cache, const vo
     if (prof) cudaEventRecord(g_scan_start, st);
     for (int part = 0; part < P; ++part) {
       const int64_t s0 = nseg * part / P, s1 = nseg * (part + 1) / P;
-      TRY(run_scan_part(p, cp, s0, s1, st));
+      TRY(run_scan_part(p, cp, s0, s1, st, false));
       if (cudaEventRecord(r->ev[part], st) != cudaSuccess || cudaStreamWaitEvent(r->side, r->ev[part], 0) != cudaSuccess)
         return fail(TKV_ECUDA, "pipeline fork failed");
-      TRY(run_kth_part(p, cp, sl, s0, s1, part, r->side));
+      TRY(run_kth_part(p, cp, sl, s0, s1, part, r->side, false));
       TRY(run_emit(p, q, k_cache, v_cache, n_ctx, n_win, idx, scores, packed, out, gather, ws, L, r->side,
                    static_cast<int>(s0 * G), static_cast<int>((s1 - s0) * G)));
     }

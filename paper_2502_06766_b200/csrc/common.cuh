@@ -320,6 +320,13 @@ __device__ void radix_select_u64(Load load, int64_t n, uint32_t need, uint32_t* 
   prefix_out = prefix;
 }
 
+// Programmatic dependent launch (sm_90+): a kernel launched with programmatic stream
+// serialisation may start while its predecessor still runs; pdl_wait() blocks until the
+// predecessor grid has completed and its memory is visible, pdl_trigger() lets this grid's
+// successor launch early. Both are no-ops for ordinary launches.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

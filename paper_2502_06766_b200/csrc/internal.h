@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 namespace tkv {
 
 constexpr int kSamples = 4096;       // sampled rows per (b, kv head) for the threshold estimate
@@ -76,6 +78,7 @@ struct ScanParams {
   HeadState hs;
   int fallback;
   int64_t seg_begin, seg_count;  // (b, kv head) segments to scan; seg_count 0 = all B*Hkv
+  int pdl;                       // launch with programmatic dependent launch (see launch_pdl)
 };
 
 enum SelectPass { kPassMain = 0, kPassFallback = 1, kPassMerge = 2 };
@@ -96,6 +99,7 @@ struct SelectParams {
   uint64_t* packed_out;  // optional [B*Hq*k] composites (shard candidates)
   int pass;
   int bh_begin, bh_count;  // heads handled (kth_kernel); bh_count 0 = all B*Hq
+  int pdl;                 // launch kth_kernel with programmatic dependent launch
   // exactness fallback, tail-launched by kth_kernel (main pass) when a head failed
   ScanParams fb_scan;
   int fb_scan_grid;
@@ -184,6 +188,25 @@ struct FusedParams {
 };
 constexpr int kFusedKS = 4;
 __host__ __device__ inline int fused_ctl_words(int NG, int NH) { return 8 + 2 * NG + 5 * NH; }
+
+// Launch with programmatic stream serialisation (the kernel calls pdl_wait() before touching
+// its predecessor's outputs), or an ordinary launch when pdl is false.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+bool pdl_enabled();
 
 cudaError_t launch_fused(const FusedParams& p, cudaStream_t s);
 cudaError_t launch_fused_tc(FusedParams p, cudaStream_t s);

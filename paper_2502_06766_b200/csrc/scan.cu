@@ -28,6 +28,7 @@
 namespace tkv {
 
 __global__ void __launch_bounds__(kSampleThreads) sample_kernel(SampleParams p) {
+  pdl_trigger();  // the threshold kernel may launch now; it waits for this grid's samples
   const int seg = blockIdx.y;
   const int b = seg / p.Hkv, kvh = seg % p.Hkv;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -65,6 +66,8 @@ __global__ void __launch_bounds__(kThrThreads) threshold_kernel(SampleParams p) 
   __shared__ uint32_t s_scr[32];
   __shared__ uint32_t s_out[2];
   __shared__ uint32_t s_max[32];
+  pdl_trigger();  // the scan may launch now: its TMA / MMA warps need no threshold
+  pdl_wait();     // samples of the sample kernel
   const int bh = blockIdx.x;
   const int b = bh / p.Hq;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -158,6 +161,8 @@ __global__ void __launch_bounds__(kThrThreads) threshold_kernel(SampleParams p) 
 __global__ void __launch_bounds__(kScanWarps * 32, 2) scan_kernel(ScanParams p) {
   extern __shared__ uint64_t s_buf[];  // [G][kScanStage]
   __shared__ uint32_t s_cnt[8];
+  pdl_trigger();
+  pdl_wait();  // thresholds, zeroed counters and histograms of threshold_kernel
   scan_body(p, s_buf, s_cnt);
 }
 
@@ -168,8 +173,7 @@ cudaError_t launch_sample(const SampleParams& p, cudaStream_t s) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
-  threshold_kernel<<<p.B * p.Hq, kThrThreads, 0, s>>>(p);
-  return cudaGetLastError();
+  return launch_pdl(threshold_kernel, dim3(p.B * p.Hq), dim3(kThrThreads), 0, s, pdl_enabled() && !p.no_filter, p);
 }
 
 static int scan_grid(int G, size_t smem) {
@@ -226,8 +230,7 @@ cudaError_t launch_scan(const ScanParams& p, cudaStream_t s) {
   if (total == 0) return cudaSuccess;
   int grid = scan_grid(p.G, smem);
   if (total < grid) grid = static_cast<int>(total);
-  scan_kernel<<<grid, kScanWarps * 32, smem, s>>>(p);
-  return cudaGetLastError();
+  return launch_pdl(scan_kernel, dim3(grid), dim3(kScanWarps * 32), smem, s, p.pdl != 0, p);
 }
 
 }  // namespace tkv

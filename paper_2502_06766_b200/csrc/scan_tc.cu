@@ -89,6 +89,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) scan_tc_kernel(const __grid_con
   __shared__ __align__(8) uint64_t s_bar[kTcBarWords];
   __shared__ uint32_t s_tmem;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  pdl_trigger();  // the k-th kernel may launch now; it waits for this grid to complete
   TcPipe t = tc_setup(smem_raw, s_bar, &s_tmem, p.G, flush_every, n_stages, &kmap, tid == 0, warp == 1);
   tc_fence_before();
   __syncthreads();
@@ -116,6 +117,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) scan_tc_kernel(const __grid_con
       tc_mma_issue(t, i, slot, lane, mode);
     }
   } else {  // epilogue
+    pdl_wait();  // thresholds, zeroed counters and histograms of threshold_kernel (the TMA and
+                 // MMA warps read only q and K and start streaming before it completes)
     const int ew = warp - 2;
     const int quarter = warp & 3;  // TMEM lanes this warp may access: [32·quarter, +32)
     uint64_t* wbuf = t.s_buf + static_cast<int64_t>(ew) * p.G * t.cap;
@@ -230,8 +233,8 @@ cudaError_t launch_scan_tc(const ScanParams& p, cudaStream_t s) {
   }();
   int grid = sms;
   if (total < grid) grid = static_cast<int>(total);
-  scan_tc_kernel<<<grid, kTcThreads, smem, s>>>(map, p, sh.stages, sh.flush, mode);
-  return cudaGetLastError();
+  return launch_pdl(scan_tc_kernel, dim3(grid), dim3(kTcThreads), smem, s, p.pdl != 0, map, p, sh.stages,
+                    sh.flush, mode);
 }
 
 }  // namespace tkv

@@ -329,6 +329,7 @@ __global__ void __launch_bounds__(kKthThreads) kth_kernel(SelectParams p) {
   __shared__ uint64_t s_rmax[KW];
   __shared__ int s_last;
 
+  pdl_wait();  // candidates and histograms of the scan
   const int bh = p.bh_begin + blockIdx.y, part = blockIdx.x, P = gridDim.x;
   const int b = bh / p.Hq, h = bh % p.Hq;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -511,8 +512,8 @@ cudaError_t launch_kth(const SelectParams& p, cudaStream_t s) {
     cudaFuncSetAttribute(kth_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     carve = true;
   }
-  kth_kernel<<<dim3(kKthCtas, p.bh_count ? p.bh_count : p.B * p.Hq), kKthThreads, kKthSmem, s>>>(p);
-  return cudaGetLastError();
+  return launch_pdl(kth_kernel, dim3(kKthCtas, p.bh_count ? p.bh_count : p.B * p.Hq), dim3(kKthThreads), kKthSmem, s,
+                    p.pdl && p.pass == kPassMain, p);
 }
 
 // ---------------------------------------------------------------- optional sorted output
