@@ -176,6 +176,15 @@ int tkv_last_launch_count(void);
 int tkv_profile_scan_events(void* start, void* stop);
 
 /*
+ * Diagnostics: with a non-NULL device buffer of 16 uint64 (even slots initialised to
+ * UINT64_MAX, odd slots to 0), subsequent multi-kernel compute calls on this thread record
+ * %globaltimer first-start / last-end stamps of: 0 sample, 1 threshold, 2 threshold past its
+ * dependency wait, 3 key scan, 4 scan epilogue past its dependency wait, 5 k-th, 6 gather.
+ * NULL disables.
+ */
+int tkv_debug_timeline(void* buf);
+
+/*
  * Measurement hook: with a non-NULL device buffer of n_items × 4 uint64, the fused layer-step
  * kernel records, per work item index i < n_items, {start ns, end ns, type << 32 | cta,
  * a << 32 | b} (%globaltimer). NULL disables. Diagnostic only.

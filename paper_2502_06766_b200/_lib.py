@@ -34,6 +34,7 @@ EXPORTS = (
     "tkv_shard_finalize",
     "tkv_last_launch_count",
     "tkv_profile_scan_events",
+    "tkv_debug_timeline",
     "tkv_debug_trace",
     "tkv_convert_rows_f32",
 )
@@ -77,6 +78,7 @@ _SIG = {
     "tkv_device_check": ([], _I),
     "tkv_last_launch_count": ([], _I),
     "tkv_profile_scan_events": ([_P, _P], _I),
+    "tkv_debug_timeline": ([_P], _I),
     "tkv_debug_trace": ([_P, ctypes.c_uint32], _I),
     "tkv_convert_rows_f32": ([_P, ctypes.c_int64, ctypes.c_int32, _P, _P], _I),
     "tkv_workspace_bytes": ([ctypes.POINTER(Problem), ctypes.POINTER(ctypes.c_size_t)], _I),

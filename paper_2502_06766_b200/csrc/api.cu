@@ -23,6 +23,7 @@ thread_local std::string g_err;
 thread_local int g_launches = 0;
 thread_local cudaEvent_t g_scan_start = nullptr, g_scan_stop = nullptr;
 thread_local uint64_t* g_trace = nullptr;
+thread_local uint64_t* g_tl = nullptr;
 thread_local uint32_t g_trace_cap = 0;
 
 int fail(int code, const char* fmt, ...) {
@@ -186,6 +187,7 @@ int run_prefix(const tkv_problem* p, const void* q, const void* k_cache, const i
   sp.no_filter = (p->flags & TKV_F_NO_FILTER) ? 1 : 0;
   sp.samp = at<uint32_t>(ws, L.samp);
   sp.hs = hs;
+  sp.tl = g_tl;
   TKV_LAUNCH(launch_sample(sp, st));
   if (!sp.no_filter) ++g_launches;  // sample + threshold kernels
 
@@ -204,6 +206,7 @@ int run_prefix(const tkv_problem* p, const void* q, const void* k_cache, const i
   cp.cap = L.cap;
   cp.hs = hs;
   cp.fallback = 0;
+  cp.tl = g_tl;
   cp.seg_begin = 0;
   cp.seg_count = static_cast<int64_t>(p->batch) * p->n_kv_heads;
 
@@ -221,6 +224,7 @@ int run_prefix(const tkv_problem* p, const void* q, const void* k_cache, const i
   sl.meta_kb = at<int32_t>(ws, L.mkb);
   sl.hs = hs;
   sl.pass = kPassMain;
+  sl.tl = g_tl;
   *cp_out = cp;
   *sl_out = sl;
   return TKV_OK;
@@ -355,6 +359,7 @@ AttendParams make_attend(const tkv_problem* p, const void* q, const void* k_cach
   a.cap = L.cap;
   a.cand_cnt = at<uint32_t>(ws, L.cnt);
   a.out_cnt = at<uint32_t>(ws, L.outc);
+  a.tl = g_tl;
   return a;
 }
 
@@ -508,6 +513,11 @@ int tkv_last_launch_count(void) { return g_launches; }
 int tkv_debug_trace(void* buf, uint32_t n_items) {
   g_trace = static_cast<uint64_t*>(buf);
   g_trace_cap = buf ? n_items : 0u;
+  return TKV_OK;
+}
+
+int tkv_debug_timeline(void* buf) {
+  g_tl = static_cast<uint64_t*>(buf);
   return TKV_OK;
 }
 

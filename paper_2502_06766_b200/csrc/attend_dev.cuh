@@ -181,18 +181,17 @@ struct AttSmem {
   int last;
 };
 
-// Gather the V rows listed in sm.row (local rows, -1 = skip) weighted by sm.w and reduce them
-// into the head's partial slot (l, o[128]). Ends with a barrier (smem reusable).
+// Accumulate the V rows listed in sm.row (local rows, -1 = skip) weighted by sm.w into this
+// thread's registers: lane part·8 .. +7 of the 128 dims (16 lanes per 256-byte row, 16-byte
+// loads, 8 rows in flight per half-warp), and the weight sum. Leaves sm.row / sm.w intact.
 template <class Gp = CtaGrp>
-__device__ void gather_partial(const AttendParams& p, int bh, int slot, int nrows, AttSmem& sm) {
+__device__ void gather_acc(const AttendParams& p, int bh, int nrows, const AttSmem& sm, float (&acc)[8],
+                           float& lw) {
   const int b = bh / p.Hq, h = bh % p.Hq, kvh = h / p.G;
   const int tid = Gp::tid(), lane = tid & 31, warp = tid >> 5;
   const int half = lane >> 4, part = lane & 15;
   const __nv_bfloat16* vb =
       p.vc + (static_cast<int64_t>(b) * p.Hkv + kvh) * p.cache_rows * kD + part * 8;
-  float acc[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) acc[j] = 0.f;
   constexpr int UNR = 8;
   for (int r0 = warp * 2 + half; r0 < nrows; r0 += 2 * NW * UNR) {
     uint4 v[UNR];
@@ -216,14 +215,22 @@ __device__ void gather_partial(const AttendParams& p, int bh, int slot, int nrow
       acc[7] = fmaf(w[u], bf16hi(v[u].w), acc[7]);
     }
   }
+  for (int i = tid; i < nrows; i += NT) lw += sm.w[i];
+}
+
+// Reduce the per-thread (acc, lw) of gather_acc over the block into the head's partial slot
+// (l, o[128]). Ends with a barrier (smem reusable).
+template <class Gp = CtaGrp>
+__device__ void partial_write(const AttendParams& p, int bh, int slot, AttSmem& sm, float (&acc)[8], float lw) {
+  const int tid = Gp::tid(), lane = tid & 31, warp = tid >> 5;
+  const int half = lane >> 4, part = lane & 15;
 #pragma unroll
   for (int j = 0; j < 8; ++j) acc[j] += __shfl_xor_sync(kFull, acc[j], 16);
+  Gp::sync();  // sm.row / sm.w readers are done before the reduction buffers are reused
   if (half == 0) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) sm.red[warp][part * 8 + j] = acc[j];
   }
-  float lw = 0.f;
-  for (int i = tid; i < nrows; i += NT) lw += sm.w[i];
   lw = warp_sum(lw);
   if (lane == 0) sm.l[warp] = lw;
   Gp::sync();
@@ -240,6 +247,18 @@ __device__ void gather_partial(const AttendParams& p, int bh, int slot, int nrow
     p.part_l[static_cast<int64_t>(bh) * p.nchunks + slot] = l;
   }
   Gp::sync();
+}
+
+// Gather the V rows listed in sm.row weighted by sm.w and reduce them into the head's partial
+// slot (l, o[128]). Ends with a barrier (smem reusable).
+template <class Gp = CtaGrp>
+__device__ void gather_partial(const AttendParams& p, int bh, int slot, int nrows, AttSmem& sm) {
+  float acc[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+  float lw = 0.f;
+  gather_acc<Gp>(p, bh, nrows, sm, acc, lw);
+  partial_write<Gp>(p, bh, slot, sm, acc, lw);
 }
 
 // The last CTA of a head (caller decided, after a __threadfence): combine the nslots partials

@@ -327,6 +327,20 @@ __device__ void radix_select_u64(Load load, int64_t n, uint32_t need, uint32_t* 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// Diagnostics (tkv_debug_timeline): first-start (slot 2e) / last-end (slot 2e+1) %globaltimer
+// stamps of pipeline event e; tl == nullptr when not requested.
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void tl_start(uint64_t* tl, int e) {
+  if (tl) atomicMin(reinterpret_cast<unsigned long long*>(tl + 2 * e), static_cast<unsigned long long>(gtimer()));
+}
+__device__ __forceinline__ void tl_end(uint64_t* tl, int e) {
+  if (tl) atomicMax(reinterpret_cast<unsigned long long*>(tl + 2 * e + 1), static_cast<unsigned long long>(gtimer()));
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

@@ -855,17 +855,14 @@ __global__ void __launch_bounds__(kFtcThreads, 1) fused_tc_kernel(const __grid_c
     }
   } else if (warp == 1) {  // MMA issuer
     uint32_t i = 0;
-    int slot = -1;
+    QRing qr;
     for (int g = 0; g < NG; ++g) {
       int64_t lo, hi;
       group_share(p, g, ups, lo, hi);
       for (int64_t u = lo; u < hi; ++u, ++i) {
         tc_mma_acquire(t, i);
-        if (u == lo) {
-          slot = (slot + 1) % kTcQSlots;
-          tc_load_q(t, slot, a.q + static_cast<int64_t>(g) * a.G * kD, a.G, lane);
-        }
-        tc_mma_issue(t, i, slot, lane, 0);
+        if (u == lo) tc_next_q(t, qr, a.q + static_cast<int64_t>(g) * a.G * kD, a.G, lane);
+        tc_mma_issue(t, i, qr.slot, lane, 0);
       }
     }
   } else if (warp < kTcThreads / 32) {  // epilogue

@@ -25,7 +25,10 @@ constexpr int kKthSmemBucket = 2048;    // threshold-bucket members rank-selecte
 constexpr int kKthSmem = kKthSmemBucket * 8;  // kth_kernel dynamic shared memory (fits beside the scan)
 constexpr int kAttendThreads = 256;
 constexpr int kAttendChunk = 512;    // selected rows per gather CTA (list mode)
-constexpr int kCandChunk = 1024;     // candidates per work item (candidate mode)
+#ifndef TKV_CAND_CHUNK
+#define TKV_CAND_CHUNK 1024
+#endif
+constexpr int kCandChunk = TKV_CAND_CHUNK;  // candidates per work item (candidate mode)
 constexpr int kSortMax = 16384;      // sorted output supported up to this k
 constexpr uint32_t kNoFilterShift = 20;  // histogram shift when every score is a candidate
 constexpr int kMinSampleStride = 8;      // small contexts sample at most every 8th row
@@ -55,6 +58,7 @@ struct HeadState {
 };
 
 struct SampleParams {
+  uint64_t* tl;  // diagnostics timeline (tkv_debug_timeline), nullptr normally
   const __nv_bfloat16* q;
   const __nv_bfloat16* kc;
   int64_t cache_rows;
@@ -66,6 +70,7 @@ struct SampleParams {
 };
 
 struct ScanParams {
+  uint64_t* tl;  // diagnostics timeline (tkv_debug_timeline), nullptr normally
   const __nv_bfloat16* q;
   const __nv_bfloat16* kc;
   int64_t cache_rows;
@@ -84,6 +89,7 @@ struct ScanParams {
 enum SelectPass { kPassMain = 0, kPassFallback = 1, kPassMerge = 2 };
 
 struct SelectParams {
+  uint64_t* tl;  // diagnostics timeline (tkv_debug_timeline), nullptr normally
   const uint64_t* src;   // candidates: src + bh*src_stride (main/fallback)
   int64_t src_stride;    // merge: element i of head bh is
   int64_t shard_stride;  //   src[(i / k) * shard_stride + bh * k + i % k]
@@ -118,6 +124,7 @@ struct SortParams {
 };
 
 struct AttendParams {
+  uint64_t* tl;  // diagnostics timeline (tkv_debug_timeline), nullptr normally
   const __nv_bfloat16* q;
   const __nv_bfloat16* kc;
   const __nv_bfloat16* vc;

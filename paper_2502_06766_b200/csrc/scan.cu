@@ -29,6 +29,7 @@ namespace tkv {
 
 __global__ void __launch_bounds__(kSampleThreads) sample_kernel(SampleParams p) {
   pdl_trigger();  // the threshold kernel may launch now; it waits for this grid's samples
+  if (threadIdx.x == 0) tl_start(p.tl, 0);
   const int seg = blockIdx.y;
   const int b = seg / p.Hkv, kvh = seg % p.Hkv;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -57,6 +58,7 @@ __global__ void __launch_bounds__(kSampleThreads) sample_kernel(SampleParams p) 
         p.samp[(static_cast<int64_t>(b) * p.Hq + kvh * p.G + col) * kSamples + s] = score_key(acc[i]);
     }
   }
+  if (threadIdx.x == 0) tl_end(p.tl, 0);
 }
 
 __global__ void __launch_bounds__(kThrThreads) threshold_kernel(SampleParams p) {
@@ -67,7 +69,9 @@ __global__ void __launch_bounds__(kThrThreads) threshold_kernel(SampleParams p) 
   __shared__ uint32_t s_out[2];
   __shared__ uint32_t s_max[32];
   pdl_trigger();  // the scan may launch now: its TMA / MMA warps need no threshold
+  if (threadIdx.x == 0) tl_start(p.tl, 1);
   pdl_wait();     // samples of the sample kernel
+  if (threadIdx.x == 0) tl_start(p.tl, 2);
   const int bh = blockIdx.x;
   const int b = bh / p.Hq;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -154,6 +158,7 @@ __global__ void __launch_bounds__(kThrThreads) threshold_kernel(SampleParams p) 
     p.hs.max_comp[bh] = 0ull;
     p.hs.bkt_cnt[bh] = 0u;
     p.hs.out_cnt[bh] = 0u;
+    tl_end(p.tl, 1);
   }
 }
 

@@ -82,7 +82,7 @@ struct UnitWalk {
   }
 };
 
-__global__ void __launch_bounds__(kTcThreads, 1) scan_tc_kernel(const __grid_constant__ CUtensorMap kmap,
+__global__ void __launch_bounds__(kTcScanThreads, 1) scan_tc_kernel(const __grid_constant__ CUtensorMap kmap,
                                                                 ScanParams p, int n_stages, int flush_every,
                                                                 int mode) {
   extern __shared__ uint8_t smem_raw[];
@@ -90,7 +90,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) scan_tc_kernel(const __grid_con
   __shared__ uint32_t s_tmem;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   pdl_trigger();  // the k-th kernel may launch now; it waits for this grid to complete
-  TcPipe t = tc_setup(smem_raw, s_bar, &s_tmem, p.G, flush_every, n_stages, &kmap, tid == 0, warp == 1);
+  if (tid == 0) tl_start(p.tl, 3);
+  TcPipe t = tc_setup(smem_raw, s_bar, &s_tmem, p.G, flush_every, n_stages, &kmap, tid == 0, warp == 1,
+                      kTcScanGroups);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -107,19 +109,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) scan_tc_kernel(const __grid_con
     for (uint32_t i = 0; w.next(p, new_seg); ++i)
       tc_produce(t, i, &kmap, static_cast<int>(w.cur_seg * p.cache_rows + w.cur_row0), lane, mode);
   } else if (warp == 1) {  // MMA issuer
-    int slot = -1;
+    QRing qr;
     for (uint32_t i = 0; w.next(p, new_seg); ++i) {
       tc_mma_acquire(t, i);
-      if (new_seg) {
-        slot = (slot + 1) % kTcQSlots;
-        tc_load_q(t, slot, p.q + (static_cast<int64_t>(w.cur_b) * p.Hq + w.cur_kvh * p.G) * kD, p.G, lane);
-      }
-      tc_mma_issue(t, i, slot, lane, mode);
+      if (new_seg) tc_next_q(t, qr, p.q + (static_cast<int64_t>(w.cur_b) * p.Hq + w.cur_kvh * p.G) * kD, p.G, lane);
+      tc_mma_issue(t, i, qr.slot, lane, mode);
     }
-  } else {  // epilogue
+  } else {  // epilogue: two groups of four warps take alternate units
     pdl_wait();  // thresholds, zeroed counters and histograms of threshold_kernel (the TMA and
                  // MMA warps read only q and K and start streaming before it completes)
+    if (lane == 0) tl_start(p.tl, 4);
     const int ew = warp - 2;
+    const uint32_t group = static_cast<uint32_t>(ew / kTcEpiWarps);
     const int quarter = warp & 3;  // TMEM lanes this warp may access: [32·quarter, +32)
     uint64_t* wbuf = t.s_buf + static_cast<int64_t>(ew) * p.G * t.cap;
     uint32_t thr[8], shift[8], cnt[8];
@@ -138,6 +139,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) scan_tc_kernel(const __grid_con
           shift[n] = n < p.G ? p.hs.hshift[bh0 + n] : 0u;
         }
       }
+      if (i % kTcScanGroups != group) continue;
       uint32_t v[16];
       tc_epi_load(t, i, quarter, lane, v, mode);
       tc_epi_emit(v, w.cur_row0, w.cur_nctx, quarter, lane, p.G, p.row_offset, thr, wbuf, t.cap, cnt,
@@ -148,11 +150,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) scan_tc_kernel(const __grid_con
       }
     }
     if (bh0 >= 0) tc_warp_flush(p.cand, p.cap, p.hs.cand_cnt, p.hs.hist, p.G, bh0, wbuf, t.cap, cnt, thr, shift, lane);
+    if (lane == 0) tl_end(p.tl, 4);
   }
 
   tc_fence_before();
   __syncthreads();
   tc_teardown(t.tmem, warp == 1);
+  if (tid == 0) tl_end(p.tl, 3);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -206,16 +210,16 @@ cudaError_t launch_scan_tc(const ScanParams& p, cudaStream_t s) {
     const char* e = getenv("TKV_TC_FLUSH");
     return e ? atoi(e) : 0;
   }();
-  TcShape sh = tc_shape(p.G);
+  TcShape sh = tc_shape(p.G, kTcScanGroups);
   if (stages_env >= 2 && stages_env <= kTcMaxStages && stages_env != sh.stages) {
     sh.stages = stages_env;
     const int free_b = kTcSmemLimit - 1024 - kTcQSlots * kTcQBytes - sh.stages * kTcUnitBytes;
-    sh.flush = free_b / tc_stage_bytes(p.G, 1);
+    sh.flush = free_b / tc_stage_bytes(p.G, 1, kTcScanGroups);
     if (sh.flush > kTcMaxFlush) sh.flush = kTcMaxFlush;
     if (sh.flush < 1) return cudaErrorInvalidValue;
   }
   if (flush_env > 0 && flush_env < sh.flush) sh.flush = flush_env;
-  const size_t smem = tc_smem_bytes(p.G, sh);
+  const size_t smem = tc_smem_bytes(p.G, sh, kTcScanGroups);
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(scan_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmemLimit);
@@ -233,7 +237,7 @@ cudaError_t launch_scan_tc(const ScanParams& p, cudaStream_t s) {
   }();
   int grid = sms;
   if (total < grid) grid = static_cast<int>(total);
-  return launch_pdl(scan_tc_kernel, dim3(grid), dim3(kTcThreads), smem, s, p.pdl != 0, map, p, sh.stages,
+  return launch_pdl(scan_tc_kernel, dim3(grid), dim3(kTcScanThreads), smem, s, p.pdl != 0, map, p, sh.stages,
                     sh.flush, mode);
 }
 

@@ -23,16 +23,25 @@ constexpr int kTcUnitBytes = kTcUnit * kD * 2;     // 64 KB per ring stage
 constexpr int kTcHalfBytes = kTcUnitBytes / 2;     // [256 rows × 64 elements]: one swizzle span wide
 constexpr int kTcSubBytes = kTcM * 128;            // one sub-tile inside a half
 constexpr int kTcMaxStages = 3;
-constexpr int kTcAcc = 4;                          // unit accumulators in flight
+// TMEM is a deep score buffer: 32 units (8192 rows per SM, ~45 us of streaming) may be scored
+// before the epilogue drains them, so the TMA/MMA stream keeps going while the epilogue still
+// waits for the candidate thresholds (threshold_kernel overlaps the scan through PDL)
+#ifndef TKV_TC_ACC
+#define TKV_TC_ACC 32
+#endif
+constexpr int kTcAcc = TKV_TC_ACC;                 // unit accumulators in flight
 constexpr int kTcAccCols = kTcSub * kTcN;          // TMEM columns per unit
-constexpr uint32_t kTcTmemCols = 64;               // >= kTcAcc * kTcAccCols, power of two >= 32
-constexpr int kTcQSlots = kTcAcc;                  // q slots: reuse is safe once kTcAcc units drained
+constexpr uint32_t kTcTmemCols = kTcAcc * kTcAccCols <= 32 ? 32 : kTcAcc * kTcAccCols;  // power of two
+static_assert((kTcTmemCols & (kTcTmemCols - 1)) == 0 && kTcTmemCols <= 512, "TMEM columns");
+constexpr int kTcQSlots = 4;                       // q slots, each released by a tcgen05.commit
 constexpr int kTcQBytes = kTcN * kD * 2;           // 2 KB: one 8-row swizzle atom per half
-constexpr int kTcEpiWarps = 4;
-constexpr int kTcThreads = 64 + 32 * kTcEpiWarps;
+constexpr int kTcEpiWarps = 4;                     // epilogue warps per unit (one per TMEM lane quarter)
+constexpr int kTcThreads = 64 + 32 * kTcEpiWarps;  // one epilogue group (fused_tc_kernel)
+constexpr int kTcScanGroups = 2;                   // scan_tc_kernel: two groups alternate units
+constexpr int kTcScanThreads = 64 + 32 * kTcEpiWarps * kTcScanGroups;
 constexpr int kTcWarpRows = kTcUnit / 4;           // rows per unit one epilogue warp handles
 constexpr int kTcMaxFlush = 4;  // units between a warp's flushes (flat from 4 to 16; 4 leaves room beside the CTA)
-constexpr int kTcSmemLimit = 227 * 1024 - 512;     // opt-in maximum minus the static barriers
+constexpr int kTcSmemLimit = 227 * 1024 - 1024;    // opt-in maximum minus the static barriers (<= 1 KB)
 
 static_assert(kTcTmemCols >= kTcAcc * kTcAccCols, "TMEM allocation too small");
 
@@ -40,20 +49,24 @@ static_assert(kTcTmemCols >= kTcAcc * kTcAccCols, "TMEM allocation too small");
 struct TcShape {
   int stages, flush;
 };
-inline int tc_stage_bytes(int G, int flush) { return kTcEpiWarps * G * flush * kTcWarpRows * 8; }
-inline TcShape tc_shape(int G) {
+// staging: every epilogue warp (4 per group) holds flush units' worth of rows per head
+inline int tc_stage_bytes(int G, int flush, int groups = 1) { return groups * kTcEpiWarps * G * flush * kTcWarpRows * 8; }
+inline TcShape tc_shape(int G, int groups = 1) {
   // two stages and the rest of shared memory as staging: measured faster on cfg3 than three
   // stages with 3-unit flushes (fewer flush round trips beat a deeper ring)
   for (int st = 2; st >= 2; --st) {
     const int free_b = kTcSmemLimit - 1024 - kTcQSlots * kTcQBytes - st * kTcUnitBytes;
-    int f = free_b / tc_stage_bytes(G, 1);
-    if (f > kTcMaxFlush) f = kTcMaxFlush;
+    int f = free_b / tc_stage_bytes(G, 1, groups);
+    // own units between a warp's flushes: 4 with one group; 2 with two (the same rows per flush,
+    // and the staging stays small enough for the k-th / gather kernels to share the SM)
+    const int fmax = kTcMaxFlush / groups;
+    if (f > fmax) f = fmax;
     if (f >= 2 || st == 2) return {st, f};
   }
   return {2, 1};
 }
-inline size_t tc_smem_bytes(int G, const TcShape& sh) {
-  return 1024 + ((tc_stage_bytes(G, sh.flush) + 1023) & ~1023) + kTcQSlots * kTcQBytes +
+inline size_t tc_smem_bytes(int G, const TcShape& sh, int groups = 1) {
+  return 1024 + ((tc_stage_bytes(G, sh.flush, groups) + 1023) & ~1023) + kTcQSlots * kTcQBytes +
          static_cast<size_t>(sh.stages) * kTcUnitBytes;
 }
 
@@ -140,8 +153,9 @@ struct TcPipe {
   __device__ __forceinline__ uint32_t empty(int s) const { return bar0 + 8u * (kTcMaxStages + s); }
   __device__ __forceinline__ uint32_t tfull(int a) const { return bar0 + 8u * (2 * kTcMaxStages + a); }
   __device__ __forceinline__ uint32_t tempty(int a) const { return bar0 + 8u * (2 * kTcMaxStages + kTcAcc + a); }
+  __device__ __forceinline__ uint32_t qfree(int s) const { return bar0 + 8u * (2 * kTcMaxStages + 2 * kTcAcc + s); }
 };
-constexpr int kTcBarWords = 2 * kTcMaxStages + 2 * kTcAcc;
+constexpr int kTcBarWords = 2 * kTcMaxStages + 2 * kTcAcc + kTcQSlots;
 
 // Lays out the pipeline in `smem_raw` (dynamic shared memory) and, on the calling threads,
 // initialises it: thread `init_tid` the barriers, warp `alloc_warp` the TMEM accumulators. All
@@ -149,13 +163,13 @@ constexpr int kTcBarWords = 2 * kTcMaxStages + 2 * kTcAcc;
 // read the TMEM base with tc_tmem_base().
 __device__ __forceinline__ TcPipe tc_setup(uint8_t* smem_raw, uint64_t* s_bar, uint32_t* s_tmem, int G,
                                            int flush_every, int n_stages, const CUtensorMap* kmap,
-                                           bool init_thread, bool alloc_warp) {
+                                           bool init_thread, bool alloc_warp, int groups = 1) {
   TcPipe t;
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;  // 1024-byte alignment for the swizzle atoms
   uint8_t* gbase = smem_raw + (base - raw);
   t.cap = flush_every * kTcWarpRows;
-  const int stage_b = (kTcEpiWarps * G * t.cap * 8 + 1023) & ~1023;
+  const int stage_b = (groups * kTcEpiWarps * G * t.cap * 8 + 1023) & ~1023;
   t.s_buf = reinterpret_cast<uint64_t*>(gbase);
   t.sQ = base + stage_b;
   t.sA = t.sQ + kTcQSlots * kTcQBytes;
@@ -172,6 +186,7 @@ __device__ __forceinline__ TcPipe tc_setup(uint8_t* smem_raw, uint64_t* s_bar, u
       mbar_init(t.tfull(a), 1);
       mbar_init(t.tempty(a), kTcEpiWarps);
     }
+    for (int q = 0; q < kTcQSlots; ++q) mbar_init(t.qfree(q), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(kmap)) : "memory");
   }
@@ -208,14 +223,14 @@ __device__ __forceinline__ void tc_produce(const TcPipe& t, uint32_t i, const CU
   __syncwarp();
 }
 
-// MMA warp, step 1 of unit i: wait until accumulator i % kTcAcc is drained (all MMAs of units
-// <= i - kTcAcc are then complete, so a q slot last used kTcQSlots >= kTcAcc units back is free)
+// MMA warp, step 1 of unit i: wait until accumulator i % kTcAcc is drained by the epilogue
 __device__ __forceinline__ void tc_mma_acquire(const TcPipe& t, uint32_t i) {
   mbar_wait(t.tempty(static_cast<int>(i % kTcAcc)), ((i / kTcAcc) & 1u) ^ 1u);
 }
 
 // MMA warp: the GQA group's query rows → q slot (B operand, 8 rows, rows >= G zero), in the
-// 128-byte-swizzled K-major layout: chunk (h, j) of row n at h·1024 + n·128 + (j ^ n)·16
+// 128-byte-swizzled K-major layout: chunk (h, j) of row n at h·1024 + n·128 + (j ^ n)·16.
+// Prefer tc_next_q, which also manages the slot's release.
 __device__ __forceinline__ void tc_load_q(const TcPipe& t, int slot, const __nv_bfloat16* qg, int G, int lane) {
   uint8_t* qs = t.q_generic + slot * kTcQBytes;
   for (int e = lane; e < kTcN * 16; e += 32) {
@@ -226,6 +241,26 @@ __device__ __forceinline__ void tc_load_q(const TcPipe& t, int slot, const __nv_
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncwarp();
+}
+
+// The MMA warp's q-slot ring. Switching to a new segment releases the current slot with a
+// tcgen05.commit on qfree[slot] (it fires once every MMA that read the slot has completed);
+// a slot is rewritten only after its previous release fired.
+struct QRing {
+  int slot = -1;
+  uint32_t used = 0;    // bit s: slot s has been used before
+  uint32_t parity = 0;  // bit s: phase parity of slot s's next release
+};
+__device__ __forceinline__ void tc_next_q(const TcPipe& t, QRing& r, const __nv_bfloat16* qg, int G, int lane) {
+  if (r.slot >= 0 && lane == 0) umma_commit(t.qfree(r.slot));
+  r.slot = (r.slot + 1) % kTcQSlots;
+  const uint32_t bit = 1u << r.slot;
+  if (r.used & bit) {
+    mbar_wait(t.qfree(r.slot), (r.parity & bit) ? 1u : 0u);
+    r.parity ^= bit;
+  }
+  r.used |= bit;
+  tc_load_q(t, r.slot, qg, G, lane);
 }
 
 // MMA warp, step 2 of unit i: wait for the tile, one lane issues 2 sub-tiles × 8 K-steps, then

@@ -330,6 +330,7 @@ __global__ void __launch_bounds__(kKthThreads) kth_kernel(SelectParams p) {
   __shared__ int s_last;
 
   pdl_wait();  // candidates and histograms of the scan
+  if (threadIdx.x == 0) tl_start(p.tl, 5);
   const int bh = p.bh_begin + blockIdx.y, part = blockIdx.x, P = gridDim.x;
   const int b = bh / p.Hq, h = bh % p.Hq;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -491,6 +492,7 @@ __global__ void __launch_bounds__(kKthThreads) kth_kernel(SelectParams p) {
       p.hs.group_fail[b * p.Hkv + h / p.G] = 0u;
       *p.hs.fb_launched = 0u;
     }
+    tl_end(p.tl, 5);
   }
 }
 

@@ -1,0 +1,56 @@
+"""Cross-kernel timeline of one multi-kernel layer step (tkv_debug_timeline): when each kernel
+first started / last ended, relative to the sample kernel's start. Diagnostic only.
+
+    python tools/timeline.py --config cfg3 [--steps 20]
+"""
+import argparse
+import ctypes
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+NAMES = ["sample", "threshold", "threshold past wait", "scan", "scan epilogue past wait", "k-th", "gather"]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="cfg3")
+    ap.add_argument("--steps", type=int, default=20)
+    args = ap.parse_args()
+    import numpy as np
+    import torch
+
+    import bench
+    import paper_2502_06766_b200 as tkv
+    from paper_2502_06766_b200 import _lib
+
+    cfg = bench.CONFIGS[args.config]
+    dev = torch.device("cuda", 0)
+    q, K, V, n = bench.make_inputs(cfg, cfg["N"] + 8, 0, dev)
+    B, k = cfg["B"], cfg["k"]
+    nc = torch.full((B,), n, dtype=torch.int32, device=dev)
+    kw = dict(max_ctx=n)
+    lib = _lib.load()
+    acc = np.zeros((len(NAMES), 2))
+    for it in range(args.steps + 3):
+        buf = torch.zeros(16, dtype=torch.int64, device=dev)
+        buf[0::2] = -1  # UINT64_MAX
+        tkv.topk_decode_attention(q, K, V, nc, k, **kw)  # previous step in flight: realistic
+        lib.tkv_debug_timeline(ctypes.c_void_p(buf.data_ptr()))
+        tkv.topk_decode_attention(q, K, V, nc, k, **kw)
+        lib.tkv_debug_timeline(None)
+        torch.cuda.synchronize()
+        t = buf.cpu().numpy().view(np.uint64).astype(np.float64)
+        t0 = t[0]
+        if it >= 3:
+            for e in range(len(NAMES)):
+                s, en = t[2 * e], t[2 * e + 1]
+                acc[e, 0] += (s - t0) / 1e3 if s < 1.8e19 else np.nan
+                acc[e, 1] += (en - t0) / 1e3 if en > 0 else np.nan
+    acc /= args.steps
+    for e, nm in enumerate(NAMES):
+        print(f"  {nm:26s} start {acc[e, 0]:8.1f}  end {acc[e, 1]:8.1f} us")
+
+
+if __name__ == "__main__":
+    main()
