@@ -378,7 +378,24 @@ int run_emit(const tkv_problem* p, const void* q, const void* k_cache, const voi
   a.out = out;
   a.gather = gather;
   a.partial_only = 0;
-  TKV_LAUNCH(launch_attend_cand(a, st));
+  // Gather structure: one fused filter + gather pass over the candidates, or (many selected
+  // rows) a filter pass writing idx/scores followed by a streaming gather over those lists —
+  // measured faster from ~1M selected rows per step (cfg5 family), slower below (cfg1-3).
+  // TKV_LIST_GATHER=0/1 forces either.
+  static const int list_env = [] {
+    const char* e = getenv("TKV_LIST_GATHER");
+    return e ? atoi(e) : -1;
+  }();
+  const double sel_rows = static_cast<double>(bh_count) * p->k;
+  const bool list_gather = list_env >= 0 ? list_env != 0 : sel_rows >= 1.0e6;
+  if (gather && list_gather) {
+    a.gather = 0;  // filter only: idx / scores
+    TKV_LAUNCH(launch_attend_cand(a, st));
+    a.gather = 1;
+    TKV_LAUNCH(launch_attend_list(a, st));
+  } else {
+    TKV_LAUNCH(launch_attend_cand(a, st));
+  }
   if (p->flags & TKV_F_SORTED) {
     SortParams so{idx, scores, at<int32_t>(ws, L.mkb), p->k, bh_begin};
     TKV_LAUNCH(launch_sort(so, bh_count, st));

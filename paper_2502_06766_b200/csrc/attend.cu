@@ -210,6 +210,144 @@ __global__ void __launch_bounds__(NT, 4) attend_cand_kernel(AttendParams p) {
   if (threadIdx.x == 0) tl_end(p.tl, 6);
 }
 
+// List gather (after a filter pass wrote each head's kb selected rows to idx/scores): items
+// are (head, kListRows consecutive entries); every half-warp streams its rows — id and score
+// straight from global memory, 16-byte V loads, 8 rows in flight — with no compaction phase,
+// and each item ends with one reduction into its partial slot and the head ticket.
+constexpr int kListRows = 2048;
+__global__ void __launch_bounds__(NT, 4) attend_list_kernel(AttendParams p) {
+  __shared__ AttSmem sm;
+  extern __shared__ uint32_t s_pref[];  // [heads + 1] work-item prefix
+  if (threadIdx.x == 0) tl_start(p.tl, 6);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int half = lane >> 4, part = lane & 15, hw = warp * 2 + half;
+  const int BH = p.bh_count ? p.bh_count : p.B * p.Hq;
+  // rows per item: about 4 items per CTA over all heads (256 .. kListRows, multiple of 256)
+  const int per = (BH + NT - 1) / NT;
+  {
+    uint32_t rsum = 0;
+    for (int j = 0; j < per; ++j) {
+      const int lh = tid * per + j;
+      if (lh < BH) rsum += static_cast<uint32_t>(max(p.meta_kb[p.bh_begin + lh], 0));
+    }
+    rsum = warp_sum(rsum);
+    if (lane == 0) sm.wcnt[warp] = rsum;
+  }
+  __syncthreads();
+  uint32_t total_rows = 0;
+  for (int w = 0; w < NW; ++w) total_rows += sm.wcnt[w];
+  __syncthreads();
+  int R = static_cast<int>((total_rows + 4 * gridDim.x - 1) / (4 * gridDim.x));
+  R = (R + 255) / 256 * 256;
+  R = R < 256 ? 256 : (R > kListRows ? kListRows : R);
+  auto nslots_of = [&](int lh) -> int {
+    const int kb = p.meta_kb[p.bh_begin + lh];
+    return kb > 0 ? (kb + R - 1) / R : 1;
+  };
+  {
+    uint32_t sum = 0;
+    for (int j = 0; j < per; ++j) {
+      const int lh = tid * per + j;
+      sum += lh < BH ? nslots_of(lh) : 0;
+    }
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) sm.wcnt[warp] = incl;
+    __syncthreads();
+    uint32_t woff = 0;
+    for (int w = 0; w < warp; ++w) woff += sm.wcnt[w];
+    uint32_t run = woff + incl - sum;
+    for (int j = 0; j < per; ++j) {
+      const int lh = tid * per + j;
+      if (lh < BH) {
+        s_pref[lh] = run;
+        run += nslots_of(lh);
+      }
+    }
+    if (tid == NT - 1) s_pref[BH] = run;
+    __syncthreads();
+  }
+  const uint32_t total = s_pref[BH];
+  const float zs = p.scale * kLog2e;
+  for (uint32_t item = blockIdx.x; item < total; item += gridDim.x) {
+    int lo = 0, hi = BH;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (s_pref[mid] <= item) lo = mid; else hi = mid;
+    }
+    const int bh = p.bh_begin + lo;
+    const int slot = static_cast<int>(item - s_pref[lo]);
+    const int nslots = static_cast<int>(s_pref[lo + 1] - s_pref[lo]);
+    const int b = bh / p.Hq, kvh = (bh % p.Hq) / p.G;
+    const int kb = p.meta_kb[bh];
+    const float zref = kb > 0 ? p.meta_max[bh] * zs : 0.f;
+    const int r_lo = slot * R, r_hi = min(kb, r_lo + R);
+    const int32_t* ids = p.idx_out + static_cast<int64_t>(bh) * p.k;
+    const float* scs = p.scores_out + static_cast<int64_t>(bh) * p.k;
+    const __nv_bfloat16* vb =
+        p.vc + (static_cast<int64_t>(b) * p.Hkv + kvh) * p.cache_rows * kD + part * 8;
+    float acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+    float lw = 0.f;
+    constexpr int UNR = 8;
+    for (int r0 = r_lo + hw; r0 < r_hi; r0 += 2 * NW * UNR) {
+      int id[UNR];
+      float sc[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int r = r0 + 2 * NW * u;
+        id[u] = r < r_hi ? __ldcg(&ids[r]) : -1;
+        sc[u] = r < r_hi ? __ldcg(&scs[r]) : 0.f;
+      }
+      uint4 v[UNR];
+      float w[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const bool ok = id[u] >= 0;
+        w[u] = ok ? exp2f(fmaf(sc[u], zs, -zref)) : 0.f;
+        v[u] = ok ? ldg_stream(vb + (static_cast<int64_t>(id[u]) - p.row_offset) * kD) : make_uint4(0, 0, 0, 0);
+        if (part == 0) lw += w[u];
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        acc[0] = fmaf(w[u], bf16lo(v[u].x), acc[0]);
+        acc[1] = fmaf(w[u], bf16hi(v[u].x), acc[1]);
+        acc[2] = fmaf(w[u], bf16lo(v[u].y), acc[2]);
+        acc[3] = fmaf(w[u], bf16hi(v[u].y), acc[3]);
+        acc[4] = fmaf(w[u], bf16lo(v[u].z), acc[4]);
+        acc[5] = fmaf(w[u], bf16hi(v[u].z), acc[5]);
+        acc[6] = fmaf(w[u], bf16lo(v[u].w), acc[6]);
+        acc[7] = fmaf(w[u], bf16hi(v[u].w), acc[7]);
+      }
+    }
+    partial_write(p, bh, slot, sm, acc, lw);
+    ticket_finish(p, bh, nslots, sm);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) tl_end(p.tl, 6);
+}
+
+cudaError_t launch_attend_list(const AttendParams& p, cudaStream_t s) {
+  static int grid = 0;
+  if (!grid) {
+    cudaFuncSetAttribute(attend_list_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, attend_list_kernel, NT, 8192);
+    grid = sms * (per > 0 ? per : 1);
+  }
+  const size_t nbh = p.bh_count ? static_cast<size_t>(p.bh_count) : static_cast<size_t>(p.B) * p.Hq;
+  attend_list_kernel<<<grid, NT, (nbh + 1) * sizeof(uint32_t), s>>>(p);
+  return cudaGetLastError();
+}
+
 // Sharded finalize: partial_in holds the all-reduced (l, o[128]) per head.
 __global__ void __launch_bounds__(NT) finalize_kernel(AttendParams p) {
   __shared__ float s_z[128];

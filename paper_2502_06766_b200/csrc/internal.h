@@ -226,6 +226,7 @@ void scan_launch_shape(const ScanParams& p, int* grid, int* smem_bytes);
 cudaError_t launch_select(const SelectParams& p, cudaStream_t s);
 cudaError_t launch_kth(const SelectParams& p, cudaStream_t s);
 cudaError_t launch_attend_cand(const AttendParams& p, cudaStream_t s);
+cudaError_t launch_attend_list(const AttendParams& p, cudaStream_t s);
 cudaError_t launch_sort(const SortParams& p, int nbh, cudaStream_t s);
 cudaError_t launch_attend(const AttendParams& p, cudaStream_t s);
 cudaError_t launch_finalize(const AttendParams& p, cudaStream_t s);

@@ -41,8 +41,31 @@ void run(const uint4* V, const int* rows, int n, float* out, int per_sm) {
   const double bytes = double(n) * 256 * 10;
   printf("U=%2d ctas/sm=%d: %.1f us per gather of %d rows -> %.0f GB/s\n", U, per_sm, ms * 100, n, bytes / (ms * 1e-3) / 1e9);
 }
-int main() {
+int main(int argc, char** argv) {
   const int64_t nrows = (2LL << 30) / 256;  // 2 GiB of V rows
+  if (argc > 1) {  // row list from a file (int32, global row index into the 2 GiB buffer)
+    FILE* f = fopen(argv[1], "rb");
+    if (!f) { perror(argv[1]); return 1; }
+    std::vector<int> h;
+    int x;
+    while (fread(&x, 4, 1, f) == 1) h.push_back(x);
+    fclose(f);
+    const int n = static_cast<int>(h.size());
+    fprintf(stderr, "read %d rows\n", n);
+    for (int i = 0; i < n; ++i)
+      if (h[i] < 0 || h[i] >= nrows) { fprintf(stderr, "row %d out of range: %d\n", i, h[i]); return 1; }
+    uint4* V = nullptr;
+    if (cudaMalloc(&V, nrows * 256) != cudaSuccess) { fprintf(stderr, "cudaMalloc failed\n"); return 1; }
+    cudaMemset(V, 0, nrows * 256);
+    int* rows; cudaMalloc(&rows, n * 4); cudaMemcpy(rows, h.data(), n * 4, cudaMemcpyHostToDevice);
+    float* out; cudaMalloc(&out, 4);
+    printf("file rows (%d, in output order):\n", n);
+    run<8>(V, rows, n, out, 4); run<16>(V, rows, n, out, 8);
+    std::mt19937 g(2); std::shuffle(h.begin(), h.end(), g);
+    cudaMemcpy(rows, h.data(), n * 4, cudaMemcpyHostToDevice);
+    printf("same rows shuffled:\n"); run<8>(V, rows, n, out, 4);
+    return 0;
+  }
   uint4* V; cudaMalloc(&V, nrows * 256); cudaMemset(V, 0, nrows * 256);
   const int n = 32 * 16384;  // cfg3: 32 heads × k
   std::vector<int> h(n); std::mt19937 g(1);
