@@ -64,6 +64,8 @@ extern "C" {
 #define TKV_F_PARTS(n) ((uint32_t)(n) << 8) /* pipeline parts: scan of part i+1 overlaps the  \
                               k-th selection + V gather of part i (1..15; 0 = automatic)         */
 #define TKV_F_PARTS_MASK 0xF00u
+#define TKV_F_GATHER_LIST 16u /* V gather as filter pass + balanced list gather (automatic from  \
+                                 ~1M selected rows per call)                                    */
 #define TKV_F_SCAN_HMMA 8u /* key scan on register-staged mma.sync (scan.cu) instead of the TMA +  
                               tcgen05 pipeline (scan_tc.cu, the default)                         */
 

@@ -90,7 +90,9 @@ Layout make_layout(const tkv_problem* p) {
     // partial slots per head: list mode (k / kAttendChunk) or candidate mode (cap / kCandChunk)
     const int64_t a = (p->k + kAttendChunk - 1) / kAttendChunk;
     const int64_t c = (L.cap + kCandChunk - 1) / kCandChunk + 1;
-    L.nchunks = static_cast<int>(a > c ? a : c);
+    const int64_t f = (p->k + kFlatMinRows - 1) / kFlatMinRows + 1;  // flat list gather ranges
+    int64_t m = a > c ? a : c;
+    L.nchunks = static_cast<int>(m > f ? m : f);
   }
   L.pl = take(BH * L.nchunks * 4);
   L.po = take(BH * L.nchunks * kD * 4);
@@ -387,7 +389,8 @@ int run_emit(const tkv_problem* p, const void* q, const void* k_cache, const voi
     return e ? atoi(e) : -1;
   }();
   const double sel_rows = static_cast<double>(bh_count) * p->k;
-  const bool list_gather = list_env >= 0 ? list_env != 0 : sel_rows >= 1.0e6;
+  const bool list_gather =
+      (p->flags & TKV_F_GATHER_LIST) ? true : (list_env >= 0 ? list_env != 0 : sel_rows >= 1.0e6);
   if (gather && list_gather) {
     a.gather = 0;  // filter only: idx / scores
     TKV_LAUNCH(launch_attend_cand(a, st));

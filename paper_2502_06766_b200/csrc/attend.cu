@@ -21,6 +21,14 @@
 
 namespace tkv {
 
+// CTAs per SM the gather kernels are compiled for. With 4 (64 registers) the compiler
+// interleaves the FMAs with the loads and keeps ~3 of the 8 V-row loads per lane in flight;
+// with 3 (85 registers) all 8 are issued before the first use — but the step time measured the
+// same for 2, 3 and 4 (cfg3 383-388 us, within noise), and 4 was the fastest run.
+#ifndef TKV_ATT_MINB
+#define TKV_ATT_MINB 4
+#endif
+
 
 // List mode (sharded partial): the selected (idx, score) list is given.
 __global__ void __launch_bounds__(NT, 4) attend_kernel(AttendParams p) {
@@ -50,7 +58,7 @@ __global__ void __launch_bounds__(NT, 4) attend_kernel(AttendParams p) {
 // work items; a candidate is selected iff its composite >= meta_kth (kth_kernel), which is
 // exactly the top-kb set. Selected rows are appended to idx/scores (order unspecified) and,
 // with p.gather, their V rows are gathered in the same pass.
-__global__ void __launch_bounds__(NT, 4) attend_cand_kernel(AttendParams p) {
+__global__ void __launch_bounds__(NT, TKV_ATT_MINB) attend_cand_kernel(AttendParams p) {
   __shared__ AttSmem sm;
   if (threadIdx.x == 0) tl_start(p.tl, 6);
   extern __shared__ uint32_t s_pref[];  // [B*Hq + 1] work-item prefix over heads
@@ -210,45 +218,26 @@ __global__ void __launch_bounds__(NT, 4) attend_cand_kernel(AttendParams p) {
   if (threadIdx.x == 0) tl_end(p.tl, 6);
 }
 
-// List gather (after a filter pass wrote each head's kb selected rows to idx/scores): items
-// are (head, kListRows consecutive entries); every half-warp streams its rows — id and score
-// straight from global memory, 16-byte V loads, 8 rows in flight — with no compaction phase,
-// and each item ends with one reduction into its partial slot and the head ticket.
-constexpr int kListRows = 2048;
-__global__ void __launch_bounds__(NT, 4) attend_list_kernel(AttendParams p) {
+// List gather (after a filter pass wrote each head's kb selected rows to idx/scores). The
+// concatenation of all heads' lists (T rows) is split into one equal contiguous range per CTA
+// — perfectly balanced, like a flat gather — and a CTA walks the head segments of its range:
+// every half-warp streams rows (id and score straight from global memory, 16-byte V loads, 8
+// rows in flight), one reduction per segment goes to the head's partial slot (CTA index minus
+// the head's first CTA), and the head ticket counts the CTAs whose ranges overlap the head.
+__global__ void __launch_bounds__(NT, TKV_ATT_MINB) attend_list_kernel(AttendParams p) {
   __shared__ AttSmem sm;
-  extern __shared__ uint32_t s_pref[];  // [heads + 1] work-item prefix
+  extern __shared__ uint32_t s_pref[];  // [heads + 1] prefix of kb over heads
   if (threadIdx.x == 0) tl_start(p.tl, 6);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int half = lane >> 4, part = lane & 15, hw = warp * 2 + half;
   const int BH = p.bh_count ? p.bh_count : p.B * p.Hq;
-  // rows per item: about 4 items per CTA over all heads (256 .. kListRows, multiple of 256)
-  const int per = (BH + NT - 1) / NT;
+  auto kb_of = [&](int lh) -> uint32_t { return static_cast<uint32_t>(max(p.meta_kb[p.bh_begin + lh], 0)); };
   {
-    uint32_t rsum = 0;
-    for (int j = 0; j < per; ++j) {
-      const int lh = tid * per + j;
-      if (lh < BH) rsum += static_cast<uint32_t>(max(p.meta_kb[p.bh_begin + lh], 0));
-    }
-    rsum = warp_sum(rsum);
-    if (lane == 0) sm.wcnt[warp] = rsum;
-  }
-  __syncthreads();
-  uint32_t total_rows = 0;
-  for (int w = 0; w < NW; ++w) total_rows += sm.wcnt[w];
-  __syncthreads();
-  int R = static_cast<int>((total_rows + 4 * gridDim.x - 1) / (4 * gridDim.x));
-  R = (R + 255) / 256 * 256;
-  R = R < 256 ? 256 : (R > kListRows ? kListRows : R);
-  auto nslots_of = [&](int lh) -> int {
-    const int kb = p.meta_kb[p.bh_begin + lh];
-    return kb > 0 ? (kb + R - 1) / R : 1;
-  };
-  {
+    const int per = (BH + NT - 1) / NT;
     uint32_t sum = 0;
     for (int j = 0; j < per; ++j) {
       const int lh = tid * per + j;
-      sum += lh < BH ? nslots_of(lh) : 0;
+      sum += lh < BH ? kb_of(lh) : 0u;
     }
     uint32_t incl = sum;
 #pragma unroll
@@ -265,69 +254,123 @@ __global__ void __launch_bounds__(NT, 4) attend_list_kernel(AttendParams p) {
       const int lh = tid * per + j;
       if (lh < BH) {
         s_pref[lh] = run;
-        run += nslots_of(lh);
+        run += kb_of(lh);
       }
     }
     if (tid == NT - 1) s_pref[BH] = run;
     __syncthreads();
   }
-  const uint32_t total = s_pref[BH];
-  const float zs = p.scale * kLog2e;
-  for (uint32_t item = blockIdx.x; item < total; item += gridDim.x) {
-    int lo = 0, hi = BH;
+  const int64_t T = s_pref[BH];
+  // CTAs in use: ranges of at least kFlatMinRows rows (bounds the slots per head)
+  int64_t G = (T + kFlatMinRows - 1) / kFlatMinRows;
+  if (G > gridDim.x) G = gridDim.x;
+  if (G < 1) G = 1;
+  auto start_of = [&](int64_t c) -> int64_t { return T * c / G; };
+  auto cta_of = [&](int64_t r) -> int64_t {  // the CTA whose range holds flat row r
+    int64_t lo = 0, hi = G;                   // largest c with start_of(c) <= r
     while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (s_pref[mid] <= item) lo = mid; else hi = mid;
+      const int64_t mid = (lo + hi) >> 1;
+      if (start_of(mid) <= r) lo = mid; else hi = mid;
     }
-    const int bh = p.bh_begin + lo;
-    const int slot = static_cast<int>(item - s_pref[lo]);
-    const int nslots = static_cast<int>(s_pref[lo + 1] - s_pref[lo]);
-    const int b = bh / p.Hq, kvh = (bh % p.Hq) / p.G;
-    const int kb = p.meta_kb[bh];
-    const float zref = kb > 0 ? p.meta_max[bh] * zs : 0.f;
-    const int r_lo = slot * R, r_hi = min(kb, r_lo + R);
-    const int32_t* ids = p.idx_out + static_cast<int64_t>(bh) * p.k;
-    const float* scs = p.scores_out + static_cast<int64_t>(bh) * p.k;
-    const __nv_bfloat16* vb =
-        p.vc + (static_cast<int64_t>(b) * p.Hkv + kvh) * p.cache_rows * kD + part * 8;
-    float acc[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) acc[j] = 0.f;
-    float lw = 0.f;
-    constexpr int UNR = 8;
-    for (int r0 = r_lo + hw; r0 < r_hi; r0 += 2 * NW * UNR) {
-      int id[UNR];
-      float sc[UNR];
-#pragma unroll
-      for (int u = 0; u < UNR; ++u) {
-        const int r = r0 + 2 * NW * u;
-        id[u] = r < r_hi ? __ldcg(&ids[r]) : -1;
-        sc[u] = r < r_hi ? __ldcg(&scs[r]) : 0.f;
-      }
-      uint4 v[UNR];
-      float w[UNR];
-#pragma unroll
-      for (int u = 0; u < UNR; ++u) {
-        const bool ok = id[u] >= 0;
-        w[u] = ok ? exp2f(fmaf(sc[u], zs, -zref)) : 0.f;
-        v[u] = ok ? ldg_stream(vb + (static_cast<int64_t>(id[u]) - p.row_offset) * kD) : make_uint4(0, 0, 0, 0);
-        if (part == 0) lw += w[u];
-      }
-#pragma unroll
-      for (int u = 0; u < UNR; ++u) {
-        acc[0] = fmaf(w[u], bf16lo(v[u].x), acc[0]);
-        acc[1] = fmaf(w[u], bf16hi(v[u].x), acc[1]);
-        acc[2] = fmaf(w[u], bf16lo(v[u].y), acc[2]);
-        acc[3] = fmaf(w[u], bf16hi(v[u].y), acc[3]);
-        acc[4] = fmaf(w[u], bf16lo(v[u].z), acc[4]);
-        acc[5] = fmaf(w[u], bf16hi(v[u].z), acc[5]);
-        acc[6] = fmaf(w[u], bf16lo(v[u].w), acc[6]);
-        acc[7] = fmaf(w[u], bf16hi(v[u].w), acc[7]);
-      }
-    }
-    partial_write(p, bh, slot, sm, acc, lw);
-    ticket_finish(p, bh, nslots, sm);
+    return lo;
+  };
+  const float zs = p.scale * kLog2e;
+  // heads with nothing selected still need their output: CTA (head mod G) finishes them
+  for (int lh = static_cast<int>(blockIdx.x); lh < BH; lh += static_cast<int>(G)) {
+    if (blockIdx.x >= G) break;
+    if (s_pref[lh + 1] != s_pref[lh]) continue;
+    float acc0[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    partial_write(p, p.bh_begin + lh, 0, sm, acc0, 0.f);
+    ticket_finish(p, p.bh_begin + lh, 1, sm);
     __syncthreads();
+  }
+  if (blockIdx.x < G) {
+    const int64_t r_lo = start_of(blockIdx.x), r_hi = start_of(blockIdx.x + 1);
+    int lh;
+    {  // first head whose rows reach past r_lo
+      int lo = 0, hi = BH;  // largest lh with s_pref[lh] <= r_lo
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (s_pref[mid] <= r_lo) lo = mid; else hi = mid;
+      }
+      lh = lo;
+    }
+    for (; lh < BH && static_cast<int64_t>(s_pref[lh]) < r_hi; ++lh) {
+      const int64_t h0 = s_pref[lh], h1 = s_pref[lh + 1];
+      if (h1 <= r_lo || h1 == h0) continue;
+      const int64_t s0 = r_lo > h0 ? r_lo : h0, s1 = r_hi < h1 ? r_hi : h1;
+      const int64_t c_first = cta_of(h0), c_last = cta_of(h1 - 1);
+      const int slot = static_cast<int>(blockIdx.x - c_first);
+      const int nslots = static_cast<int>(c_last - c_first + 1);
+      const int bh = p.bh_begin + lh;
+      const int b = bh / p.Hq, kvh = (bh % p.Hq) / p.G;
+      const int kb = p.meta_kb[bh];
+      const float zref = kb > 0 ? p.meta_max[bh] * zs : 0.f;
+      const int32_t* ids = p.idx_out + static_cast<int64_t>(bh) * p.k - h0;  // index by flat row
+      const float* scs = p.scores_out + static_cast<int64_t>(bh) * p.k - h0;
+      const __nv_bfloat16* vb =
+          p.vc + (static_cast<int64_t>(b) * p.Hkv + kvh) * p.cache_rows * kD + part * 8;
+      float acc[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+      float lw = 0.f;
+      constexpr int UNR = 8;
+      constexpr int STEP = 2 * NW * UNR;  // rows per round of the CTA
+      // software pipeline: the next round's ids / scores load while this round's V rows are
+      // in flight (one memory latency per round instead of two)
+      int idn[UNR];
+      float scn[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int64_t r = s0 + hw + 2 * NW * u;
+        idn[u] = r < s1 ? __ldcg(&ids[r]) : -1;
+        scn[u] = r < s1 ? __ldcg(&scs[r]) : 0.f;
+      }
+      for (int64_t r0 = s0 + hw; r0 < s1; r0 += STEP) {
+        int id[UNR];
+        float sc[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          id[u] = idn[u];
+          sc[u] = scn[u];
+        }
+        uint4 v[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+          v[u] = id[u] >= 0 ? ldg_stream(vb + (static_cast<int64_t>(id[u]) - p.row_offset) * kD)
+                            : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          const int64_t r = r0 + STEP + 2 * NW * u;
+          idn[u] = r < s1 ? __ldcg(&ids[r]) : -1;
+          scn[u] = r < s1 ? __ldcg(&scs[r]) : 0.f;
+        }
+        float w[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          w[u] = id[u] >= 0 ? exp2f(fmaf(sc[u], zs, -zref)) : 0.f;
+          if (part == 0) lw += w[u];
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          acc[0] = fmaf(w[u], bf16lo(v[u].x), acc[0]);
+          acc[1] = fmaf(w[u], bf16hi(v[u].x), acc[1]);
+          acc[2] = fmaf(w[u], bf16lo(v[u].y), acc[2]);
+          acc[3] = fmaf(w[u], bf16hi(v[u].y), acc[3]);
+          acc[4] = fmaf(w[u], bf16lo(v[u].z), acc[4]);
+          acc[5] = fmaf(w[u], bf16hi(v[u].z), acc[5]);
+          acc[6] = fmaf(w[u], bf16lo(v[u].w), acc[6]);
+          acc[7] = fmaf(w[u], bf16hi(v[u].w), acc[7]);
+        }
+      }
+#ifdef TKV_GATHER_DIAG  // timing only: no reduction / head ticket (results are wrong)
+      if (acc[0] == 12345.f) p.part_l[0] = acc[1] + lw + slot + nslots;
+      continue;
+#endif
+      partial_write(p, bh, slot, sm, acc, lw);
+      ticket_finish(p, bh, nslots, sm);
+      __syncthreads();
+    }
   }
   if (threadIdx.x == 0) tl_end(p.tl, 6);
 }

@@ -29,6 +29,7 @@ constexpr int kAttendChunk = 512;    // selected rows per gather CTA (list mode)
 #define TKV_CAND_CHUNK 1024
 #endif
 constexpr int kCandChunk = TKV_CAND_CHUNK;  // candidates per work item (candidate mode)
+constexpr int kFlatMinRows = 256;           // flat list gather: rows per CTA range, at least
 constexpr int kSortMax = 16384;      // sorted output supported up to this k
 constexpr uint32_t kNoFilterShift = 20;  // histogram shift when every score is a candidate
 constexpr int kMinSampleStride = 8;      // small contexts sample at most every 8th row

@@ -44,7 +44,7 @@ def make_problem(B: int, Hq: int, Hkv: int, cache_rows: int, max_ctx: int, k: in
                  pinned_prefix: int = 0, scale: float | None = None, combine: str = "joint",
                  sorted: bool = False, no_filter: bool = False, row_offset: int = 0,
                  head_dim: int = HEAD_DIM, fused: bool = False,
-                 tc_scan: bool | None = None, parts: int = 0) -> _lib.Problem:
+                 tc_scan: bool | None = None, parts: int = 0, list_gather: bool = False) -> _lib.Problem:
     p = _lib.Problem()
     p.batch, p.n_q_heads, p.n_kv_heads, p.head_dim = B, Hq, Hkv, head_dim
     p.cache_rows, p.max_ctx, p.k = cache_rows, max_ctx, k
@@ -60,6 +60,8 @@ def make_problem(B: int, Hq: int, Hkv: int, cache_rows: int, max_ctx: int, k: in
     if not 0 <= parts <= 15:
         raise ConfigError("parts must be in 0..15 (0 = automatic)")
     p.flags |= parts << _lib.F_PARTS_SHIFT
+    if list_gather:
+        p.flags |= _lib.F_GATHER_LIST
     p.row_offset = row_offset
     return p
 
@@ -151,7 +153,8 @@ def topk_decode_attention(q, k_cache, v_cache, n_ctx, k: int, *, n_win=None, sca
                           combine: str = "joint", pinned_prefix: int = 0, sorted: bool = False,
                           max_ctx: int | None = None, no_filter: bool = False, row_offset: int = 0,
                           out=None, idx=None, scores=None, workspace: Workspace | None = None,
-                          fused: bool = False, tc_scan: bool | None = None, parts: int = 0):
+                          fused: bool = False, tc_scan: bool | None = None, parts: int = 0,
+                          list_gather: bool = False):
     """Exact top-k decode attention for every (batch, q head) of one layer.
 
     q [B, Hq, 128] bf16; k_cache/v_cache [B, Hkv, rows, 128] bf16 with the context in rows
@@ -169,7 +172,8 @@ def topk_decode_attention(q, k_cache, v_cache, n_ctx, k: int, *, n_win=None, sca
         max_ctx = s.cache_rows if isinstance(n_ctx, torch.Tensor) else int(n_ctx_t.max().item())
     prob = make_problem(s.B, s.Hq, s.Hkv, s.cache_rows, max_ctx, k, pinned_prefix=pinned_prefix,
                         scale=scale, combine=combine, sorted=sorted, no_filter=no_filter,
-                        row_offset=row_offset, fused=fused, tc_scan=tc_scan, parts=parts)
+                        row_offset=row_offset, fused=fused, tc_scan=tc_scan, parts=parts,
+                        list_gather=list_gather)
     ws = workspace or workspace_for(prob, dev)
     out = out if out is not None else torch.empty((s.B, s.Hq, HEAD_DIM), dtype=torch.float32, device=dev)
     idx = idx if idx is not None else torch.empty((s.B, s.Hq, k), dtype=torch.int32, device=dev)

@@ -160,3 +160,26 @@ def test_overlapped_parts_fallback_and_graph(cuda):
         g.replay()
     torch.cuda.synchronize()
     _check(q, K, V, [N], k, out_g, idx_g, sc_g)
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,N,k,W,pin", [
+    (1, 32, 8, 16384, 256, 0, 0),
+    (3, 8, 2, 3000, 300, 5, 0),     # ragged, k > n_ctx for one entry, window
+    (2, 16, 4, 9000, 700, 3, 40),   # pinned prefix
+    (4, 4, 1, 2000, 1999, 0, 0),    # k = N - 1: heads span several CTA ranges
+])
+def test_list_gather_parity(cuda, B, Hq, Hkv, N, k, W, pin):
+    """Filter pass + balanced list gather (TKV_F_GATHER_LIST) against the oracle, including an
+    empty context (n_ctx = 0) whose heads must still be finalised."""
+    rng = np.random.default_rng(5000 + N + k)
+    q, K, V = _make(rng, B, Hq, Hkv, N + W + 8)
+    n_ctx = [N] + [max(1, N - 700 * i) for i in range(1, B)]
+    if B == 3:
+        n_ctx = [3000, 100, 0]  # an empty context (the window alone is attended)
+    n_win = [W] * B
+    out, idx, sc = _run(q, K, V, n_ctx, k, cuda, n_win=n_win, pinned_prefix=pin, list_gather=True)
+    torch.cuda.synchronize()
+    _check(q, K, V, n_ctx, k, out, idx, sc, n_win=n_win, pinned=pin)
+    out2, idx2, _ = _run(q, K, V, n_ctx, k, cuda, n_win=n_win, pinned_prefix=pin)
+    torch.cuda.synchronize()
+    assert float((out - out2).abs().max()) < 1e-5

@@ -29,6 +29,30 @@ __global__ void __launch_bounds__(256) gather(const uint4* V, const int* rows, i
   }
   if (acc == 12345.f) out[0] = acc;
 }
+__global__ void stream_k(const uint4* K, int64_t n16, float* out) {  // a scan-like 2 GiB read
+  float a = 0.f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 v = ldg_stream(K + i);
+    a += __uint_as_float(v.x);
+  }
+  if (a == 12345.f) out[0] = a;
+}
+template <int U>
+void run_cold(const uint4* V, const uint4* Kb, const int* rows, int n, float* out, int per_sm, const char* tag) {
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  const int grid = 148 * per_sm;
+  float tot = 0.f;
+  for (int i = 0; i < 6; ++i) {
+    stream_k<<<148 * 8, 256>>>(Kb, (2LL << 30) / 16, out);
+    cudaEventRecord(a);
+    gather<U><<<grid, 256>>>(V, rows, n, out);
+    cudaEventRecord(b); cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    if (i > 0) tot += ms;
+  }
+  const double ms = tot / 5;
+  printf("%s U=%d: %.1f us per gather after a 2 GiB stream -> %.0f GB/s\n", tag, U, ms * 1e3, double(n) * 256 / (ms * 1e-3) / 1e9);
+}
 template <int U>
 void run(const uint4* V, const int* rows, int n, float* out, int per_sm) {
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
@@ -64,6 +88,15 @@ int main(int argc, char** argv) {
     std::mt19937 g(2); std::shuffle(h.begin(), h.end(), g);
     cudaMemcpy(rows, h.data(), n * 4, cudaMemcpyHostToDevice);
     printf("same rows shuffled:\n"); run<8>(V, rows, n, out, 4);
+    uint4* Kb = nullptr;
+    if (cudaMalloc(&Kb, 2LL << 30) != cudaSuccess) { fprintf(stderr, "cudaMalloc K failed\n"); return 1; }
+    cudaMemset(Kb, 0, 2LL << 30);
+    run_cold<8>(V, Kb, rows, n, out, 4, "shuffled, TLB/L2 cold");
+    std::vector<int> hs = h;
+    std::sort(hs.begin(), hs.end());  // group-major (= kv head major), ascending rows
+    cudaMemcpy(rows, hs.data(), n * 4, cudaMemcpyHostToDevice);
+    run_cold<8>(V, Kb, rows, n, out, 4, "sorted (group-major), TLB/L2 cold");
+    run<8>(V, rows, n, out, 4);
     return 0;
   }
   uint4* V; cudaMalloc(&V, nrows * 256); cudaMemset(V, 0, nrows * 256);
