@@ -172,6 +172,13 @@ __global__ void __launch_bounds__(kScanWarps * 32, 2) scan_kernel(ScanParams p) 
 }
 
 cudaError_t launch_sample(const SampleParams& p, cudaStream_t s) {
+  static bool carve = false;
+  if (!carve) {  // same carveout as the scan: the scan's CTAs start beside these (PDL)
+    cudaFuncSetAttribute(sample_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(threshold_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    carve = true;
+  }
   if (!p.no_filter) {
     dim3 grid(kSamples / kSampleThreads, p.B * p.Hkv);
     sample_kernel<<<grid, kSampleThreads, 0, s>>>(p);

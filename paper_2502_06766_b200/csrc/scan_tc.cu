@@ -218,7 +218,11 @@ cudaError_t launch_scan_tc(const ScanParams& p, cudaStream_t s) {
     if (sh.flush > kTcMaxFlush) sh.flush = kTcMaxFlush;
     if (sh.flush < 1) return cudaErrorInvalidValue;
   }
-  if (flush_env > 0 && flush_env < sh.flush) sh.flush = flush_env;
+  if (flush_env > 0) {  // experiments: set the units between a warp's flushes (bounded by smem)
+    const int free_b = kTcSmemLimit - 1024 - kTcQSlots * kTcQBytes - sh.stages * kTcUnitBytes;
+    const int fit = free_b / tc_stage_bytes(p.G, 1, kTcScanGroups);
+    sh.flush = flush_env < fit ? flush_env : fit;
+  }
   const size_t smem = tc_smem_bytes(p.G, sh, kTcScanGroups);
   static bool attr_set = false;
   if (!attr_set) {
