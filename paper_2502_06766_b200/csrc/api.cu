@@ -48,7 +48,8 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 struct Layout {
   size_t ticket_g, ticket_k, flag, gflag, fctl, fbl, ctrl_end;
   size_t maxc, bktc, bkt, outc;
-  size_t cnt, thr, hshift, hist, mmax, mkth, mkb, samp, cand, sidx, sscore, pl, po, total;
+  size_t cnt, thr, hshift, hist, mmax, mkth, mkb, samp, cand, sidx, sscore, pl, po, pinm, total;
+  int pin_words;
   int64_t cap;
   int nchunks;
 };
@@ -94,6 +95,11 @@ Layout make_layout(const tkv_problem* p) {
     int64_t m = a > c ? a : c;
     L.nchunks = static_cast<int>(m > f ? m : f);
   }
+  {
+    const int64_t pin = p->pinned_prefix < p->max_ctx ? p->pinned_prefix : p->max_ctx;
+    L.pin_words = pin > 0 ? static_cast<int>((pin + 31) / 32) : 0;
+  }
+  L.pinm = take(BH * static_cast<size_t>(L.pin_words) * 4);
   L.pl = take(BH * L.nchunks * 4);
   L.po = take(BH * L.nchunks * kD * 4);
   L.total = off;
@@ -190,6 +196,8 @@ int run_prefix(const tkv_problem* p, const void* q, const void* k_cache, const i
   sp.samp = at<uint32_t>(ws, L.samp);
   sp.hs = hs;
   sp.tl = g_tl;
+  sp.pin_words = L.pin_words;
+  sp.pin_mask = L.pin_words ? at<uint32_t>(ws, L.pinm) : nullptr;
   TKV_LAUNCH(launch_sample(sp, st));
   if (!sp.no_filter) ++g_launches;  // sample + threshold kernels
 
@@ -362,6 +370,8 @@ AttendParams make_attend(const tkv_problem* p, const void* q, const void* k_cach
   a.cand_cnt = at<uint32_t>(ws, L.cnt);
   a.out_cnt = at<uint32_t>(ws, L.outc);
   a.tl = g_tl;
+  a.pin_words = L.pin_words;
+  a.pin_mask = L.pin_words ? at<uint32_t>(ws, L.pinm) : nullptr;
   return a;
 }
 
@@ -715,6 +725,11 @@ int tkv_shard_partial(const tkv_problem* p, const void* q, const void* k_cache, 
   AttendParams a = make_attend(p, q, k_cache, v_cache, n_ctx, nullptr, idx, scores, ws, L);
   a.partial_only = 1;
   a.partial_out = partial;
+  if (a.pin_mask) {  // the list pass marks the selected pinned rows; start from none
+    const cudaError_t e = cudaMemsetAsync(a.pin_mask, 0, static_cast<size_t>(p->batch) * p->n_q_heads * L.pin_words * 4,
+                                          static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return fail(TKV_ECUDA, "cudaMemsetAsync: %s", cudaGetErrorString(e));
+  }
   TKV_LAUNCH(launch_attend(a, static_cast<cudaStream_t>(stream)));
   return TKV_OK;
 }

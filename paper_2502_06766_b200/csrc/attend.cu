@@ -47,6 +47,7 @@ __global__ void __launch_bounds__(NT, 4) attend_kernel(AttendParams p) {
     const float s = p.scores[static_cast<int64_t>(bh) * p.k + lo + i];
     const int64_t local = gid - p.row_offset;
     const bool owned = local >= 0 && local < nctx;
+    if (owned) mark_pinned(p, bh, local);
     sm.row[i] = owned ? static_cast<int32_t>(local) : -1;
     sm.w[i] = owned ? exp2f(fmaf(s, zs, -zref)) : 0.f;
   }
@@ -184,7 +185,9 @@ __global__ void __launch_bounds__(NT, TKV_ATT_MINB) attend_cand_kernel(AttendPar
       for (int u = 0; u < PER; ++u) {
         if (sel[u]) {
           const uint64_t c = cv[u];
-          sm.row[pos] = static_cast<int32_t>(static_cast<int64_t>(comp_gid(c)) - p.row_offset);
+          const int64_t local = static_cast<int64_t>(comp_gid(c)) - p.row_offset;
+          mark_pinned(p, bh, local);
+          sm.row[pos] = static_cast<int32_t>(local);
           sm.w[pos] = exp2f(fmaf(key_score(comp_key(c)), zs, -zref));
           ++pos;
         }

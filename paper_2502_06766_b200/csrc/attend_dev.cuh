@@ -14,13 +14,13 @@ constexpr int NW = NT / 32;
 
 // Online softmax accumulation over local rows [r_begin, r_end) of kv head (b, kvh) for q head
 // h. State (m, l, o) in the log2-scaled domain; thread t holds o for d = t % 128 (the two
-// halves t / 128 are summed by the caller). With `pinned`, a row is skipped when it is among
-// the selected top-k (composite >= kth). Per 128-row block: the rows are scored with the scan's
+// halves t / 128 are summed by the caller). With `skip` (a bitmask over local rows), a row
+// whose bit is set — it is among the selected top-k — is skipped. Per 128-row block: the rows are scored with the scan's
 // HMMA tile (bit-identical scores), weighted once per row, and their V rows gathered 16 bytes
 // per lane with 8 rows in flight per half-warp; s_red: NW × 128 floats.
 template <class Gp = CtaGrp>
 __device__ void accumulate_rows(const AttendParams& p, int b, int h, int kvh, int64_t r_begin,
-                                int64_t r_end, bool pinned, uint64_t kth, float& m, float& l,
+                                int64_t r_end, const uint32_t* skip, float& m, float& l,
                                 float& o, float* s_z, float* s_scr, float* s_red) {
   const int tid = Gp::tid(), lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, c = lane & 3;
@@ -46,9 +46,9 @@ __device__ void accumulate_rows(const AttendParams& p, int b, int h, int kvh, in
       if (c == (n >> 1)) {
         const float sA = sc[n & 1], sB = sc[2 + (n & 1)];
         bool okA = rA < r_end, okB = rB < r_end;
-        if (pinned) {
-          okA = okA && make_comp(score_key(sA), static_cast<uint32_t>(p.row_offset + rA)) < kth;
-          okB = okB && make_comp(score_key(sB), static_cast<uint32_t>(p.row_offset + rB)) < kth;
+        if (skip) {
+          okA = okA && !((__ldcg(&skip[rA >> 5]) >> (rA & 31)) & 1u);
+          okB = okB && !((__ldcg(&skip[rB >> 5]) >> (rB & 31)) & 1u);
         }
         s_z[warp * 16 + g] = okA ? sA * zs : -INFINITY;
         s_z[warp * 16 + g + 8] = okB ? sB * zs : -INFINITY;
@@ -135,7 +135,9 @@ __device__ void add_pinned(const AttendParams& p, int b, int h, int kvh, int64_t
   if (hi <= lo) return;
   const int bh = b * p.Hq + h;
   float m = zref;
-  accumulate_rows<Gp>(p, b, h, kvh, lo, hi, true, __ldcg(&p.meta_kth[bh]), m, l, o, s_z, s_scr, s_red);
+  // rows the top-k selected are marked in pin_mask by the gather / filter pass
+  accumulate_rows<Gp>(p, b, h, kvh, lo, hi, p.pin_mask + static_cast<int64_t>(bh) * p.pin_words, m, l, o, s_z,
+                      s_scr, s_red);
   // every unselected row scores <= the k-th selected score <= M, so m stays zref
 }
 
@@ -152,7 +154,7 @@ __device__ void finalize_head(const AttendParams& p, int b, int h, int kvh, int6
   if (nwin > p.cache_rows - nctx) nwin = p.cache_rows - nctx;
   float m_w = -INFINITY, l_w = 0.f, o_w = 0.f;
   if (nwin > 0)
-    accumulate_rows<Gp>(p, b, h, kvh, nctx, nctx + nwin, false, 0ull, m_w, l_w, o_w, s_z, s_scr, s_red);
+    accumulate_rows<Gp>(p, b, h, kvh, nctx, nctx + nwin, nullptr, m_w, l_w, o_w, s_z, s_scr, s_red);
   float val;
   if (p.combine == 0) {  // joint (attention.py:109-114)
     const float mm = fmaxf(l_c > 0.f ? zref : -INFINITY, m_w);
@@ -166,6 +168,13 @@ __device__ void finalize_head(const AttendParams& p, int b, int h, int kvh, int6
   s_o[tid] = val;
   Gp::sync();
   if (tid < kD) p.out[static_cast<int64_t>(bh) * kD + tid] = s_o[tid] + s_o[tid + kD];
+}
+
+// a selected row inside the pinned prefix: mark it so the pinned pass does not add it again
+__device__ __forceinline__ void mark_pinned(const AttendParams& p, int bh, int64_t local) {
+  if (p.pin_mask && local >= 0 && local < static_cast<int64_t>(p.pin_words) * 32 &&
+      local < static_cast<int64_t>(p.pinned) - p.row_offset)
+    atomicOr(&p.pin_mask[static_cast<int64_t>(bh) * p.pin_words + (local >> 5)], 1u << (local & 31));
 }
 
 struct AttSmem {

@@ -264,6 +264,7 @@ __device__ void do_thresh(const FusedParams& p, const Ctl& ctl, int bh, unsigned
   }
   uint4* gh = reinterpret_cast<uint4*>(p.hs.hist + static_cast<int64_t>(bh) * kHistBins);
   for (int i = tid; i < kHistBins / 4; i += FT) gh[i] = make_uint4(0, 0, 0, 0);
+  for (int i = tid; i < a.pin_words; i += FT) a.pin_mask[static_cast<int64_t>(bh) * a.pin_words + i] = 0u;
   if (tid == 0) {
     p.hs.thr[bh] = thr;
     p.hs.hshift[bh] = shift;
@@ -628,6 +629,7 @@ __device__ void do_att(const FusedParams& p, const Ctl& ctl, int bh, int ai, boo
           sc_o[o] = s;
           if (a.packed_out) a.packed_out[static_cast<int64_t>(bh) * a.k + o] = c;
         }
+        mark_pinned(a, bh, static_cast<int64_t>(gid) - a.row_offset);
         sm.row[pos] = static_cast<int32_t>(static_cast<int64_t>(gid) - a.row_offset);
         sm.w[pos] = exp2f(fmaf(s, zs, -zref));
         ++pos;

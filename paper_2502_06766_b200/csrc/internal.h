@@ -68,6 +68,8 @@ struct SampleParams {
   int no_filter;
   uint32_t* samp;  // [B*Hq*kSamples]
   HeadState hs;
+  uint32_t* pin_mask;  // [B*Hq][pin_words] selected pinned-prefix rows (zeroed by threshold_kernel)
+  int pin_words;
 };
 
 struct ScanParams {
@@ -160,6 +162,10 @@ struct AttendParams {
   float* scores_out;
   uint64_t* packed_out;
   int gather;  // 0: only write the selected rows (no attention)
+  // selected rows inside the pinned prefix, one bit per local row, set by the gather / filter
+  // pass; the pinned pass skips them (membership by id, not by a recomputed score)
+  uint32_t* pin_mask;  // [B*Hq][pin_words] or nullptr
+  int pin_words;
   int bh_begin, bh_count;  // heads handled by attend_cand_kernel; bh_count 0 = all B*Hq
 };
 

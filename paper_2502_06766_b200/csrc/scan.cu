@@ -151,6 +151,7 @@ __global__ void __launch_bounds__(kThrThreads) threshold_kernel(SampleParams p) 
   }
   uint32_t* gh = p.hs.hist + static_cast<int64_t>(bh) * kHistBins;
   for (int i = tid; i < kHistBins; i += NT) gh[i] = 0u;
+  for (int i = tid; i < p.pin_words; i += NT) p.pin_mask[static_cast<int64_t>(bh) * p.pin_words + i] = 0u;
   if (tid == 0) {
     p.hs.thr[bh] = thr;
     p.hs.hshift[bh] = shift;
