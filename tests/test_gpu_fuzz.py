@@ -30,15 +30,56 @@ def _config(seed: int):
         list_gather=bool(r.random() < 0.3),
         tc_scan=bool(r.random() < 0.8),
         no_filter=bool(r.random() < 0.15),
+        fused=bool(r.random() < 0.25),
     )
+    if opts["fused"]:  # the fused kernels run the whole layer: no parts / list options
+        opts["parts"] = 0
+        opts["list_gather"] = False
     return B, G * Hkv, Hkv, N, k, W, pin, combine, n_ctx, opts
 
 
-@pytest.mark.parametrize("seed", range(30))
+@pytest.mark.parametrize("seed", range(120))
 def test_fuzz_against_oracle(cuda, seed):
     B, Hq, Hkv, N, k, W, pin, combine, n_ctx, opts = _config(seed)
     rng = np.random.default_rng(10_000 + seed)
     q, K, V = _make(rng, B, Hq, Hkv, N + W + 4)
+    n_win = [W] * B
+    out, idx, sc = _run(q, K, V, n_ctx, k, cuda, n_win=n_win, pinned_prefix=pin, combine=combine, **opts)
+    torch.cuda.synchronize()
+    _check(q, K, V, n_ctx, k, out, idx, sc, n_win=n_win, combine=combine, pinned=pin)
+
+
+def _adversarial(seed, q, K):
+    """Distributions that stress the sampled threshold, the tie rule and the fallback."""
+    from oracle import oracle as O
+
+    r = np.random.default_rng(77 + seed)
+    kind = seed % 5
+    B, Hkv, rows, _ = K.shape
+    if kind == 0:  # many exact duplicates of a few rows (ties across the k-th boundary)
+        src = r.integers(0, rows, size=8)
+        for b in range(B):
+            for h in range(Hkv):
+                K[b, h, r.integers(0, rows, size=rows // 3)] = K[b, h, r.choice(src)]
+    elif kind == 1:  # constant keys: every score equal
+        K[:] = K[:, :, :1]
+    elif kind == 2:  # sampled rows far above the rest: the sampled threshold admits < k rows
+        K[:] = O.to_bf16_f32(K * 0.01)
+        stride = max(8, -(-rows // 4096))
+        K[:, :, ::stride] = O.to_bf16_f32(K[:, :, ::stride] + 2.0 * np.sign(q[:, :1, None, :]))
+    elif kind == 3:  # large magnitudes
+        K[:] = O.to_bf16_f32(K * 64.0)
+    else:  # tiny magnitudes (scores near zero, -0.0 / +0.0 keys)
+        K[:] = O.to_bf16_f32(K * 1e-3)
+    return K
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_fuzz_adversarial(cuda, seed):
+    B, Hq, Hkv, N, k, W, pin, combine, n_ctx, opts = _config(500 + seed)
+    rng = np.random.default_rng(20_000 + seed)
+    q, K, V = _make(rng, B, Hq, Hkv, N + W + 4)
+    K = _adversarial(seed, q, K)
     n_win = [W] * B
     out, idx, sc = _run(q, K, V, n_ctx, k, cuda, n_win=n_win, pinned_prefix=pin, combine=combine, **opts)
     torch.cuda.synchronize()
