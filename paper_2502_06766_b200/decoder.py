@@ -23,7 +23,7 @@ class TopkDecoder:
     def __init__(self, k_cache: torch.Tensor, v_cache: torch.Tensor, n_ctx, k: int, *,
                  n_win=0, scale: float | None = None, combine: str = "joint",
                  pinned_prefix: int = 0, sorted: bool = False, max_ctx: int | None = None,
-                 fused: bool = False, use_graph: bool = True):
+                 fused: bool = False, use_graph: bool = True, parts: int = 0, list_gather: bool = False):
         if k < 1:
             raise InputError("k must be >= 1")
         ops._check_cuda_bf16("k_cache", k_cache, 4)
@@ -38,7 +38,7 @@ class TopkDecoder:
         self.max_ctx = int(max_ctx if max_ctx is not None else self.rows)
         self.k = k
         self.kw = dict(scale=scale, combine=combine, pinned_prefix=pinned_prefix, sorted=sorted,
-                       max_ctx=self.max_ctx, fused=fused)
+                       max_ctx=self.max_ctx, fused=fused, parts=parts, list_gather=list_gather)
         ops.combine_code(combine)
         self.use_graph = use_graph
         self.Hq = None
@@ -56,7 +56,8 @@ class TopkDecoder:
         prob = ops.make_problem(self.B, Hq, self.Hkv, self.rows, self.max_ctx, self.k,
                                 pinned_prefix=self.kw["pinned_prefix"], scale=self.kw["scale"],
                                 combine=self.kw["combine"], sorted=self.kw["sorted"],
-                                fused=self.kw["fused"])
+                                fused=self.kw["fused"], parts=self.kw["parts"],
+                                list_gather=self.kw["list_gather"])
         self.ws = ops.Workspace(prob, dev)
         D = ops.HEAD_DIM
         bf, f32, i32 = torch.bfloat16, torch.float32, torch.int32

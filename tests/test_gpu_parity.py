@@ -317,8 +317,10 @@ def test_fused_repeated_calls_reset_state(cuda):
         _check(qq, K, V, [50000 - rep], 777, out, idx, sc)
 
 
-@pytest.mark.parametrize("use_graph", [True, False])
-def test_decoder_host_io_steps(cuda, use_graph):
+@pytest.mark.parametrize("use_graph,variant", [(True, {}), (False, {}), (True, {"fused": True}),
+                                               (True, {"parts": 2}), (True, {"list_gather": True}),
+                                               (True, {"pinned_prefix": 30})])
+def test_decoder_host_io_steps(cuda, use_graph, variant):
     """TopkDecoder.step with host tensors (the end-to-end path, CUDA-graph replayed): each step
     appends the token's k/v to the window and attends; equals the oracle on the grown cache."""
     from paper_2502_06766_b200 import TopkDecoder
@@ -327,7 +329,7 @@ def test_decoder_host_io_steps(cuda, use_graph):
     B, Hq, Hkv, N, k, steps = 2, 8, 2, 6000, 64, 4
     q0, K, V = _make(rng, B, Hq, Hkv, N + 16)
     Kd, Vd = _dev(K, cuda), _dev(V, cuda)
-    dec = TopkDecoder(Kd, Vd, N, k, max_ctx=N, use_graph=use_graph)
+    dec = TopkDecoder(Kd, Vd, N, k, max_ctx=N, use_graph=use_graph, **variant)
     Kref, Vref = K.copy(), V.copy()
     for s in range(steps):
         q = bf16_normal(rng, (B, Hq, 128))
@@ -339,4 +341,5 @@ def test_decoder_host_io_steps(cuda, use_graph):
         Vref[:, :, N + s] = vn
         _check(q, Kref, Vref, [N] * B, k, out, idx, torch.zeros(B, Hq, k) + torch.from_numpy(
             np.stack([[O.ip_scores_all(Kref[b, h // 4, :N], q[b, h])[idx.numpy()[b, h]] for h in range(Hq)]
-                      for b in range(B)]).astype(np.float32)), n_win=[s + 1] * B)
+                      for b in range(B)]).astype(np.float32)), n_win=[s + 1] * B,
+               pinned=variant.get("pinned_prefix", 0))
