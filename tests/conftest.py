@@ -15,6 +15,17 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long-running")
 
 
+def pytest_collection_modifyitems(config, items):
+    """A GPU test that hangs (e.g. a device-side wait that never ends) is ended after 300 s by
+    pytest-timeout's thread method — it works even when the main thread is blocked inside a
+    CUDA call — instead of stalling the whole run."""
+    if not config.pluginmanager.hasplugin("timeout"):
+        return
+    for item in items:
+        if item.get_closest_marker("gpu") and not item.get_closest_marker("timeout"):
+            item.add_marker(pytest.mark.timeout(300, method="thread"))
+
+
 @pytest.fixture(scope="session")
 def cuda():
     import torch
