@@ -115,10 +115,11 @@ class TopkDecoder:
         if with_kv:
             ops.kv_append(self.k_cache, self.v_cache, b["k_new"], b["v_new"], self.n_win,
                           base=self.n_ctx, advance=True)
+        # the head-finishing CTAs write the output straight into the pinned host buffer (mapped
+        # memory, 512 B per head): no device->host copy node on the step's critical path
         ops.topk_decode_attention(b["q"], self.k_cache, self.v_cache, self.n_ctx, self.k,
-                                  n_win=self.n_win, out=b["out"], idx=b["idx"], scores=b["scores"],
+                                  n_win=self.n_win, out=b["out_h"], idx=b["idx"], scores=b["scores"],
                                   workspace=self.ws, **self.kw)
-        b["out_h"].copy_(b["out"], non_blocking=True)
         if with_idx:
             b["idx_h"].copy_(b["idx"], non_blocking=True)
 
