@@ -318,8 +318,10 @@ int pipeline_parts(const tkv_problem* p, bool tc) {
 
 // per-thread, per-device side stream and fork/join events of the overlapped pipeline
 struct PipeRes {
-  cudaStream_t side = nullptr;
+  cudaStream_t side = nullptr;   // k-th of each part
+  cudaStream_t side2 = nullptr;  // gather of each part (after its k-th; beside the next k-th)
   cudaEvent_t ev[kMaxParts + 1] = {};
+  cudaEvent_t evk[kMaxParts] = {};
 };
 thread_local PipeRes g_pipe[16];
 
@@ -330,7 +332,9 @@ int pipe_res(PipeRes** out) {
   PipeRes& r = g_pipe[dev];
   if (!r.side) {
     cudaError_t e = cudaStreamCreateWithFlags(&r.side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&r.side2, cudaStreamNonBlocking);
     for (int i = 0; e == cudaSuccess && i <= kMaxParts; ++i) e = cudaEventCreateWithFlags(&r.ev[i], cudaEventDisableTiming);
+    for (int i = 0; e == cudaSuccess && i < kMaxParts; ++i) e = cudaEventCreateWithFlags(&r.evk[i], cudaEventDisableTiming);
     if (e != cudaSuccess) return fail(TKV_ECUDA, "side stream / events: %s", cudaGetErrorString(e));
   }
   *out = &r;
@@ -458,16 +462,41 @@ int run_layer(const tkv_problem* p, const void* q, const void* k_cache, const vo
       }
       return TKV_OK;
     }
+    // part boundaries: even, or (TKV_PARTS_TAIL=1) a last part of one eighth of the groups so
+    // less k-th + gather work remains after the final scan
+    static const bool tail_split = [] {
+      const char* e = getenv("TKV_PARTS_TAIL");
+      return e && atoi(e) != 0;
+    }();
+    auto bound = [&](int part) -> int64_t {
+      if (!tail_split || P < 2) return nseg * part / P;
+      int64_t last = nseg / 8;
+      if (last < 1) last = 1;
+      if (part >= P) return nseg;
+      return (nseg - last) * part / (P - 1);
+    };
     if (prof) cudaEventRecord(g_scan_start, st);
+    static const bool chain = [] {  // experiments: PDL-chained part scans
+      const char* e = getenv("TKV_PARTS_CHAIN");
+      return !(e && atoi(e) == 0);
+    }();
     for (int part = 0; part < P; ++part) {
-      const int64_t s0 = nseg * part / P, s1 = nseg * (part + 1) / P;
-      TRY(run_scan_part(p, cp, s0, s1, st, false));
+      const int64_t s0 = bound(part), s1 = bound(part + 1);
+      // the first part's scan overlaps sample / threshold (PDL); later parts' CTAs take over SMs
+      // as the previous part's retire (its epilogue waits for that grid; TMEM buffers the gap)
+      TRY(run_scan_part(p, cp, s0, s1, st, pdl_enabled() && !prof && (part == 0 || chain)));
       if (cudaEventRecord(r->ev[part], st) != cudaSuccess || cudaStreamWaitEvent(r->side, r->ev[part], 0) != cudaSuccess)
         return fail(TKV_ECUDA, "pipeline fork failed");
       TRY(run_kth_part(p, cp, sl, s0, s1, part, r->side, false));
-      TRY(run_emit(p, q, k_cache, v_cache, n_ctx, n_win, idx, scores, packed, out, gather, ws, L, r->side,
+      // the gather of this part on its own stream, so the next part's k-th need not wait for it
+      if (cudaEventRecord(r->evk[part], r->side) != cudaSuccess ||
+          cudaStreamWaitEvent(r->side2, r->evk[part], 0) != cudaSuccess)
+        return fail(TKV_ECUDA, "pipeline fork failed");
+      TRY(run_emit(p, q, k_cache, v_cache, n_ctx, n_win, idx, scores, packed, out, gather, ws, L, r->side2,
                    static_cast<int>(s0 * G), static_cast<int>((s1 - s0) * G)));
     }
+    if (cudaEventRecord(r->evk[0], r->side2) != cudaSuccess || cudaStreamWaitEvent(r->side, r->evk[0], 0) != cudaSuccess)
+      return fail(TKV_ECUDA, "pipeline join failed");
     if (prof) cudaEventRecord(g_scan_stop, st);
     if (cudaEventRecord(r->ev[P], r->side) != cudaSuccess || cudaStreamWaitEvent(st, r->ev[P], 0) != cudaSuccess)
       return fail(TKV_ECUDA, "pipeline join failed");

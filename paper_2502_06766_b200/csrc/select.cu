@@ -320,7 +320,10 @@ __global__ void __launch_bounds__(kScanWarps * 32, 2) fb_scan_kernel(ScanParams 
 //   slice of the candidates for the maximum and for the members of d* (appended to a small
 //   per-head buffer); the last CTA of the head refines inside that buffer (shared memory,
 //   8-bit radix over the 64-bit composites → exact lower-id tie resolution).
-__global__ void __launch_bounds__(kKthThreads) kth_kernel(SelectParams p) {
+// <= 32 registers (4 CTAs per SM): a kth CTA's 16 warps then fit beside a 320-thread scan CTA in
+// every SM sub-partition's 16K-register file (the scan puts 3 warps x 3840 registers on some),
+// so the k-th of one part runs while the next part is scanned
+__global__ void __launch_bounds__(kKthThreads, 4) kth_kernel(SelectParams p) {
   constexpr int KT = kKthThreads, KW = KT / 32;
   extern __shared__ uint64_t s_bkt[];  // [kKthSmemBucket]
   __shared__ __align__(16) uint32_t s_hist[kHistBins];
