@@ -119,6 +119,16 @@ int tkv_topk_search(const tkv_problem* p, const void* q, const void* k_cache,
                     size_t workspace_bytes, void* stream);
 
 /*
+ * One decode step of one layer: the window append of this token's k/v (GenWindow.append,
+ * attention.py:210; rows n_ctx[b] + n_win[b], then n_win[b] += 1 on device) folded into the
+ * attention call (tkv_topk_decode_attention over context + the grown window) — no separate
+ * append kernel. n_win is required. k_new/v_new [B, Hkv, d] bf16.
+ */
+int tkv_topk_decode_step(const tkv_problem* p, const void* q, const void* k_new, const void* v_new,
+                         void* k_cache, void* v_cache, const int32_t* n_ctx, int32_t* n_win, float* out,
+                         int32_t* idx, float* scores, void* workspace, size_t workspace_bytes, void* stream);
+
+/*
  * Append this token's post-RoPE k/v rows ([B, Hkv, d] bf16) at row base[b] + count[b] of
  * every kv head (base may be NULL → row count[b]). Replaces GenWindow.append,
  * attention.py:94-100 (with base = n_ctx, count = n_win: the window grows after the context).

@@ -23,7 +23,7 @@ from .errors import (
     ShapeError,
     TopkKvError,
 )
-from .ops import Workspace, kv_append, topk_decode_attention, topk_search
+from .ops import Workspace, kv_append, topk_decode_attention, topk_decode_step, topk_search
 from .sharded import CudaStages, shard_range, sharded_topk_attention
 
 __version__ = "0.1.0"
@@ -33,5 +33,5 @@ __all__ = [
     "FormatError", "InfeasibleBudgetError", "InputError", "MipsIndex", "ShapeError",
     "TierAccounting", "TopKResult", "TopkDecoder", "TopkKvError", "VALUE_ROW_BYTES", "Workspace",
     "build_index", "knn_search", "kv_append", "recall_at_k", "shard_range",
-    "sharded_topk_attention", "topk_attend", "topk_decode_attention", "topk_search",
+    "sharded_topk_attention", "topk_attend", "topk_decode_attention", "topk_decode_step", "topk_search",
 ]

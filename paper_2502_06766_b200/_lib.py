@@ -27,6 +27,7 @@ EXPORTS = (
     "tkv_workspace_init",
     "tkv_topk_decode_attention",
     "tkv_topk_search",
+    "tkv_topk_decode_step",
     "tkv_kv_append",
     "tkv_shard_candidates",
     "tkv_shard_merge",
@@ -87,6 +88,8 @@ _SIG = {
     "tkv_topk_decode_attention": (
         [ctypes.POINTER(Problem), _P, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P], _I),
     "tkv_topk_search": ([ctypes.POINTER(Problem), _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P], _I),
+    "tkv_topk_decode_step": (
+        [ctypes.POINTER(Problem), _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P], _I),
     "tkv_kv_append": (
         [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, _P, _P, _P, _P, _P, _P,
          ctypes.c_int32, _P], _I),

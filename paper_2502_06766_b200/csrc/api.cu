@@ -178,6 +178,16 @@ HeadState head_state(void* ws, const Layout& L) {
 }
 
 // sample → threshold for every head; fills the scan / k-th parameter templates
+// window append folded into threshold_kernel for this thread's next run_prefix (decode step)
+struct AppendFold {
+  const void* k_new = nullptr;
+  const void* v_new = nullptr;
+  void* k_cache = nullptr;
+  void* v_cache = nullptr;
+  int32_t* n_win = nullptr;
+};
+thread_local AppendFold g_fold;
+
 int run_prefix(const tkv_problem* p, const void* q, const void* k_cache, const int32_t* n_ctx, void* ws,
                const Layout& L, cudaStream_t st, ScanParams* cp_out, SelectParams* sl_out) {
   const int G = p->n_q_heads / p->n_kv_heads;
@@ -198,6 +208,12 @@ int run_prefix(const tkv_problem* p, const void* q, const void* k_cache, const i
   sp.tl = g_tl;
   sp.pin_words = L.pin_words;
   sp.pin_mask = L.pin_words ? at<uint32_t>(ws, L.pinm) : nullptr;
+  sp.k_new = static_cast<const __nv_bfloat16*>(g_fold.k_new);
+  sp.v_new = static_cast<const __nv_bfloat16*>(g_fold.v_new);
+  sp.k_dst = static_cast<__nv_bfloat16*>(g_fold.k_cache);
+  sp.v_dst = static_cast<__nv_bfloat16*>(g_fold.v_cache);
+  sp.win_count = g_fold.n_win;
+  g_fold = AppendFold{};
   TKV_LAUNCH(launch_sample(sp, st));
   if (!sp.no_filter) ++g_launches;  // sample + threshold kernels
 
@@ -650,6 +666,37 @@ int tkv_topk_search(const tkv_problem* p, const void* q, const void* k_cache, co
   float* sc = scores ? scores : at<float>(ws, L.sscore);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   return run_layer(p, q, k_cache, k_cache, n_ctx, nullptr, idx, sc, nullptr, nullptr, 0, ws, L, st);
+}
+
+int tkv_topk_decode_step(const tkv_problem* p, const void* q, const void* k_new, const void* v_new, void* k_cache,
+                         void* v_cache, const int32_t* n_ctx, int32_t* n_win, float* out, int32_t* idx,
+                         float* scores, void* ws, size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  TRY(validate(p));
+  Layout L;
+  TRY(check_ws(p, ws, ws_bytes, &L));
+  TRY(check_ptr(q, "q", 16));
+  TRY(check_ptr(k_new, "k_new", 16));
+  TRY(check_ptr(v_new, "v_new", 16));
+  TRY(check_ptr(k_cache, "k_cache", 16));
+  TRY(check_ptr(v_cache, "v_cache", 16));
+  TRY(check_ptr(n_ctx, "n_ctx", 4));
+  TRY(check_ptr(n_win, "n_win", 4));
+  TRY(check_ptr(out, "out", 4));
+  TRY(check_ptr(idx, "idx", 4));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float* sc = scores ? scores : at<float>(ws, L.sscore);
+  if (p->flags & TKV_F_FUSED) {  // the fused kernels have no threshold_kernel: append first
+    AppendParams ap{p->batch, p->n_kv_heads, p->cache_rows, static_cast<__nv_bfloat16*>(k_cache),
+                    static_cast<__nv_bfloat16*>(v_cache), static_cast<const __nv_bfloat16*>(k_new),
+                    static_cast<const __nv_bfloat16*>(v_new), n_ctx, n_win, 1};
+    TKV_LAUNCH(launch_append(ap, st));
+  } else {
+    g_fold = AppendFold{k_new, v_new, k_cache, v_cache, n_win};
+  }
+  const int rc = run_layer(p, q, k_cache, v_cache, n_ctx, n_win, idx, sc, nullptr, out, 1, ws, L, st);
+  g_fold = AppendFold{};
+  return rc;
 }
 
 int tkv_kv_append(int32_t batch, int32_t n_kv_heads, int32_t head_dim, int64_t cache_rows,

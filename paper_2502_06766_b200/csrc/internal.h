@@ -70,6 +70,13 @@ struct SampleParams {
   HeadState hs;
   uint32_t* pin_mask;  // [B*Hq][pin_words] selected pinned-prefix rows (zeroed by threshold_kernel)
   int pin_words;
+  // optional window append folded into threshold_kernel (tkv_topk_decode_step): rows
+  // n_ctx[b] + win_count[b] of K/V <- k_new/v_new[b], then win_count[b] += 1
+  const __nv_bfloat16* k_new;  // [B, Hkv, 128] or nullptr
+  const __nv_bfloat16* v_new;
+  __nv_bfloat16* k_dst;
+  __nv_bfloat16* v_dst;
+  int32_t* win_count;
 };
 
 struct ScanParams {

@@ -31,6 +31,21 @@ __global__ void __launch_bounds__(kSampleThreads) sample_kernel(SampleParams p) 
   pdl_trigger();  // the threshold kernel may launch now; it waits for this grid's samples
   if (threadIdx.x == 0) tl_start(p.tl, 0);
   const int seg = blockIdx.y;
+  if (p.k_new && blockIdx.x == 0) {
+    // GenWindow.append (attention.py:94-100, 210) of kv head (b, kvh): the token's k/v rows go
+    // after the context + window; nothing reads them before the finalising gather
+    const int b = seg / p.Hkv, kvh = seg % p.Hkv;
+    const int32_t cnt = p.win_count[b];
+    const int64_t pos = static_cast<int64_t>(p.n_ctx[b]) + cnt;
+    if (pos >= 0 && pos < p.cache_rows && threadIdx.x < 32) {
+      const int which = threadIdx.x >> 4, part = threadIdx.x & 15;
+      const __nv_bfloat16* src = (which ? p.v_new : p.k_new) + (static_cast<int64_t>(b) * p.Hkv + kvh) * kD + part * 8;
+      __nv_bfloat16* dst = (which ? p.v_dst : p.k_dst) +
+                           ((static_cast<int64_t>(b) * p.Hkv + kvh) * p.cache_rows + pos) * kD + part * 8;
+      *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src);
+    }
+    // (the counter advances in threshold_kernel, after this grid — and so every read — is done)
+  }
   const int b = seg / p.Hkv, kvh = seg % p.Hkv;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, c = lane & 3;
@@ -72,6 +87,26 @@ __global__ void __launch_bounds__(kThrThreads) threshold_kernel(SampleParams p) 
   if (threadIdx.x == 0) tl_start(p.tl, 1);
   pdl_wait();     // samples of the sample kernel
   if (threadIdx.x == 0) tl_start(p.tl, 2);
+  if (p.k_new && blockIdx.x % p.Hq == 0) {
+    // GenWindow.append (attention.py:94-100, 210) for batch entry b = blockIdx.x / Hq: the rows
+    // were written by the sample kernel (this kernel waited for it); with no sample kernel
+    // (no_filter) they are written here. Then the window counter advances.
+    const int b = blockIdx.x / p.Hq;
+    const int32_t cnt = p.win_count[b];
+    const int64_t pos = static_cast<int64_t>(p.n_ctx[b]) + cnt;
+    if (p.no_filter && pos >= 0 && pos < p.cache_rows) {
+      const int pieces = p.Hkv * 16;  // 16-byte pieces per tensor
+      for (int i = threadIdx.x; i < 2 * pieces; i += blockDim.x) {
+        const int which = i / pieces, rem = i % pieces, kvh = rem / 16, part = rem % 16;
+        const __nv_bfloat16* src = (which ? p.v_new : p.k_new) + (static_cast<int64_t>(b) * p.Hkv + kvh) * kD + part * 8;
+        __nv_bfloat16* dst = (which ? p.v_dst : p.k_dst) +
+                             ((static_cast<int64_t>(b) * p.Hkv + kvh) * p.cache_rows + pos) * kD + part * 8;
+        *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) p.win_count[b] = cnt + 1;
+  }
   const int bh = blockIdx.x;
   const int b = bh / p.Hq;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

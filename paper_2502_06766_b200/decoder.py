@@ -23,7 +23,8 @@ class TopkDecoder:
     def __init__(self, k_cache: torch.Tensor, v_cache: torch.Tensor, n_ctx, k: int, *,
                  n_win=0, scale: float | None = None, combine: str = "joint",
                  pinned_prefix: int = 0, sorted: bool = False, max_ctx: int | None = None,
-                 fused: bool = False, use_graph: bool = True, parts: int = 0, list_gather: bool = False):
+                 fused: bool = False, use_graph: bool = True, parts: int = 0, list_gather: bool = False,
+                 fold_append: bool = True):
         if k < 1:
             raise InputError("k must be >= 1")
         ops._check_cuda_bf16("k_cache", k_cache, 4)
@@ -41,6 +42,7 @@ class TopkDecoder:
                        max_ctx=self.max_ctx, fused=fused, parts=parts, list_gather=list_gather)
         ops.combine_code(combine)
         self.use_graph = use_graph
+        self.fold_append = fold_append
         self.Hq = None
         self._bufs = None
         self.ws = None
@@ -112,14 +114,19 @@ class TopkDecoder:
             b["in_d"].copy_(b["in_h"], non_blocking=True)
         else:
             b["q"].copy_(b["q_h"], non_blocking=True)
-        if with_kv:
-            ops.kv_append(self.k_cache, self.v_cache, b["k_new"], b["v_new"], self.n_win,
-                          base=self.n_ctx, advance=True)
         # the head-finishing CTAs write the output straight into the pinned host buffer (mapped
         # memory, 512 B per head): no device->host copy node on the step's critical path
-        ops.topk_decode_attention(b["q"], self.k_cache, self.v_cache, self.n_ctx, self.k,
-                                  n_win=self.n_win, out=b["out_h"], idx=b["idx"], scores=b["scores"],
-                                  workspace=self.ws, **self.kw)
+        if with_kv and not self.fold_append:
+            ops.kv_append(self.k_cache, self.v_cache, b["k_new"], b["v_new"], self.n_win,
+                          base=self.n_ctx, advance=True)
+        if with_kv and self.fold_append:  # window append folded into the attention call
+            ops.topk_decode_step(b["q"], b["k_new"], b["v_new"], self.k_cache, self.v_cache, self.n_ctx,
+                                 self.n_win, self.k, out=b["out_h"], idx=b["idx"], scores=b["scores"],
+                                 workspace=self.ws, **self.kw)
+        else:
+            ops.topk_decode_attention(b["q"], self.k_cache, self.v_cache, self.n_ctx, self.k,
+                                      n_win=self.n_win, out=b["out_h"], idx=b["idx"], scores=b["scores"],
+                                      workspace=self.ws, **self.kw)
         if with_idx:
             b["idx_h"].copy_(b["idx"], non_blocking=True)
 

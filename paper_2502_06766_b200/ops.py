@@ -184,6 +184,39 @@ def topk_decode_attention(q, k_cache, v_cache, n_ctx, k: int, *, n_win=None, sca
     return out, idx, scores
 
 
+def topk_decode_step(q, k_new, v_new, k_cache, v_cache, n_ctx, n_win, k: int, *, scale=None,
+                     combine: str = "joint", pinned_prefix: int = 0, sorted: bool = False,
+                     max_ctx: int | None = None, out=None, idx=None, scores=None,
+                     workspace: Workspace | None = None, fused: bool = False, tc_scan: bool | None = None,
+                     parts: int = 0, list_gather: bool = False):
+    """One decode step of one layer (decode_step, attention.py:203-230): append this token's
+    k_new/v_new [B, Hkv, 128] to the window (GenWindow.append, attention.py:210; n_win is a
+    device int32 counter advanced in place) and attend over context + window, in one call."""
+    if k < 1:
+        raise InputError("k must be >= 1")
+    s = check_shapes(q, k_cache, v_cache)
+    dev = q.device
+    n_ctx_t = _as_counts("n_ctx", n_ctx, s.B, dev)
+    if not (isinstance(n_win, torch.Tensor) and n_win.dtype == torch.int32 and n_win.is_cuda and n_win.numel() == s.B):
+        raise ShapeError("n_win must be a device int32 tensor of B counters (advanced in place)")
+    for name, t in (("k_new", k_new), ("v_new", v_new)):
+        _check_cuda_bf16(name, t, 3)
+        if tuple(t.shape) != (s.B, s.Hkv, HEAD_DIM):
+            raise ShapeError(f"{name} must be [B, Hkv, {HEAD_DIM}]")
+    if max_ctx is None:
+        max_ctx = s.cache_rows if isinstance(n_ctx, torch.Tensor) else int(n_ctx_t.max().item())
+    prob = make_problem(s.B, s.Hq, s.Hkv, s.cache_rows, max_ctx, k, pinned_prefix=pinned_prefix,
+                        scale=scale, combine=combine, sorted=sorted, fused=fused, tc_scan=tc_scan,
+                        parts=parts, list_gather=list_gather)
+    ws = workspace or workspace_for(prob, dev)
+    out = out if out is not None else torch.empty((s.B, s.Hq, HEAD_DIM), dtype=torch.float32, device=dev)
+    idx = idx if idx is not None else torch.empty((s.B, s.Hq, k), dtype=torch.int32, device=dev)
+    _lib.call("tkv_topk_decode_step", ctypes.byref(prob), _vp(q), _vp(k_new), _vp(v_new), _vp(k_cache),
+              _vp(v_cache), _vp(n_ctx_t), _vp(n_win), _vp(out), _vp(idx), _vp(scores), ws.ptr, ws.nbytes,
+              _stream(dev))
+    return out, idx, scores
+
+
 def topk_search(q, k_cache, n_ctx, k: int, *, sorted: bool = True, max_ctx: int | None = None,
                 no_filter: bool = False, row_offset: int = 0, workspace: Workspace | None = None,
                 fused: bool = False, tc_scan: bool | None = None, parts: int = 0):

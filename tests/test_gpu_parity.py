@@ -343,3 +343,30 @@ def test_decoder_host_io_steps(cuda, use_graph, variant):
             np.stack([[O.ip_scores_all(Kref[b, h // 4, :N], q[b, h])[idx.numpy()[b, h]] for h in range(Hq)]
                       for b in range(B)]).astype(np.float32)), n_win=[s + 1] * B,
                pinned=variant.get("pinned_prefix", 0))
+
+
+def test_decode_step_folds_append(cuda):
+    """tkv_topk_decode_step (append folded into the attention call) equals kv_append followed
+    by topk_decode_attention, step after step, including n_win advancing on device."""
+    from paper_2502_06766_b200 import kv_append, topk_decode_attention, topk_decode_step
+
+    rng = np.random.default_rng(31)
+    B, Hq, Hkv, N, k = 2, 16, 4, 5000, 128
+    q, K, V = _make(rng, B, Hq, Hkv, N + 8)
+    Ka, Va = _dev(K, cuda), _dev(V, cuda)
+    Kb, Vb = Ka.clone(), Va.clone()
+    n_ctx = torch.tensor([N, N - 300], dtype=torch.int32, device=cuda)
+    wa = torch.zeros(B, dtype=torch.int32, device=cuda)
+    wb = torch.zeros(B, dtype=torch.int32, device=cuda)
+    for s in range(3):
+        qd = _dev(bf16_normal(rng, (B, Hq, 128)), cuda)
+        kn = _dev(bf16_normal(rng, (B, Hkv, 128)), cuda)
+        vn = _dev(bf16_normal(rng, (B, Hkv, 128)), cuda)
+        kv_append(Ka, Va, kn, vn, wa, base=n_ctx, advance=True)
+        o1, i1, _ = topk_decode_attention(qd, Ka, Va, n_ctx, k, n_win=wa, max_ctx=N)
+        o2, i2, _ = topk_decode_step(qd, kn, vn, Kb, Vb, n_ctx, wb, k, max_ctx=N)
+        torch.cuda.synchronize()
+        assert torch.equal(wa, wb) and int(wb[0]) == s + 1
+        assert torch.equal(Ka, Kb) and torch.equal(Va, Vb)
+        assert torch.equal(i1.sort(-1).values, i2.sort(-1).values)
+        assert float((o1 - o2).abs().max()) < 1e-5
