@@ -279,7 +279,13 @@ int run_scan_part(const tkv_problem* p, ScanParams cp, int64_t s0, int64_t s1, c
   cp.seg_begin = s0;
   cp.seg_count = s1 - s0;
   cp.pdl = pdl ? 1 : 0;
-  if (use_tc_scan(p, cp))
+  static const bool fma = [] {  // the north star's CUDA-core FMA scan, for the ncu A/B
+    const char* e = getenv("TKV_SCAN");
+    return e && std::string(e) == "fma";
+  }();
+  if (fma)
+    TKV_LAUNCH(launch_scan_fma(cp, st));
+  else if (use_tc_scan(p, cp))
     TKV_LAUNCH(launch_scan_tc(cp, st));
   else
     TKV_LAUNCH(launch_scan(cp, st));

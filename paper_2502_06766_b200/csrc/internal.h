@@ -235,6 +235,7 @@ bool fused_tc_supported(const FusedParams& p);
 cudaError_t launch_sample(const SampleParams& p, cudaStream_t s);
 cudaError_t launch_scan(const ScanParams& p, cudaStream_t s);
 cudaError_t launch_scan_tc(const ScanParams& p, cudaStream_t s);
+cudaError_t launch_scan_fma(const ScanParams& p, cudaStream_t s);
 bool scan_tc_supported(const ScanParams& p);
 void scan_launch_shape(const ScanParams& p, int* grid, int* smem_bytes);
 cudaError_t launch_select(const SelectParams& p, cudaStream_t s);

@@ -207,6 +207,125 @@ __global__ void __launch_bounds__(kScanWarps * 32, 2) scan_kernel(ScanParams p) 
   scan_body(p, s_buf, s_cnt);
 }
 
+// ------------------------------------------------------------------------------ FMA scan
+// The north-star baseline for the tensor-core scans: CUDA-core FMA + warp-shuffle reductions.
+// A half-warp owns one 256-byte K row (16 lanes × 16-byte load, 8 rows in flight per
+// half-warp); each lane multiplies its 8 elements with the G query heads' matching elements
+// (FMA, q in registers), and 4 xor-shuffle steps per head reduce the 16 partial sums. The
+// candidate emission (threshold test, per-head staging, bulk flush with the key histogram)
+// is the mma.sync scan's. Selected with TKV_SCAN=fma (A/B against the tcgen05 scan by ncu).
+constexpr int kFmaRowsPerIter = kScanWarps * 2 * 8;  // 8 warps × 2 half-warps × 8 rows = 128
+template <int GG>
+__global__ void __launch_bounds__(kScanWarps * 32, 2) scan_fma_kernel(ScanParams p) {
+  extern __shared__ uint64_t s_buf[];  // [G][kScanStage]
+  __shared__ uint32_t s_cnt[8];
+  pdl_trigger();
+  pdl_wait();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int half = lane >> 4, part = lane & 15;
+  const int64_t tps = (p.max_ctx + kFmaRowsPerIter - 1) / kFmaRowsPerIter;
+  const int64_t nseg = p.seg_count ? p.seg_count : static_cast<int64_t>(p.B) * p.Hkv;
+  const int64_t total = nseg * tps;
+  const int64_t t0 = total * blockIdx.x / gridDim.x, t1 = total * (blockIdx.x + 1) / gridDim.x;
+  if (tid < 8) s_cnt[tid] = 0u;
+  __syncthreads();
+  ScanState st;
+  float qv[GG][8];  // [head][element]: this lane's 8 elements of every head of the group
+  uint32_t thr[GG];
+  const __nv_bfloat16* kbase = nullptr;
+  int since = 0;
+  for (int64_t t = t0; t < t1; ++t) {
+    const int64_t lseg = t / tps;
+    const int64_t seg = p.seg_begin + lseg;
+    if (seg != st.seg) {
+      if (st.seg >= 0) scan_flush(p, st, s_buf, s_cnt, warp, lane);
+      since = 0;
+      st.seg = seg;
+      st.b = static_cast<int>(seg / p.Hkv);
+      st.kvh = static_cast<int>(seg % p.Hkv);
+      st.nctx = p.n_ctx[st.b];
+      st.active = true;
+      const int64_t bh0 = static_cast<int64_t>(st.b) * p.Hq + st.kvh * p.G;
+#pragma unroll
+      for (int n = 0; n < GG; ++n) {
+        const bool ok = n < p.G;
+        const uint4 w = ok ? *reinterpret_cast<const uint4*>(p.q + (bh0 + n) * kD + part * 8) : make_uint4(0, 0, 0, 0);
+        qv[n][0] = bf16lo(w.x); qv[n][1] = bf16hi(w.x); qv[n][2] = bf16lo(w.y); qv[n][3] = bf16hi(w.y);
+        qv[n][4] = bf16lo(w.z); qv[n][5] = bf16hi(w.z); qv[n][6] = bf16lo(w.w); qv[n][7] = bf16hi(w.w);
+        thr[n] = ok ? p.hs.thr[bh0 + n] : 0xFFFFFFFFu;
+      }
+      kbase = p.kc + (static_cast<int64_t>(st.b) * p.Hkv + st.kvh) * p.cache_rows * kD + part * 8;
+    }
+    const int64_t rbase = (t - lseg * tps) * kFmaRowsPerIter + (warp * 2 + half) * 8;
+    uint4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t r = rbase + u;
+      v[u] = r < st.nctx ? ldg_stream(kbase + r * kD) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t r = rbase + u;
+      const float x[8] = {bf16lo(v[u].x), bf16hi(v[u].x), bf16lo(v[u].y), bf16hi(v[u].y),
+                          bf16lo(v[u].z), bf16hi(v[u].z), bf16lo(v[u].w), bf16hi(v[u].w)};
+      float sc[GG];
+#pragma unroll
+      for (int n = 0; n < GG; ++n) {
+        float a = 0.f;
+        {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) a = fmaf(qv[n][j], x[j], a);
+#pragma unroll
+          for (int o = 8; o > 0; o >>= 1) a += __shfl_xor_sync(kFull, a, o);
+        }
+        sc[n] = a;
+      }
+      // lane 0 of each half-warp holds the row's G scores
+      const bool row_ok = part == 0 && r < st.nctx;
+#pragma unroll
+      for (int n = 0; n < GG; ++n) {
+        if (n >= p.G) break;
+        const uint32_t key = score_key(sc[n]);
+        const bool pass = row_ok && key >= thr[n];
+        const unsigned m = __ballot_sync(kFull, pass);
+        if (m == 0u) continue;
+        uint32_t b0 = 0;
+        if (lane == static_cast<int>(__ffs(m) - 1)) b0 = atomicAdd(&s_cnt[n], static_cast<uint32_t>(__popc(m)));
+        b0 = __shfl_sync(kFull, b0, __ffs(m) - 1);
+        if (pass) s_buf[n * kScanStage + b0 + __popc(m & lanemask_lt())] = make_comp(key, p.row_offset + static_cast<uint32_t>(r));
+      }
+    }
+    if (++since == kScanFlushEvery) {
+      scan_flush(p, st, s_buf, s_cnt, warp, lane);
+      since = 0;
+    }
+  }
+  if (st.seg >= 0) scan_flush(p, st, s_buf, s_cnt, warp, lane);
+}
+
+cudaError_t launch_scan_fma(const ScanParams& p, cudaStream_t s) {
+  const size_t smem = static_cast<size_t>(p.G) * kScanStage * sizeof(uint64_t);
+  static int grid = 0;
+  if (!grid) {
+    cudaFuncSetAttribute(scan_fma_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         8 * kScanStage * static_cast<int>(sizeof(uint64_t)));
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, scan_fma_kernel<4>, kScanWarps * 32, smem);
+    grid = sms * (per > 0 ? per : 1);
+  }
+  auto k = p.G <= 1 ? scan_fma_kernel<1> : p.G <= 2 ? scan_fma_kernel<2> : p.G <= 4 ? scan_fma_kernel<4> : scan_fma_kernel<8>;
+  static bool attr = false;
+  if (!attr) {
+    for (auto kk : {scan_fma_kernel<1>, scan_fma_kernel<2>, scan_fma_kernel<4>, scan_fma_kernel<8>})
+      cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           8 * kScanStage * static_cast<int>(sizeof(uint64_t)));
+    attr = true;
+  }
+  return launch_pdl(k, dim3(grid), dim3(kScanWarps * 32), smem, s, p.pdl != 0, p);
+}
+
 cudaError_t launch_sample(const SampleParams& p, cudaStream_t s) {
   static bool carve = false;
   if (!carve) {  // same carveout as the scan: the scan's CTAs start beside these (PDL)
