@@ -209,12 +209,29 @@ __global__ void __launch_bounds__(kScanWarps * 32, 2) scan_kernel(ScanParams p) 
 
 // ------------------------------------------------------------------------------ FMA scan
 // The north-star baseline for the tensor-core scans: CUDA-core FMA + warp-shuffle reductions.
-// A half-warp owns one 256-byte K row (16 lanes × 16-byte load, 8 rows in flight per
-// half-warp); each lane multiplies its 8 elements with the G query heads' matching elements
-// (FMA, q in registers), and 4 xor-shuffle steps per head reduce the 16 partial sums. The
+// A half-warp owns 8 K rows per iteration (16 lanes × 16-byte loads, 8 rows in flight); each
+// lane multiplies its 8 elements of each row with the G query heads' matching elements (FMA,
+// q in registers), and one transposed butterfly reduces all 8·G partial sums at once. The
 // candidate emission (threshold test, per-head staging, bulk flush with the key histogram)
 // is the mma.sync scan's. Selected with TKV_SCAN=fma (A/B against the tcgen05 scan by ncu).
 constexpr int kFmaRowsPerIter = kScanWarps * 2 * 8;  // 8 warps × 2 half-warps × 8 rows = 128
+
+// one exchange of the transposed butterfly: N live values → N / 2 (lane bit o picks the half it
+// keeps and adds its partner's copy of); with a single value left, a plain butterfly step
+template <int N, int CAP>
+__device__ __forceinline__ void fma_xstep(float (&a)[CAP], int part, int o) {
+  if constexpr (N >= 2) {
+    const bool up = (part & o) != 0;
+#pragma unroll
+    for (int i = 0; i < N / 2; ++i) {
+      const float send = up ? a[i] : a[i + N / 2];
+      const float keep = up ? a[i + N / 2] : a[i];
+      a[i] = keep + __shfl_xor_sync(kFull, send, o);
+    }
+  } else {
+    a[0] += __shfl_xor_sync(kFull, a[0], o);
+  }
+}
 template <int GG>
 __global__ void __launch_bounds__(kScanWarps * 32, 2) scan_fma_kernel(ScanParams p) {
   extern __shared__ uint64_t s_buf[];  // [G][kScanStage]
@@ -263,30 +280,43 @@ __global__ void __launch_bounds__(kScanWarps * 32, 2) scan_fma_kernel(ScanParams
       const int64_t r = rbase + u;
       v[u] = r < st.nctx ? ldg_stream(kbase + r * kD) : make_uint4(0, 0, 0, 0);
     }
+    // partial dot products of this lane's 8 elements: a[row·GG + head]
+    constexpr int NV = 8 * GG;
+    float a[NV];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const int64_t r = rbase + u;
       const float x[8] = {bf16lo(v[u].x), bf16hi(v[u].x), bf16lo(v[u].y), bf16hi(v[u].y),
                           bf16lo(v[u].z), bf16hi(v[u].z), bf16lo(v[u].w), bf16hi(v[u].w)};
-      float sc[GG];
 #pragma unroll
       for (int n = 0; n < GG; ++n) {
-        float a = 0.f;
-        {
+        float acc = 0.f;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) a = fmaf(qv[n][j], x[j], a);
-#pragma unroll
-          for (int o = 8; o > 0; o >>= 1) a += __shfl_xor_sync(kFull, a, o);
-        }
-        sc[n] = a;
+        for (int j = 0; j < 8; ++j) acc = fmaf(qv[n][j], x[j], acc);
+        a[u * GG + n] = acc;
       }
-      // lane 0 of each half-warp holds the row's G scores
-      const bool row_ok = part == 0 && r < st.nctx;
+    }
+    // transposed butterfly over the 16 lanes of the half-warp: each exchange sends half of the
+    // remaining values and halves the count, so 8 rows × GG heads need NV/2 + NV/4 + ... shuffles
+    // (3.75 per row at GG = 4) instead of 4·GG per row; lane `part` ends with values
+    // j = part·C + t (t < C = NV/16) of the flattened (row, head) index
+    fma_xstep<NV>(a, part, 8);
+    fma_xstep<NV / 2>(a, part, 4);
+    fma_xstep<NV / 4>(a, part, 2);
+    fma_xstep<NV / 8>(a, part, 1);
+    constexpr int C = NV >= 16 ? NV / 16 : 1;  // values per lane after the butterfly
+#pragma unroll
+    for (int t = 0; t < C; ++t) {
+      // (row, head) of this lane's value t: j = part·C + t; with GG = 1 lane pairs hold one row
+      const int j = NV >= 16 ? part * C + t : (part >> 1);
+      const int row = NV >= 16 ? j / GG : j;
+      const int head = NV >= 16 ? j % GG : 0;
+      const int64_t r = rbase + row;
+      const uint32_t key = score_key(a[t]);
+      const bool valid = r < st.nctx && (NV >= 16 || (part & 1) == 0);
 #pragma unroll
       for (int n = 0; n < GG; ++n) {
         if (n >= p.G) break;
-        const uint32_t key = score_key(sc[n]);
-        const bool pass = row_ok && key >= thr[n];
+        const bool pass = valid && head == n && key >= thr[n];
         const unsigned m = __ballot_sync(kFull, pass);
         if (m == 0u) continue;
         uint32_t b0 = 0;
