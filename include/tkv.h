@@ -188,12 +188,16 @@ int tkv_last_launch_count(void);
 int tkv_profile_scan_events(void* start, void* stop);
 
 /*
- * Diagnostics: with a non-NULL device buffer of 16 uint64 (even slots initialised to
- * UINT64_MAX, odd slots to 0), subsequent multi-kernel compute calls on this thread record
- * %globaltimer first-start / last-end stamps of: 0 sample, 1 threshold, 2 threshold past its
- * dependency wait, 3 key scan, 4 scan epilogue past its dependency wait, 5 k-th, 6 gather.
- * NULL disables.
+ * Diagnostics: with a non-NULL device buffer of TKV_TIMELINE_WORDS uint64 (words 0..19:
+ * even words initialised to UINT64_MAX, odd words to 0; words 20.. to 0), subsequent
+ * multi-kernel compute calls on this thread record %globaltimer first-start / last-end stamps
+ * (slot e = words 2e, 2e+1) of: 0 sample, 1 threshold, 2 threshold past its dependency wait,
+ * 3 key scan, 4 scan epilogue past its dependency wait, 5 k-th (or the small-k head kernel),
+ * 6 gather, 7-9 head kernel: threshold found / rows compacted / V gathered; and slots 10-20
+ * accumulate (sum of ns, count) of the head kernel's per-CTA phase durations (see
+ * tools/timeline.py). NULL disables.
  */
+#define TKV_TIMELINE_WORDS 64
 int tkv_debug_timeline(void* buf);
 
 /*

@@ -442,6 +442,70 @@ int run_emit(const tkv_problem* p, const void* q, const void* k_cache, const voi
   return TKV_OK;
 }
 
+// Small k: one CTA per head does the k-th selection, the V gather and the finish
+// (head_topk_kernel) instead of kth_kernel + attend_cand_kernel. Measured faster up to
+// k = 2048 at 32 heads (cfg1/cfg2); above that one SM per head gathers too little in parallel.
+// TKV_HEAD_TOPK=0/1 forces either (1 still needs k <= kHeadMaxK).
+bool use_head_topk(const tkv_problem* p, int gather) {
+  static const int env = [] {
+    const char* e = getenv("TKV_HEAD_TOPK");
+    return e ? atoi(e) : -1;
+  }();
+  if (p->k > kHeadMaxK || (p->flags & TKV_F_GATHER_LIST) || env == 0) return false;
+  if (env > 0) return true;
+  (void)gather;
+  return p->k <= 2048;
+}
+
+int run_head(const tkv_problem* p, const void* q, const void* k_cache, const void* v_cache, const int32_t* n_ctx,
+             const int32_t* n_win, int32_t* idx, float* scores, uint64_t* packed, float* out, int gather, void* ws,
+             const Layout& L, cudaStream_t st, ScanParams cp, SelectParams sl, int nbh, bool pdl) {
+  HeadParams hp{};
+  cp.seg_begin = 0;
+  cp.seg_count = static_cast<int64_t>(p->batch) * p->n_kv_heads;
+  cp.fallback = 1;
+  cp.pdl = 0;
+  sl.pdl = pdl ? 1 : 0;
+  sl.bh_begin = 0;
+  sl.bh_count = nbh;
+  sl.fb_scan = cp;
+  scan_launch_shape(cp, &sl.fb_scan_grid, &sl.fb_scan_smem);
+  hp.s = sl;
+  AttendParams& a = hp.a;
+  a = make_attend(p, q, k_cache, v_cache, n_ctx, n_win, idx, scores, ws, L);
+  a.bh_begin = 0;
+  a.bh_count = nbh;
+  a.idx_out = idx;
+  a.scores_out = scores;
+  a.packed_out = packed;
+  a.out = out;
+  a.gather = gather;
+  a.partial_only = 0;
+  // CTAs per head: enough heads x CTAs to cover the SMs (the gather is per-SM bound), at
+  // least ~256 selected rows per CTA, at most one partial slot each
+  static const int sms = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v > 0 ? v : 148;
+  }();
+  static const int env_c = [] {
+    const char* e = getenv("TKV_HEAD_CTAS");
+    return e ? atoi(e) : 0;
+  }();
+  int C = env_c > 0 ? env_c : sms / nbh;  // one wave: the kernel holds one CTA per SM
+  if (env_c <= 0 && C > (p->k + 255) / 256) C = (p->k + 255) / 256;
+  if (C > 8) C = 8;
+  if (C > L.nchunks) C = L.nchunks;
+  hp.ctas_per_head = C < 1 ? 1 : C;
+  TKV_LAUNCH(launch_head_topk(hp, st));
+  if (p->flags & TKV_F_SORTED) {
+    SortParams so{idx, scores, at<int32_t>(ws, L.mkb), p->k, 0};
+    TKV_LAUNCH(launch_sort(so, nbh, st));
+  }
+  return TKV_OK;
+}
+
 // The whole layer step: the multi-kernel pipeline (default) or, with TKV_F_FUSED, the fused
 // persistent work-queue kernel (fused.cu).
 int run_layer(const tkv_problem* p, const void* q, const void* k_cache, const void* v_cache,
@@ -461,6 +525,9 @@ int run_layer(const tkv_problem* p, const void* q, const void* k_cache, const vo
       // between two kernels would hide the overlap anyway)
       TRY(run_scan_part(p, cp, 0, nseg, st, pdl_enabled() && !prof));
       if (prof) cudaEventRecord(g_scan_stop, st);
+      if (use_head_topk(p, gather))
+        return run_head(p, q, k_cache, v_cache, n_ctx, n_win, idx, scores, packed, out, gather, ws, L, st, cp, sl,
+                        static_cast<int>(nseg * G), pdl_enabled() && !prof);
       TRY(run_kth_part(p, cp, sl, 0, nseg, 0, st, pdl_enabled() && !prof));
       return run_emit(p, q, k_cache, v_cache, n_ctx, n_win, idx, scores, packed, out, gather, ws, L, st, 0,
                       static_cast<int>(nseg * G));

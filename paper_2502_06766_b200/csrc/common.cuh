@@ -341,6 +341,16 @@ __device__ __forceinline__ void tl_end(uint64_t* tl, int e) {
   if (tl) atomicMax(reinterpret_cast<unsigned long long*>(tl + 2 * e + 1), static_cast<unsigned long long>(gtimer()));
 }
 
+// per-CTA phase durations: slot e accumulates (sum of ns, count) — averaged by tools/timeline.py
+__device__ __forceinline__ void tl_phase(uint64_t* tl, int e, uint64_t& t_prev) {
+  if (tl) {
+    const uint64_t t = gtimer();
+    atomicAdd(reinterpret_cast<unsigned long long*>(tl + 2 * e), static_cast<unsigned long long>(t - t_prev));
+    atomicAdd(reinterpret_cast<unsigned long long*>(tl + 2 * e + 1), 1ull);
+    t_prev = t;
+  }
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

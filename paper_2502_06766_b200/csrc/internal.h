@@ -176,6 +176,18 @@ struct AttendParams {
   int bh_begin, bh_count;  // heads handled by attend_cand_kernel; bh_count 0 = all B*Hq
 };
 
+// head_topk_kernel (select.cu): k-th selection + V gather + finish of a head by ctas_per_head
+// CTAs, for k <= kHeadMaxK. att_grid: grid of the candidate-mode gather the exactness fallback
+// tail-launches over all heads.
+constexpr int kHeadThreads = 512;
+constexpr int kHeadMaxK = 4096;
+struct HeadParams {
+  SelectParams s;
+  AttendParams a;
+  int ctas_per_head;  // <= nchunks (partial slots)
+  int att_grid;
+};
+
 struct AppendParams {
   int B, Hkv;
   int64_t cache_rows;
@@ -240,6 +252,7 @@ bool scan_tc_supported(const ScanParams& p);
 void scan_launch_shape(const ScanParams& p, int* grid, int* smem_bytes);
 cudaError_t launch_select(const SelectParams& p, cudaStream_t s);
 cudaError_t launch_kth(const SelectParams& p, cudaStream_t s);
+cudaError_t launch_head_topk(const HeadParams& p, cudaStream_t s);
 cudaError_t launch_attend_cand(const AttendParams& p, cudaStream_t s);
 cudaError_t launch_attend_list(const AttendParams& p, cudaStream_t s);
 cudaError_t launch_sort(const SortParams& p, int nbh, cudaStream_t s);

@@ -21,13 +21,14 @@
 // candidates gathered from every shard; histogram built here from the candidates' range).
 #include <math.h>
 
+#include "attend_cand_dev.cuh"
 #include "scan_dev.cuh"
 
 namespace tkv {
 
 namespace {
-constexpr int NT = kSelectThreads;
-constexpr int NWARP = NT / 32;
+constexpr int SNT = kSelectThreads;
+constexpr int NWARP = SNT / 32;
 
 struct Emit {
   int32_t* idx;
@@ -57,7 +58,7 @@ __device__ __forceinline__ void emit_sel(bool sel, uint64_t c, uint32_t* counter
 }
 }  // namespace
 
-__global__ void __launch_bounds__(NT) select_kernel(SelectParams p) {
+__global__ void __launch_bounds__(SNT) select_kernel(SelectParams p) {
   extern __shared__ uint64_t s_bkt[];  // [kSelectBucketCap]
   __shared__ __align__(16) uint32_t s_hist[kHistBins];
   __shared__ uint32_t s_scr[32];
@@ -90,16 +91,16 @@ __global__ void __launch_bounds__(NT) select_kernel(SelectParams p) {
     shift = p.hs.hshift[bh];
     nvalid = n;
     const uint32_t* gh = p.hs.hist + static_cast<int64_t>(bh) * kHistBins;
-    copy_g2s_u32<NT, kHistBins>(s_hist, gh, kHistBins);
+    copy_g2s_u32<SNT, kHistBins>(s_hist, gh, kHistBins);
     __syncthreads();
   } else {
     uint32_t kmin = 0xffffffffu, kmax = 0u, nv = 0u;
     constexpr int UNR = 8;
-    for (int64_t start = 0; start < n; start += NT * UNR) {
+    for (int64_t start = 0; start < n; start += SNT * UNR) {
       uint64_t cv[UNR];
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
-        const int64_t i = start + u * NT + tid;
+        const int64_t i = start + u * SNT + tid;
         cv[u] = i < n ? load(i) : 0ull;
       }
 #pragma unroll
@@ -123,7 +124,7 @@ __global__ void __launch_bounds__(NT) select_kernel(SelectParams p) {
       s_kmax[warp] = kmax;
       s_scr[warp] = nv;
     }
-    for (int i = tid; i < kHistBins; i += NT) s_hist[i] = 0u;
+    for (int i = tid; i < kHistBins; i += SNT) s_hist[i] = 0u;
     __syncthreads();
     if (warp == 0) {
       uint32_t a = lane < NWARP ? s_kmin[lane] : 0xffffffffu;
@@ -148,11 +149,11 @@ __global__ void __launch_bounds__(NT) select_kernel(SelectParams p) {
     shift = bits > 12 ? static_cast<uint32_t>(bits - 12) : 0u;
     nvalid = s_nvalid;
     __syncthreads();
-    for (int64_t start = 0; start < n; start += NT * UNR) {
+    for (int64_t start = 0; start < n; start += SNT * UNR) {
       uint64_t cv[UNR];
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
-        const int64_t i = start + u * NT + tid;
+        const int64_t i = start + u * SNT + tid;
         cv[u] = i < n ? load(i) : 0ull;
       }
 #pragma unroll
@@ -176,7 +177,7 @@ __global__ void __launch_bounds__(NT) select_kernel(SelectParams p) {
   if (p.pass == kPassMain && nvalid < kb) {
     // The sampled threshold let fewer than k rows through: re-scan this head with thr = 0.
     uint32_t* gh = p.hs.hist + static_cast<int64_t>(bh) * kHistBins;
-    for (int i = tid; i < kHistBins; i += NT) gh[i] = 0u;
+    for (int i = tid; i < kHistBins; i += SNT) gh[i] = 0u;
     if (tid == 0) {
       p.hs.flag_fail[bh] = 1u;
       p.hs.group_fail[b * p.Hkv + h / p.G] = 1u;
@@ -192,7 +193,7 @@ __global__ void __launch_bounds__(NT) select_kernel(SelectParams p) {
   uint32_t dstar = kHistBins, need = 0, bcnt = 0;
   bool whole = true;
   if (!all && kb > 0) {
-    find_bucket<NT, kHistBins>(s_hist, static_cast<uint32_t>(kb), s_out, s_scr);
+    find_bucket<SNT, kHistBins>(s_hist, static_cast<uint32_t>(kb), s_out, s_scr);
     dstar = s_out[0];
     need = static_cast<uint32_t>(kb) - s_out[1];
     bcnt = s_hist[dstar];
@@ -211,11 +212,11 @@ __global__ void __launch_bounds__(NT) select_kernel(SelectParams p) {
   uint64_t vmax = 0ull, vmin = ~0ull;
   if (kb > 0) {
     constexpr int UNR = 8;  // loads in flight per thread (the loop is latency-bound otherwise)
-    for (int64_t start = 0; start < n; start += NT * UNR) {
+    for (int64_t start = 0; start < n; start += SNT * UNR) {
       uint64_t cv[UNR];
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
-        const int64_t i = start + u * NT + tid;
+        const int64_t i = start + u * SNT + tid;
         cv[u] = i < n ? load(i) : 0ull;
       }
 #pragma unroll
@@ -250,8 +251,8 @@ __global__ void __launch_bounds__(NT) select_kernel(SelectParams p) {
         c = s_bkt[i];
         return true;
       };
-      radix_select_u64<NT>(ld, nb, need, s_hist, s_scr, s_out, cs, cp);
-      for (int64_t start = 0; start < nb; start += NT) {
+      radix_select_u64<SNT>(ld, nb, need, s_hist, s_scr, s_out, cs, cp);
+      for (int64_t start = 0; start < nb; start += SNT) {
         const int64_t i = start + tid;
         const uint64_t c = i < nb ? s_bkt[i] : 0ull;
         emit_sel(i < nb && (c >> cs) >= cp, c, &s_nout, em, vmin);
@@ -263,8 +264,8 @@ __global__ void __launch_bounds__(NT) select_kernel(SelectParams p) {
         c = load(i);
         return c != 0ull && hist_digit(comp_key(c), thr, shift) == dstar;
       };
-      radix_select_u64<NT>(ld, n, need, s_hist, s_scr, s_out, cs, cp);
-      for (int64_t start = 0; start < n; start += NT) {
+      radix_select_u64<SNT>(ld, n, need, s_hist, s_scr, s_out, cs, cp);
+      for (int64_t start = 0; start < n; start += SNT) {
         const int64_t i = start + tid;
         uint64_t c = 0ull;
         const bool in = i < n && ld(i, c);
@@ -274,7 +275,7 @@ __global__ void __launch_bounds__(NT) select_kernel(SelectParams p) {
   }
 
   // pads for k > kb (reference clamps k to N, attention.py:147-149)
-  for (int64_t i = kb + tid; i < p.k; i += NT) {
+  for (int64_t i = kb + tid; i < p.k; i += SNT) {
     em.idx[i] = -1;
     em.sc[i] = -INFINITY;
     if (em.pk) em.pk[i] = 0ull;
@@ -521,10 +522,352 @@ cudaError_t launch_kth(const SelectParams& p, cudaStream_t s) {
                     p.pdl && p.pass == kPassMain, p);
 }
 
+// ---------------------------------------------------------------- small k: a few CTAs per head
+// head_topk_kernel: grid (heads x C), 512 threads, for k <= kHeadMaxK. Replaces kth_kernel +
+// attend_cand_kernel when the selected set of a head is small: each of the head's C CTAs
+// finds the k-th threshold itself (histogram bucket → bucket members → rank select, exactly as
+// kth_kernel; the candidates are L2-resident, so the C-fold re-read is cheap and no cross-CTA
+// hand-off is needed), then compacts the selected rows of its 1/C of the candidates into shared
+// memory (idx/scores written on the way), gathers their V rows into partial slot c, and the
+// last CTA of the head finishes it (pinned prefix, window, normalisation). C spreads a head's
+// gather over several SMs: a random 256-byte-row gather runs at ~40 GB/s per SM
+// (profiles/r1_micro.md), so one SM per head would leave most of HBM idle.
+// A head whose sampled threshold let fewer than kb rows through is flagged as in kth_kernel,
+// and the first such head tail-launches the exact chain: re-scan, k-th (fallback pass), and the
+// candidate-mode gather over ALL heads of the call (it rewrites the good heads identically up
+// to fp32 summation order).
+#ifndef TKV_NO_CDP
+__global__ void __launch_bounds__(NT, 4) attend_cand_fb_kernel(AttendParams p) {
+  __shared__ AttSmem sm;
+  extern __shared__ uint32_t s_pref[];
+  attend_cand_run(p, sm, s_pref);
+}
+#endif
+
+constexpr int kHeadSmem = kHistBins * 4 + kHeadMaxK * 12;  // hist | bucket (= comp) | w
+static_assert(kKthSmemBucket <= kHeadMaxK, "bucket aliases the selected composites");
+static_assert((kHeadThreads / 32) * kD <= kHistBins, "reduction aliases the histogram");
+static_assert(kHeadThreads >= NT, "finish group");
+
+__global__ void __launch_bounds__(kHeadThreads, 1) head_topk_kernel(HeadParams hp) {
+  constexpr int HT = kHeadThreads, HW = HT / 32, UNR = 16;
+  const SelectParams& p = hp.s;
+  const AttendParams& a = hp.a;
+  extern __shared__ __align__(16) uint8_t s_dyn[];
+  uint32_t* s_hist = reinterpret_cast<uint32_t*>(s_dyn);  // then s_red [HW][kD]
+  float* s_red = reinterpret_cast<float*>(s_dyn);
+  uint64_t* s_bkt = reinterpret_cast<uint64_t*>(s_dyn + kHistBins * 4);  // then s_comp
+  uint64_t* s_comp = s_bkt;
+  float* s_w = reinterpret_cast<float*>(s_dyn + kHistBins * 4 + kHeadMaxK * 8);
+  __shared__ AttSmem sm;
+  __shared__ uint32_t s_scr[32], s_out[2], s_cnt;
+  __shared__ uint64_t s_rmax[HW], s_res;
+  __shared__ float s_l[HW];
+
+  pdl_wait();  // candidates and histograms of the scan
+  uint64_t t_ph = p.tl ? gtimer() : 0ull;
+  if (threadIdx.x == 0) tl_start(p.tl, 5);
+  const int C = hp.ctas_per_head;
+  const int bh = p.bh_begin + static_cast<int>(blockIdx.x) / C, c = static_cast<int>(blockIdx.x) % C;
+  const int b = bh / p.Hq, h = bh % p.Hq;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t* src = p.src + static_cast<int64_t>(bh) * p.src_stride;
+  int64_t n = p.hs.cand_cnt[bh];
+  if (n > p.src_stride) n = p.src_stride;
+  const int64_t N = p.n_ctx[b];
+  const int64_t kb = N < p.k ? N : p.k;
+  if (tid == 0) tl_phase(p.tl, 10, t_ph);
+
+  if (n < kb) {
+    if (c == 0) {
+      uint32_t* gh = p.hs.hist + static_cast<int64_t>(bh) * kHistBins;
+      for (int i = tid; i < kHistBins; i += HT) gh[i] = 0u;
+      if (tid == 0) {
+        p.hs.flag_fail[bh] = 1u;
+        p.hs.group_fail[b * p.Hkv + h / p.G] = 1u;
+        p.hs.cand_cnt[bh] = 0u;
+        p.hs.thr[bh] = 0u;
+        p.hs.hshift[bh] = kNoFilterShift;
+        __threadfence();
+#ifndef TKV_NO_CDP
+        if (atomicExch(p.hs.fb_launched, 1u) == 0u) {
+          fb_scan_kernel<<<p.fb_scan_grid, kScanWarps * 32, p.fb_scan_smem, cudaStreamTailLaunch>>>(p.fb_scan);
+          SelectParams f = p;
+          f.pass = kPassFallback;
+          f.pdl = 0;
+          const int nbh = p.bh_count ? p.bh_count : p.B * p.Hq;
+          kth_kernel<<<dim3(kKthCtas, nbh), kKthThreads, kKthSmem, cudaStreamTailLaunch>>>(f);
+          attend_cand_fb_kernel<<<hp.att_grid, NT, (nbh + 1) * sizeof(uint32_t), cudaStreamTailLaunch>>>(a);
+        }
+#endif
+      }
+    }
+    return;
+  }
+
+  // ---- k-th threshold T: { c >= T } is exactly the top-kb candidate set. The first batch of
+  // candidates is loaded before the histogram so both memory round trips overlap.
+  uint64_t cv0[UNR];
+#pragma unroll
+  for (int u = 0; u < UNR; ++u) {
+    const int64_t i = u * HT + tid;
+    cv0[u] = i < n ? src[i] : 0ull;
+  }
+  const uint32_t thr = p.hs.thr[bh], shift = p.hs.hshift[bh];
+  const bool all = kb >= n;  // includes kb == 0 (then n == 0)
+  uint32_t dstar = 0, need = 0, bcnt = 0;
+  bool whole = true;
+  if (!all) {
+    copy_g2s_u32<HT, kHistBins>(s_hist, p.hs.hist + static_cast<int64_t>(bh) * kHistBins, kHistBins);
+    __syncthreads();
+    find_bucket<HT, kHistBins>(s_hist, static_cast<uint32_t>(kb), s_out, s_scr);
+    dstar = s_out[0];
+    need = static_cast<uint32_t>(kb) - s_out[1];
+    bcnt = s_hist[dstar];
+    whole = bcnt == need;
+  }
+  if (tid == 0) tl_phase(p.tl, 11, t_ph);
+  const bool refine = !all && !whole;
+  bool big = refine && bcnt > static_cast<uint32_t>(kKthSmemBucket);
+  if (tid == 0) s_cnt = 0u;
+  __syncthreads();
+  uint64_t vmax = 0ull;
+  for (int64_t start = 0; start < n; start += HT * UNR) {
+    uint64_t cv[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int64_t i = start + u * HT + tid;
+      cv[u] = start == 0 ? cv0[u] : (i < n ? src[i] : 0ull);
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const uint64_t cc = cv[u];
+      vmax = cc > vmax ? cc : vmax;
+      const bool inb = refine && !big && cc != 0ull && hist_digit(comp_key(cc), thr, shift) == dstar;
+      const unsigned bb = __ballot_sync(kFull, inb);
+      if (bb) {
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(&s_cnt, __popc(bb));
+        base = __shfl_sync(kFull, base, 0);
+        const uint32_t pos = base + __popc(bb & lanemask_lt());
+        if (inb && pos < static_cast<uint32_t>(kKthSmemBucket)) s_bkt[pos] = cc;
+      }
+    }
+  }
+  vmax = warp_max_u64(vmax);
+  if (lane == 0) s_rmax[warp] = vmax;
+  __syncthreads();
+  vmax = 0ull;
+#pragma unroll
+  for (int w = 0; w < HW; ++w) vmax = s_rmax[w] > vmax ? s_rmax[w] : vmax;
+  const uint32_t nbkt = s_cnt;
+  if (nbkt > static_cast<uint32_t>(kKthSmemBucket)) big = refine;  // histogram/list mismatch guard
+  if (tid == 0) tl_phase(p.tl, 12, t_ph);
+  uint64_t T;
+  if (all) {
+    T = 1ull;  // every valid (non-zero) candidate
+  } else if (whole) {
+    T = static_cast<uint64_t>(thr + (dstar << shift)) << 32;  // lower bound of bucket d*
+  } else if (!big) {
+    T = block_rank_select<HT>(s_bkt, static_cast<int>(nbkt), static_cast<int>(need), &s_res);
+  } else {
+    int cs = 64;
+    uint64_t cp = 0;
+    auto ld = [&](int64_t i, uint64_t& cc) {
+      cc = src[i];
+      return cc != 0ull && hist_digit(comp_key(cc), thr, shift) == dstar;
+    };
+    radix_select_u64<HT>(ld, n, need, s_hist, s_scr, s_out, cs, cp);
+    T = cp << cs;
+  }
+  if (tid == 0) { tl_end(p.tl, 7); tl_phase(p.tl, 13, t_ph); }
+  const float zs = a.scale * kLog2e;
+  const float mscore = key_score(comp_key(vmax));
+  const float zref = kb > 0 ? mscore * zs : 0.f;
+  int32_t* idx_o = a.idx_out + static_cast<int64_t>(bh) * p.k;
+  float* sc_o = a.scores_out + static_cast<int64_t>(bh) * p.k;
+  uint64_t* pk_o = a.packed_out ? a.packed_out + static_cast<int64_t>(bh) * p.k : nullptr;
+  if (c == 0) {
+    if (tid == 0) {
+      p.meta_kth[bh] = kb > 0 ? T : ~0ull;
+      p.meta_kb[bh] = static_cast<int32_t>(kb);
+      p.meta_max[bh] = kb > 0 ? mscore : -INFINITY;
+    }
+    for (int i = static_cast<int>(kb) + tid; i < p.k; i += HT) {  // pads (attention.py:147-149)
+      idx_o[i] = -1;
+      sc_o[i] = -INFINITY;
+      if (pk_o) pk_o[i] = 0ull;
+    }
+  }
+  __syncthreads();  // s_bkt / s_cnt readers done
+  if (tid == 0) s_cnt = 0u;
+  __syncthreads();
+  if (tid == 0) tl_phase(p.tl, 14, t_ph);
+
+  // ---- compaction of this CTA's share (candidate columns [u_lo, u_hi) of every batch) of the
+  // selected rows
+  const int u_lo = c * UNR / C, u_hi = (c + 1) * UNR / C;
+  __shared__ uint32_t s_wsum[HW];
+  uint32_t run = 0u;
+  for (int64_t start = 0; start < n && kb > 0; start += HT * UNR) {
+    uint64_t cv[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int64_t i = start + u * HT + tid;
+      const bool mine = u >= u_lo && u < u_hi;
+      cv[u] = !mine ? 0ull : (start == 0 ? cv0[u] : (i < n ? src[i] : 0ull));
+    }
+    // block-ordered compaction: per-thread counts, one warp scan + one barrier per batch
+    uint32_t mask = 0u;
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) mask |= (cv[u] != 0ull && cv[u] >= T) ? (1u << u) : 0u;
+    const uint32_t mine = __popc(mask);
+    uint32_t incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) s_wsum[warp] = incl;
+    __syncthreads();
+    uint32_t woff = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < HW; ++w) {
+      const uint32_t x = s_wsum[w];
+      woff += w < warp ? x : 0u;
+      tot += x;
+    }
+    uint32_t pos = run + woff + incl - mine;
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      if (mask & (1u << u)) {
+        const uint64_t cc = cv[u];
+        if (pos < static_cast<uint32_t>(kb)) {
+          mark_pinned(a, bh, static_cast<int64_t>(comp_gid(cc)) - a.row_offset);
+          s_comp[pos] = cc;
+          s_w[pos] = exp2f(fmaf(key_score(comp_key(cc)), zs, -zref));
+        }
+        ++pos;
+      }
+    }
+    run += tot;
+    __syncthreads();  // s_wsum reusable
+  }
+  if (tid == 0) s_cnt = run;
+  __syncthreads();
+  // output slots of this CTA's rows: one reservation atomic, completed during the gather
+  if (tid == 0) tl_phase(p.tl, 15, t_ph);
+  __shared__ uint32_t s_gbase;
+  if (tid == 0) s_gbase = s_cnt ? atomicAdd(&a.out_cnt[bh], s_cnt) : 0u;
+  if (tid == 0) { tl_end(p.tl, 8); tl_phase(p.tl, 16, t_ph); }
+  const int nsel = static_cast<int>(min(static_cast<int64_t>(s_cnt), kb));
+  auto write_ids = [&] {  // selected ids / raw scores (order unspecified)
+    const uint32_t gb = s_gbase;
+    for (int i = tid; i < nsel; i += HT) {
+      const uint32_t o = gb + i;
+      if (o < static_cast<uint32_t>(kb)) {
+        const uint64_t cc = s_comp[i];
+        idx_o[o] = static_cast<int32_t>(comp_gid(cc));
+        sc_o[o] = key_score(comp_key(cc));
+        if (pk_o) pk_o[o] = cc;
+      }
+    }
+  };
+  if (!a.gather) {
+    __syncthreads();
+    write_ids();
+    if (tid == 0) tl_end(p.tl, 5);
+    return;
+  }
+
+  // ---- V gather: 16 lanes per 256-byte row, 8 rows in flight per half-warp
+  const int kvh = h / p.G;
+  const int half = lane >> 4, part = lane & 15;
+  const __nv_bfloat16* vb = a.vc + (static_cast<int64_t>(b) * a.Hkv + kvh) * a.cache_rows * kD + part * 8;
+  constexpr int GU = 8;
+  float acc[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+  for (int r0 = warp * 2 + half; r0 < nsel; r0 += 2 * HW * GU) {
+    uint4 v[GU];
+    float w[GU];
+#pragma unroll
+    for (int u = 0; u < GU; ++u) {
+      const int r = r0 + 2 * HW * u;
+      const int64_t row = r < nsel ? static_cast<int64_t>(comp_gid(s_comp[r])) - a.row_offset : -1;
+      w[u] = r < nsel ? s_w[r] : 0.f;
+      v[u] = row >= 0 ? ldg_stream(vb + row * kD) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < GU; ++u) {
+      acc[0] = fmaf(w[u], bf16lo(v[u].x), acc[0]);
+      acc[1] = fmaf(w[u], bf16hi(v[u].x), acc[1]);
+      acc[2] = fmaf(w[u], bf16lo(v[u].y), acc[2]);
+      acc[3] = fmaf(w[u], bf16hi(v[u].y), acc[3]);
+      acc[4] = fmaf(w[u], bf16lo(v[u].z), acc[4]);
+      acc[5] = fmaf(w[u], bf16hi(v[u].z), acc[5]);
+      acc[6] = fmaf(w[u], bf16lo(v[u].w), acc[6]);
+      acc[7] = fmaf(w[u], bf16hi(v[u].w), acc[7]);
+    }
+  }
+  if (tid == 0) tl_phase(p.tl, 17, t_ph);
+  float lw = 0.f;
+  for (int i = tid; i < nsel; i += HT) lw += s_w[i];
+  __syncthreads();  // s_gbase (tid 0, after the compaction barrier) visible
+  write_ids();
+  if (tid == 0) tl_phase(p.tl, 18, t_ph);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j] += __shfl_xor_sync(kFull, acc[j], 16);
+  if (half == 0) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s_red[warp * kD + part * 8 + j] = acc[j];
+  }
+  lw = warp_sum(lw);
+  if (lane == 0) s_l[warp] = lw;
+  __syncthreads();
+  if (tid < kD) {
+    float o = 0.f;
+#pragma unroll
+    for (int w2 = 0; w2 < HW; ++w2) o += s_red[w2 * kD + tid];
+    a.part_o[(static_cast<int64_t>(bh) * a.nchunks + c) * kD + tid] = o;
+  }
+  if (tid == 0) {
+    float l = 0.f;
+#pragma unroll
+    for (int w2 = 0; w2 < HW; ++w2) l += s_l[w2];
+    a.part_l[static_cast<int64_t>(bh) * a.nchunks + c] = l;
+  }
+  if (tid == 0) { tl_end(p.tl, 9); tl_phase(p.tl, 19, t_ph); }
+  // ---- the head's last CTA finishes it: pinned prefix, window, normalisation (first 8 warps)
+  if (tid >= NT) return;
+  ticket_finish<WarpGrp<0, NT, 1>>(a, bh, C, sm);
+  if (tid == 0) { tl_end(p.tl, 5); tl_phase(p.tl, 20, t_ph); }
+}
+
+cudaError_t launch_head_topk(const HeadParams& p, cudaStream_t s) {
+  prepare_fallback_kernels();
+  static int att_grid = 0;
+  if (!att_grid) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+#ifndef TKV_NO_CDP
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, attend_cand_fb_kernel, NT, 8192);
+#endif
+    att_grid = sms * (per > 0 ? per : 1);
+    cudaFuncSetAttribute(head_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHeadSmem);
+  }
+  HeadParams q = p;
+  q.att_grid = att_grid;
+  const int nbh = p.s.bh_count ? p.s.bh_count : p.s.B * p.s.Hq;
+  return launch_pdl(head_topk_kernel, dim3(nbh * p.ctas_per_head), dim3(kHeadThreads), kHeadSmem, s, p.s.pdl != 0,
+                    q);
+}
+
 // ---------------------------------------------------------------- optional sorted output
 // Bitonic sort (descending composite = score desc, id asc: TopKResult order, ann.py:166)
 // of the kb selected rows in shared memory.
-__global__ void __launch_bounds__(NT) sort_kernel(SortParams p) {
+__global__ void __launch_bounds__(SNT) sort_kernel(SortParams p) {
   extern __shared__ uint64_t s_c[];
   const int bh = p.bh_begin + blockIdx.x;
   const int kb = p.meta_kb[bh];
@@ -533,12 +876,12 @@ __global__ void __launch_bounds__(NT) sort_kernel(SortParams p) {
   while (P < kb) P <<= 1;
   int32_t* idx = p.idx + static_cast<int64_t>(bh) * p.k;
   float* sc = p.scores + static_cast<int64_t>(bh) * p.k;
-  for (int i = threadIdx.x; i < P; i += NT)
+  for (int i = threadIdx.x; i < P; i += SNT)
     s_c[i] = i < kb ? make_comp(score_key(sc[i]), static_cast<uint32_t>(idx[i])) : 0ull;
   __syncthreads();
   for (int size = 2; size <= P; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = threadIdx.x; i < P / 2; i += NT) {
+      for (int i = threadIdx.x; i < P / 2; i += SNT) {
         const int lo = 2 * i - (i & (stride - 1));
         const int hi = lo + stride;
         const bool desc = (lo & size) == 0;
@@ -551,7 +894,7 @@ __global__ void __launch_bounds__(NT) sort_kernel(SortParams p) {
       __syncthreads();
     }
   }
-  for (int i = threadIdx.x; i < kb; i += NT) {
+  for (int i = threadIdx.x; i < kb; i += SNT) {
     const uint64_t c = s_c[i];
     idx[i] = static_cast<int32_t>(comp_gid(c));
     sc[i] = key_score(comp_key(c));
@@ -565,7 +908,7 @@ cudaError_t launch_select(const SelectParams& p, cudaStream_t s) {
     cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  select_kernel<<<p.B * p.Hq, NT, smem, s>>>(p);
+  select_kernel<<<p.B * p.Hq, SNT, smem, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -580,7 +923,7 @@ cudaError_t launch_sort(const SortParams& p, int nbh, cudaStream_t s) {
                          static_cast<int>(kSortMax * sizeof(uint64_t)));
     attr = true;
   }
-  sort_kernel<<<nbh, NT, smem, s>>>(p);
+  sort_kernel<<<nbh, SNT, smem, s>>>(p);
   return cudaGetLastError();
 }
 

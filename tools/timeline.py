@@ -9,7 +9,11 @@ import sys
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
-NAMES = ["sample", "threshold", "threshold past wait", "scan", "scan epilogue past wait", "k-th", "gather"]
+NAMES = ["sample", "threshold", "threshold past wait", "scan", "scan epilogue past wait", "k-th", "gather",
+         "head: threshold found", "head: rows compacted", "head: V gathered"]
+PHASES = ["head CTA: start→params", "→hist+bucket", "→pass 1 (max, bucket members)", "→T",
+          "→pads/meta + barriers", "→compaction loop", "→out_cnt reservation", "→V gather loop", "→ids written",
+          "→partial slot written", "→finished (last CTA)"]
 
 
 def main():
@@ -32,9 +36,11 @@ def main():
     kw = dict(max_ctx=n)
     lib = _lib.load()
     acc = np.zeros((len(NAMES), 2))
+    ph = np.zeros(len(PHASES))
     for it in range(args.steps + 3):
-        buf = torch.zeros(16, dtype=torch.int64, device=dev)
-        buf[0::2] = -1  # UINT64_MAX
+        buf = torch.zeros(64,  # TKV_TIMELINE_WORDS
+                           dtype=torch.int64, device=dev)
+        buf[0:2 * len(NAMES):2] = -1  # UINT64_MAX (first-start slots); phase sums stay 0
         tkv.topk_decode_attention(q, K, V, nc, k, **kw)  # previous step in flight: realistic
         lib.tkv_debug_timeline(ctypes.c_void_p(buf.data_ptr()))
         tkv.topk_decode_attention(q, K, V, nc, k, **kw)
@@ -43,6 +49,10 @@ def main():
         t = buf.cpu().numpy().view(np.uint64).astype(np.float64)
         t0 = t[0]
         if it >= 3:
+            for j in range(len(PHASES)):
+                e = len(NAMES) + j
+                if t[2 * e + 1] > 0:
+                    ph[j] += t[2 * e] / t[2 * e + 1] / 1e3
             for e in range(len(NAMES)):
                 s, en = t[2 * e], t[2 * e + 1]
                 acc[e, 0] += (s - t0) / 1e3 if s < 1.8e19 else np.nan
@@ -50,6 +60,9 @@ def main():
     acc /= args.steps
     for e, nm in enumerate(NAMES):
         print(f"  {nm:26s} start {acc[e, 0]:8.1f}  end {acc[e, 1]:8.1f} us")
+    for j, nm in enumerate(PHASES):
+        if ph[j] > 0:
+            print(f"  {nm:34s} {ph[j] / args.steps:8.2f} us (mean)")
 
 
 if __name__ == "__main__":
