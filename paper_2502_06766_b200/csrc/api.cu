@@ -442,19 +442,21 @@ int run_emit(const tkv_problem* p, const void* q, const void* k_cache, const voi
   return TKV_OK;
 }
 
-// Small k: one CTA per head does the k-th selection, the V gather and the finish
-// (head_topk_kernel) instead of kth_kernel + attend_cand_kernel. Measured faster up to
-// k = 2048 at 32 heads (cfg1/cfg2); above that one SM per head gathers too little in parallel.
-// TKV_HEAD_TOPK=0/1 forces either (1 still needs k <= kHeadMaxK).
+// Small k: C CTAs per head do the k-th selection, the V gather and the finish
+// (head_topk_kernel) instead of kth_kernel + attend_cand_kernel. Measured (tools/scan_ab.py):
+// cfg1 (k = 256) 41.9 -> 37.4 us per step; cfg2 (k = 2048) 90.2 vs 91.5; cfg3 (k = 16384)
+// 373 vs 390 — with one 512-thread CTA per SM the head kernel keeps ~64 KB of V rows in flight
+// per SM (~25 GB/s), half of what attend_cand's four CTAs per SM sustain. TKV_HEAD_TOPK=0/1
+// forces either (any k: the selected rows stream through a kHeadCap-row buffer).
 bool use_head_topk(const tkv_problem* p, int gather) {
   static const int env = [] {
     const char* e = getenv("TKV_HEAD_TOPK");
     return e ? atoi(e) : -1;
   }();
-  if (p->k > kHeadMaxK || (p->flags & TKV_F_GATHER_LIST) || env == 0) return false;
+  if ((p->flags & TKV_F_GATHER_LIST) || env == 0) return false;
   if (env > 0) return true;
   (void)gather;
-  return p->k <= 2048;
+  return p->k <= 1024;
 }
 
 int run_head(const tkv_problem* p, const void* q, const void* k_cache, const void* v_cache, const int32_t* n_ctx,

@@ -177,10 +177,10 @@ struct AttendParams {
 };
 
 // head_topk_kernel (select.cu): k-th selection + V gather + finish of a head by ctas_per_head
-// CTAs, for k <= kHeadMaxK. att_grid: grid of the candidate-mode gather the exactness fallback
+// CTAs (selected rows streamed through a kHeadCap-row shared buffer). att_grid: grid of the candidate-mode gather the exactness fallback
 // tail-launches over all heads.
 constexpr int kHeadThreads = 512;
-constexpr int kHeadMaxK = 4096;
+constexpr int kHeadCap = 8192;
 struct HeadParams {
   SelectParams s;
   AttendParams a;

@@ -523,7 +523,7 @@ cudaError_t launch_kth(const SelectParams& p, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------- small k: a few CTAs per head
-// head_topk_kernel: grid (heads x C), 512 threads, for k <= kHeadMaxK. Replaces kth_kernel +
+// head_topk_kernel: grid (heads x C), 512 threads. Replaces kth_kernel +
 // attend_cand_kernel when the selected set of a head is small: each of the head's C CTAs
 // finds the k-th threshold itself (histogram bucket → bucket members → rank select, exactly as
 // kth_kernel; the candidates are L2-resident, so the C-fold re-read is cheap and no cross-CTA
@@ -544,8 +544,10 @@ __global__ void __launch_bounds__(NT, 4) attend_cand_fb_kernel(AttendParams p) {
 }
 #endif
 
-constexpr int kHeadSmem = kHistBins * 4 + kHeadMaxK * 12;  // hist | bucket (= comp) | w
-static_assert(kKthSmemBucket <= kHeadMaxK, "bucket aliases the selected composites");
+// (staging the V rows through shared memory with 1-D bulk copies instead measured 6.7 GB/s
+// per SM — one 256-byte cp.async.bulk per ~36 ns — against ~25 GB/s for register loads)
+constexpr int kHeadSmem = kHistBins * 4 + kHeadCap * 12;  // hist | bucket (= comp) | w
+static_assert(kKthSmemBucket <= kHeadCap, "bucket aliases the selected composites");
 static_assert((kHeadThreads / 32) * kD <= kHistBins, "reduction aliases the histogram");
 static_assert(kHeadThreads >= NT, "finish group");
 
@@ -558,7 +560,9 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_topk_kernel(HeadParams h
   float* s_red = reinterpret_cast<float*>(s_dyn);
   uint64_t* s_bkt = reinterpret_cast<uint64_t*>(s_dyn + kHistBins * 4);  // then s_comp
   uint64_t* s_comp = s_bkt;
-  float* s_w = reinterpret_cast<float*>(s_dyn + kHistBins * 4 + kHeadMaxK * 8);
+  float* s_w = reinterpret_cast<float*>(s_dyn + kHistBins * 4 + kHeadCap * 8);
+  static_assert(kHeadCap == HT * UNR, "one batch of candidates fits the row buffer");
+
   __shared__ AttSmem sm;
   __shared__ uint32_t s_scr[32], s_out[2], s_cnt;
   __shared__ uint64_t s_rmax[HW], s_res;
@@ -704,8 +708,61 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_topk_kernel(HeadParams h
   __syncthreads();
   if (tid == 0) tl_phase(p.tl, 14, t_ph);
 
-  // ---- compaction of this CTA's share (candidate columns [u_lo, u_hi) of every batch) of the
-  // selected rows
+  // ---- streaming compaction of this CTA's share (candidate columns [u_lo, u_hi) of every
+  // batch) of the selected rows into shared memory; whenever the next batch would overflow the
+  // kHeadCap-row buffer, the buffered rows are flushed: output slots reserved (one atomic),
+  // their V rows gathered into registers (16 lanes per 256-byte row, 8 rows in flight per
+  // half-warp), ids / raw scores written (order unspecified).
+  const int kvh = h / p.G;
+  const int half = lane >> 4, part = lane & 15;
+  const __nv_bfloat16* vb = a.vc + (static_cast<int64_t>(b) * a.Hkv + kvh) * a.cache_rows * kD + part * 8;
+  float acc[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+  float lw = 0.f;
+  __shared__ uint32_t s_gbase;
+  auto flush = [&](uint32_t cnt) {  // rows [0, cnt) of s_comp / s_w; block-uniform cnt
+    if (tid == 0) s_gbase = cnt ? atomicAdd(&a.out_cnt[bh], cnt) : 0u;
+    __syncthreads();
+    const int nr = static_cast<int>(cnt);
+    if (a.gather) {
+      constexpr int GU = 8;
+      for (int r0 = warp * 2 + half; r0 < nr; r0 += 2 * HW * GU) {
+        uint4 v[GU];
+        float w[GU];
+#pragma unroll
+        for (int u = 0; u < GU; ++u) {
+          const int r = r0 + 2 * HW * u;
+          const int64_t row = r < nr ? static_cast<int64_t>(comp_gid(s_comp[r])) - a.row_offset : -1;
+          w[u] = r < nr ? s_w[r] : 0.f;
+          v[u] = row >= 0 ? ldg_stream(vb + row * kD) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < GU; ++u) {
+          acc[0] = fmaf(w[u], bf16lo(v[u].x), acc[0]);
+          acc[1] = fmaf(w[u], bf16hi(v[u].x), acc[1]);
+          acc[2] = fmaf(w[u], bf16lo(v[u].y), acc[2]);
+          acc[3] = fmaf(w[u], bf16hi(v[u].y), acc[3]);
+          acc[4] = fmaf(w[u], bf16lo(v[u].z), acc[4]);
+          acc[5] = fmaf(w[u], bf16hi(v[u].z), acc[5]);
+          acc[6] = fmaf(w[u], bf16lo(v[u].w), acc[6]);
+          acc[7] = fmaf(w[u], bf16hi(v[u].w), acc[7]);
+        }
+      }
+      for (int i = tid; i < nr; i += HT) lw += s_w[i];
+    }
+    const uint32_t gb = s_gbase;
+    for (int i = tid; i < nr; i += HT) {
+      const uint32_t o = gb + i;
+      if (o < static_cast<uint32_t>(kb)) {
+        const uint64_t cc = s_comp[i];
+        idx_o[o] = static_cast<int32_t>(comp_gid(cc));
+        sc_o[o] = key_score(comp_key(cc));
+        if (pk_o) pk_o[o] = cc;
+      }
+    }
+    __syncthreads();  // buffer reusable
+  };
   const int u_lo = c * UNR / C, u_hi = (c + 1) * UNR / C;
   __shared__ uint32_t s_wsum[HW];
   uint32_t run = 0u;
@@ -737,85 +794,31 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_topk_kernel(HeadParams h
       woff += w < warp ? x : 0u;
       tot += x;
     }
+    if (run + tot > static_cast<uint32_t>(kHeadCap)) {  // a batch selects at most HT * UNR = kHeadCap
+      flush(run);
+      run = 0u;
+    }
     uint32_t pos = run + woff + incl - mine;
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
       if (mask & (1u << u)) {
         const uint64_t cc = cv[u];
-        if (pos < static_cast<uint32_t>(kb)) {
-          mark_pinned(a, bh, static_cast<int64_t>(comp_gid(cc)) - a.row_offset);
-          s_comp[pos] = cc;
-          s_w[pos] = exp2f(fmaf(key_score(comp_key(cc)), zs, -zref));
-        }
+        mark_pinned(a, bh, static_cast<int64_t>(comp_gid(cc)) - a.row_offset);
+        s_comp[pos] = cc;
+        s_w[pos] = exp2f(fmaf(key_score(comp_key(cc)), zs, -zref));
         ++pos;
       }
     }
     run += tot;
-    __syncthreads();  // s_wsum reusable
+    __syncthreads();  // s_wsum reusable; rows visible
   }
-  if (tid == 0) s_cnt = run;
-  __syncthreads();
-  // output slots of this CTA's rows: one reservation atomic, completed during the gather
   if (tid == 0) tl_phase(p.tl, 15, t_ph);
-  __shared__ uint32_t s_gbase;
-  if (tid == 0) s_gbase = s_cnt ? atomicAdd(&a.out_cnt[bh], s_cnt) : 0u;
+  flush(run);
   if (tid == 0) { tl_end(p.tl, 8); tl_phase(p.tl, 16, t_ph); }
-  const int nsel = static_cast<int>(min(static_cast<int64_t>(s_cnt), kb));
-  auto write_ids = [&] {  // selected ids / raw scores (order unspecified)
-    const uint32_t gb = s_gbase;
-    for (int i = tid; i < nsel; i += HT) {
-      const uint32_t o = gb + i;
-      if (o < static_cast<uint32_t>(kb)) {
-        const uint64_t cc = s_comp[i];
-        idx_o[o] = static_cast<int32_t>(comp_gid(cc));
-        sc_o[o] = key_score(comp_key(cc));
-        if (pk_o) pk_o[o] = cc;
-      }
-    }
-  };
   if (!a.gather) {
-    __syncthreads();
-    write_ids();
     if (tid == 0) tl_end(p.tl, 5);
     return;
   }
-
-  // ---- V gather: 16 lanes per 256-byte row, 8 rows in flight per half-warp
-  const int kvh = h / p.G;
-  const int half = lane >> 4, part = lane & 15;
-  const __nv_bfloat16* vb = a.vc + (static_cast<int64_t>(b) * a.Hkv + kvh) * a.cache_rows * kD + part * 8;
-  constexpr int GU = 8;
-  float acc[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) acc[j] = 0.f;
-  for (int r0 = warp * 2 + half; r0 < nsel; r0 += 2 * HW * GU) {
-    uint4 v[GU];
-    float w[GU];
-#pragma unroll
-    for (int u = 0; u < GU; ++u) {
-      const int r = r0 + 2 * HW * u;
-      const int64_t row = r < nsel ? static_cast<int64_t>(comp_gid(s_comp[r])) - a.row_offset : -1;
-      w[u] = r < nsel ? s_w[r] : 0.f;
-      v[u] = row >= 0 ? ldg_stream(vb + row * kD) : make_uint4(0, 0, 0, 0);
-    }
-#pragma unroll
-    for (int u = 0; u < GU; ++u) {
-      acc[0] = fmaf(w[u], bf16lo(v[u].x), acc[0]);
-      acc[1] = fmaf(w[u], bf16hi(v[u].x), acc[1]);
-      acc[2] = fmaf(w[u], bf16lo(v[u].y), acc[2]);
-      acc[3] = fmaf(w[u], bf16hi(v[u].y), acc[3]);
-      acc[4] = fmaf(w[u], bf16lo(v[u].z), acc[4]);
-      acc[5] = fmaf(w[u], bf16hi(v[u].z), acc[5]);
-      acc[6] = fmaf(w[u], bf16lo(v[u].w), acc[6]);
-      acc[7] = fmaf(w[u], bf16hi(v[u].w), acc[7]);
-    }
-  }
-  if (tid == 0) tl_phase(p.tl, 17, t_ph);
-  float lw = 0.f;
-  for (int i = tid; i < nsel; i += HT) lw += s_w[i];
-  __syncthreads();  // s_gbase (tid 0, after the compaction barrier) visible
-  write_ids();
-  if (tid == 0) tl_phase(p.tl, 18, t_ph);
 #pragma unroll
   for (int j = 0; j < 8; ++j) acc[j] += __shfl_xor_sync(kFull, acc[j], 16);
   if (half == 0) {
