@@ -20,7 +20,8 @@ from dataclasses import dataclass
 import torch
 
 from . import ops
-from .errors import InputError
+from .budget import LayerBudget
+from .errors import ConfigError, InputError
 
 
 @dataclass(frozen=True)
@@ -64,11 +65,23 @@ def rmsnorm(x: torch.Tensor, w: torch.Tensor, eps: float) -> torch.Tensor:
 class TopkLlamaDecoder:
     """Batch-1 decode with every layer's KV cache resident in HBM ([1, Hkv, rows, 128] bf16)."""
 
-    def __init__(self, shape: LlamaShape, n_ctx: int, k: int, *, device="cuda", seed: int = 0,
-                 window_capacity: int = 256, init_std: float = 0.02):
+    def __init__(self, shape: LlamaShape, n_ctx: int, k: "int | LayerBudget", *, device="cuda", seed: int = 0,
+                 window_capacity: int = 256, init_std: float = 0.02, retrieval_hook=None):
+        """k: one k for every layer, or a per-layer LayerBudget (budget.py; the reference's
+        decode_step takes `budget[l]`, attention.py:202-221 — its layer count must match,
+        attention.py:190-191). retrieval_hook(layer, idx): called after each layer's attention
+        with the selected ids (device tensor [1, Hq, k_layer], -1 pads), like the reference's
+        per-head hook (attention.py:229-230); eager steps only."""
         if shape.head_dim != ops.HEAD_DIM:
             raise InputError(f"head_dim must be {ops.HEAD_DIM}")
-        self.shape, self.n, self.k = shape, n_ctx, k
+        if isinstance(k, LayerBudget):
+            if k.n_layers != shape.n_layers:
+                raise ConfigError(f"budget has {k.n_layers} layers, model has {shape.n_layers}")
+            self.budget = k
+        else:
+            self.budget = LayerBudget(tuple([int(k)] * shape.n_layers))
+        self.shape, self.n, self.k = shape, n_ctx, self.budget.k_max
+        self.retrieval_hook = retrieval_hook
         self.device = torch.device(device)
         dev, s = self.device, shape
         g = torch.Generator(device=dev).manual_seed(seed)
@@ -101,17 +114,21 @@ class TopkLlamaDecoder:
         self.n_win = torch.zeros(1, dtype=torch.int32, device=dev)
         self.pos = torch.zeros(1, dtype=torch.int64, device=dev)  # absolute position of the token
         self.cos, self.sin = rope_tables(s, rows, dev)
-        prob = ops.make_problem(1, s.n_heads, s.n_kv_heads, rows, n_ctx, k)
+        # one workspace sized for the largest k serves every layer: its control words sit at
+        # k-independent offsets (api.cu make_layout)
+        prob = ops.make_problem(1, s.n_heads, s.n_kv_heads, rows, n_ctx, self.k)
         self.ws = ops.Workspace(prob, dev)
         self.token = torch.zeros(1, dtype=torch.int64, device=dev)
         self.next_token = torch.zeros(1, dtype=torch.int64, device=dev)
         self.attn_out = torch.empty((1, s.n_heads, s.head_dim), dtype=torch.float32, device=dev)
-        self.idx = torch.empty((1, s.n_heads, k), dtype=torch.int32, device=dev)
-        self.scores = torch.empty((1, s.n_heads, k), dtype=torch.float32, device=dev)
+        self._sel = {kl: (torch.empty((1, s.n_heads, kl), dtype=torch.int32, device=dev),
+                          torch.empty((1, s.n_heads, kl), dtype=torch.float32, device=dev))
+                     for kl in sorted(set(self.budget.k_per_layer))}
+        self.idx, self.scores = self._sel[self.k]
         self.graph = None
         self.pos.fill_(n_ctx)
 
-    def _layer(self, x: torch.Tensor, lw: dict) -> torch.Tensor:
+    def _layer(self, x: torch.Tensor, lw: dict, layer: int = 0) -> torch.Tensor:
         s = self.shape
         h = rmsnorm(x, lw["n1"], s.eps)
         qkv = (h @ lw["wqkv"]).float()
@@ -126,9 +143,13 @@ class TopkLlamaDecoder:
         v = v.to(torch.bfloat16).contiguous()
         # window append (attention.py:210) — advance n_win once per step, after the last layer
         ops.kv_append(lw["K"], lw["V"], kk, v, self.n_win, base=self.n_ctx, advance=False)
-        ops.topk_decode_attention(q.contiguous(), lw["K"], lw["V"], self.n_ctx, self.k, n_win=self._n_win_next,
-                                  out=self.attn_out, idx=self.idx, scores=self.scores, workspace=self.ws,
+        kl = self.budget[layer]
+        idx, scores = self._sel[kl]
+        ops.topk_decode_attention(q.contiguous(), lw["K"], lw["V"], self.n_ctx, kl, n_win=self._n_win_next,
+                                  out=self.attn_out, idx=idx, scores=scores, workspace=self.ws,
                                   max_ctx=self.n)
+        if self.retrieval_hook is not None:
+            self.retrieval_hook(layer, idx)
         x = x + self.attn_out.view(1, -1).to(torch.bfloat16) @ lw["wo"]
         h2 = rmsnorm(x, lw["n2"], s.eps)
         gu = h2 @ lw["wgu"]
@@ -139,8 +160,8 @@ class TopkLlamaDecoder:
     def _step_body(self) -> None:
         x = self.embed.index_select(0, self.token)
         self._n_win_next = self.n_win + 1  # the token attends to itself (attention.py:210)
-        for lw in self.layers:
-            x = self._layer(x, lw)
+        for layer, lw in enumerate(self.layers):
+            x = self._layer(x, lw, layer)
         logits = rmsnorm(x, self.norm_f, self.shape.eps) @ self.lm_head
         self.next_token.copy_(logits.argmax(-1))
         self.n_win.add_(1)
@@ -159,6 +180,8 @@ class TopkLlamaDecoder:
 
     def capture(self) -> None:
         """Capture one step into a CUDA graph (window and position advance on device)."""
+        if self.retrieval_hook is not None:
+            raise ConfigError("retrieval_hook runs host code per layer: eager steps only, no graph capture")
         torch.cuda.synchronize(self.device)
         saved = (self.n_win.clone(), self.pos.clone(), self.token.clone())
         self._step_body()  # warm-up: lazy libtkv / cuBLAS setup outside the capture

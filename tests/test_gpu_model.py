@@ -48,3 +48,30 @@ def test_graph_step_advances_window(cuda):
     dec2 = TopkLlamaDecoder(_tiny(), 5000, 100, device=cuda, seed=2)
     toks2 = [int(dec2.step(7 if i == 0 else None).item()) for i in range(4)]
     assert toks == toks2
+
+
+def test_layer_budget_and_retrieval_hook(cuda):
+    """Per-layer k from a LayerBudget (attention.py:202-221 budget[l]) with one shared workspace,
+    and the retrieval hook seeing each layer's ids (context rows only: generated tokens never
+    enter the index)."""
+    from paper_2502_06766_b200 import budget as B
+    from paper_2502_06766_b200.model import TopkLlamaDecoder
+
+    shape = _tiny()
+    bud = B.linear_budget(shape.n_layers, 40 * shape.n_layers)
+    seen = {}
+    N = 4000
+    dec = TopkLlamaDecoder(shape, N, bud, device=cuda, seed=3,
+                           retrieval_hook=lambda layer, idx: seen.__setitem__(layer, idx.clone()))
+    assert dec.k == max(bud.k_per_layer)
+    dec.step(11)
+    torch.cuda.synchronize()
+    assert sorted(seen) == list(range(shape.n_layers))
+    for layer, idx in seen.items():
+        assert idx.shape == (1, shape.n_heads, bud[layer])
+        assert int(idx.min()) >= 0 and int(idx.max()) < N
+        assert all(len(set(row.tolist())) == bud[layer] for row in idx[0].cpu())  # distinct ids
+    with pytest.raises(Exception):
+        dec.capture()  # hook set: eager only
+    with pytest.raises(Exception):
+        TopkLlamaDecoder(shape, N, B.uniform_budget(shape.n_layers + 1, 100), device=cuda)
