@@ -48,6 +48,8 @@ F_FUSED = 4
 F_SCAN_HMMA = 8
 F_PARTS_SHIFT = 8  # TKV_F_PARTS(n): bits 8..11
 F_GATHER_LIST = 16
+F_HEAD = 32
+F_NO_HEAD = 64
 
 
 class Problem(ctypes.Structure):

@@ -447,13 +447,15 @@ int run_emit(const tkv_problem* p, const void* q, const void* k_cache, const voi
 // cfg1 (k = 256) 41.9 -> 37.4 us per step; cfg2 (k = 2048) 90.2 vs 91.5; cfg3 (k = 16384)
 // 373 vs 390 — with one 512-thread CTA per SM the head kernel keeps ~64 KB of V rows in flight
 // per SM (~25 GB/s), half of what attend_cand's four CTAs per SM sustain. TKV_HEAD_TOPK=0/1
-// forces either (any k: the selected rows stream through a kHeadCap-row buffer).
+// forces either (any k: the selected rows stream through a kHeadCap-row buffer); the
+// TKV_F_HEAD / TKV_F_NO_HEAD flags force it per call.
 bool use_head_topk(const tkv_problem* p, int gather) {
   static const int env = [] {
     const char* e = getenv("TKV_HEAD_TOPK");
     return e ? atoi(e) : -1;
   }();
-  if ((p->flags & TKV_F_GATHER_LIST) || env == 0) return false;
+  if (p->flags & TKV_F_HEAD) return true;
+  if ((p->flags & (TKV_F_GATHER_LIST | TKV_F_NO_HEAD)) || env == 0) return false;
   if (env > 0) return true;
   (void)gather;
   return p->k <= 1024;

@@ -44,7 +44,8 @@ def make_problem(B: int, Hq: int, Hkv: int, cache_rows: int, max_ctx: int, k: in
                  pinned_prefix: int = 0, scale: float | None = None, combine: str = "joint",
                  sorted: bool = False, no_filter: bool = False, row_offset: int = 0,
                  head_dim: int = HEAD_DIM, fused: bool = False,
-                 tc_scan: bool | None = None, parts: int = 0, list_gather: bool = False) -> _lib.Problem:
+                 tc_scan: bool | None = None, parts: int = 0, list_gather: bool = False,
+                 head: bool | None = None) -> _lib.Problem:
     p = _lib.Problem()
     p.batch, p.n_q_heads, p.n_kv_heads, p.head_dim = B, Hq, Hkv, head_dim
     p.cache_rows, p.max_ctx, p.k = cache_rows, max_ctx, k
@@ -62,6 +63,8 @@ def make_problem(B: int, Hq: int, Hkv: int, cache_rows: int, max_ctx: int, k: in
     p.flags |= parts << _lib.F_PARTS_SHIFT
     if list_gather:
         p.flags |= _lib.F_GATHER_LIST
+    if head is not None:  # per-head k-th + gather kernel forced on / off (None: automatic, k <= 1024)
+        p.flags |= _lib.F_HEAD if head else _lib.F_NO_HEAD
     p.row_offset = row_offset
     return p
 
@@ -154,7 +157,7 @@ def topk_decode_attention(q, k_cache, v_cache, n_ctx, k: int, *, n_win=None, sca
                           max_ctx: int | None = None, no_filter: bool = False, row_offset: int = 0,
                           out=None, idx=None, scores=None, workspace: Workspace | None = None,
                           fused: bool = False, tc_scan: bool | None = None, parts: int = 0,
-                          list_gather: bool = False):
+                          list_gather: bool = False, head: bool | None = None):
     """Exact top-k decode attention for every (batch, q head) of one layer.
 
     q [B, Hq, 128] bf16; k_cache/v_cache [B, Hkv, rows, 128] bf16 with the context in rows
@@ -173,7 +176,7 @@ def topk_decode_attention(q, k_cache, v_cache, n_ctx, k: int, *, n_win=None, sca
     prob = make_problem(s.B, s.Hq, s.Hkv, s.cache_rows, max_ctx, k, pinned_prefix=pinned_prefix,
                         scale=scale, combine=combine, sorted=sorted, no_filter=no_filter,
                         row_offset=row_offset, fused=fused, tc_scan=tc_scan, parts=parts,
-                        list_gather=list_gather)
+                        list_gather=list_gather, head=head)
     ws = workspace or workspace_for(prob, dev)
     out = out if out is not None else torch.empty((s.B, s.Hq, HEAD_DIM), dtype=torch.float32, device=dev)
     idx = idx if idx is not None else torch.empty((s.B, s.Hq, k), dtype=torch.int32, device=dev)
@@ -188,7 +191,7 @@ def topk_decode_step(q, k_new, v_new, k_cache, v_cache, n_ctx, n_win, k: int, *,
                      combine: str = "joint", pinned_prefix: int = 0, sorted: bool = False,
                      max_ctx: int | None = None, out=None, idx=None, scores=None,
                      workspace: Workspace | None = None, fused: bool = False, tc_scan: bool | None = None,
-                     parts: int = 0, list_gather: bool = False):
+                     parts: int = 0, list_gather: bool = False, head: bool | None = None):
     """One decode step of one layer (decode_step, attention.py:203-230): append this token's
     k_new/v_new [B, Hkv, 128] to the window (GenWindow.append, attention.py:210; n_win is a
     device int32 counter advanced in place) and attend over context + window, in one call."""
@@ -207,7 +210,7 @@ def topk_decode_step(q, k_new, v_new, k_cache, v_cache, n_ctx, n_win, k: int, *,
         max_ctx = s.cache_rows if isinstance(n_ctx, torch.Tensor) else int(n_ctx_t.max().item())
     prob = make_problem(s.B, s.Hq, s.Hkv, s.cache_rows, max_ctx, k, pinned_prefix=pinned_prefix,
                         scale=scale, combine=combine, sorted=sorted, fused=fused, tc_scan=tc_scan,
-                        parts=parts, list_gather=list_gather)
+                        parts=parts, list_gather=list_gather, head=head)
     ws = workspace or workspace_for(prob, dev)
     out = out if out is not None else torch.empty((s.B, s.Hq, HEAD_DIM), dtype=torch.float32, device=dev)
     idx = idx if idx is not None else torch.empty((s.B, s.Hq, k), dtype=torch.int32, device=dev)
@@ -219,7 +222,7 @@ def topk_decode_step(q, k_new, v_new, k_cache, v_cache, n_ctx, n_win, k: int, *,
 
 def topk_search(q, k_cache, n_ctx, k: int, *, sorted: bool = True, max_ctx: int | None = None,
                 no_filter: bool = False, row_offset: int = 0, workspace: Workspace | None = None,
-                fused: bool = False, tc_scan: bool | None = None, parts: int = 0):
+                fused: bool = False, tc_scan: bool | None = None, parts: int = 0, head: bool | None = None):
     """Exact top-k rows per (batch, q head) without attention (knn_search flat, ann.py:203-218).
 
     Returns (idx [B, Hq, k] int32, scores [B, Hq, k] f32), TopKResult-ordered when sorted.
@@ -233,7 +236,7 @@ def topk_search(q, k_cache, n_ctx, k: int, *, sorted: bool = True, max_ctx: int 
         max_ctx = s.cache_rows if isinstance(n_ctx, torch.Tensor) else int(n_ctx_t.max().item())
     prob = make_problem(s.B, s.Hq, s.Hkv, s.cache_rows, max_ctx, k, sorted=sorted,
                         no_filter=no_filter, row_offset=row_offset, fused=fused, tc_scan=tc_scan,
-                        parts=parts)
+                        parts=parts, head=head)
     ws = workspace or workspace_for(prob, dev)
     idx = torch.empty((s.B, s.Hq, k), dtype=torch.int32, device=dev)
     scores = torch.empty((s.B, s.Hq, k), dtype=torch.float32, device=dev)
