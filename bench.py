@@ -322,8 +322,8 @@ def main():
         e2e = {"value": round(e2e_us, 2), "unit": "us", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "steps": e2e_steps,
                "path": "TopkDecoder.step: host q + new k/v row -> pinned staging -> CUDA-graph replay "
-                       "(one H2D copy, KV append, top-k attention writing out into pinned host memory) "
-                       "-> host sync, every step"}
+                       "(a staging kernel reads q/k/v from pinned host memory, KV append, top-k "
+                       "attention writing out into pinned host memory) -> host sync, every step"}
 
     if rank != 0:
         if world > 1:

@@ -66,6 +66,9 @@ extern "C" {
 #define TKV_F_PARTS_MASK 0xF00u
 #define TKV_F_GATHER_LIST 16u /* V gather as filter pass + balanced list gather (automatic from  \
                                  ~1M selected rows per call)                                    */
+#define TKV_F_HOST_Q 128u  /* q (and tkv_topk_decode_step's k_new/v_new) are pinned host buffers   \
+                              (device-accessible through UVA): one small kernel stages q into the \
+                              workspace, so a host-I/O step needs no H2D copy of its inputs      */
 #define TKV_F_HEAD 32u     /* k-th + V gather by the per-head kernel (head_topk_kernel) at any k   */
 #define TKV_F_NO_HEAD 64u  /* never the per-head kernel (automatic: k <= 1024, one part)          */
 #define TKV_F_SCAN_HMMA 8u /* key scan on register-staged mma.sync (scan.cu) instead of the TMA +  

@@ -50,6 +50,7 @@ F_PARTS_SHIFT = 8  # TKV_F_PARTS(n): bits 8..11
 F_GATHER_LIST = 16
 F_HEAD = 32
 F_NO_HEAD = 64
+F_HOST_Q = 128
 
 
 class Problem(ctypes.Structure):

@@ -24,6 +24,7 @@ thread_local int g_launches = 0;
 thread_local cudaEvent_t g_scan_start = nullptr, g_scan_stop = nullptr;
 thread_local uint64_t* g_trace = nullptr;
 thread_local uint64_t* g_tl = nullptr;
+thread_local bool g_staged = false;  // q staged by stage_kernel in this call (TKV_F_HOST_Q)
 thread_local uint32_t g_trace_cap = 0;
 
 int fail(int code, const char* fmt, ...) {
@@ -48,7 +49,7 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 struct Layout {
   size_t ticket_g, ticket_k, flag, gflag, fctl, fbl, ctrl_end;
   size_t maxc, bktc, bkt, outc;
-  size_t cnt, thr, hshift, hist, mmax, mkth, mkb, samp, cand, sidx, sscore, pl, po, pinm, total;
+  size_t cnt, thr, hshift, hist, mmax, mkth, mkb, samp, cand, sidx, sscore, pl, po, pinm, qs, total;
   int pin_words;
   int64_t cap;
   int nchunks;
@@ -100,6 +101,7 @@ Layout make_layout(const tkv_problem* p) {
     L.pin_words = pin > 0 ? static_cast<int>((pin + 31) / 32) : 0;
   }
   L.pinm = take(BH * static_cast<size_t>(L.pin_words) * 4);
+  L.qs = take((BH + 2 * BK) * kD * 2);  // TKV_F_HOST_Q staging copies of q | k_new | v_new
   L.pl = take(BH * L.nchunks * 4);
   L.po = take(BH * L.nchunks * kD * 4);
   L.total = off;
@@ -214,6 +216,7 @@ int run_prefix(const tkv_problem* p, const void* q, const void* k_cache, const i
   sp.v_dst = static_cast<__nv_bfloat16*>(g_fold.v_cache);
   sp.win_count = g_fold.n_win;
   g_fold = AppendFold{};
+  sp.pdl = g_staged && pdl_enabled() ? 1 : 0;
   TKV_LAUNCH(launch_sample(sp, st));
   if (!sp.no_filter) ++g_launches;  // sample + threshold kernels
 
@@ -512,9 +515,45 @@ int run_head(const tkv_problem* p, const void* q, const void* k_cache, const voi
 
 // The whole layer step: the multi-kernel pipeline (default) or, with TKV_F_FUSED, the fused
 // persistent work-queue kernel (fused.cu).
+int run_layer_dev(const tkv_problem* p, const void* q, const void* k_cache, const void* v_cache,
+                  const int32_t* n_ctx, const int32_t* n_win, int32_t* idx, float* scores,
+                  uint64_t* packed, float* out, int gather, void* ws, const Layout& L, cudaStream_t st);
+
+// TKV_F_HOST_Q: stage q from pinned host memory into the workspace (one small kernel; the
+// sample kernel is PDL-launched behind it), then run the layer on the device copy
 int run_layer(const tkv_problem* p, const void* q, const void* k_cache, const void* v_cache,
               const int32_t* n_ctx, const int32_t* n_win, int32_t* idx, float* scores,
               uint64_t* packed, float* out, int gather, void* ws, const Layout& L, cudaStream_t st) {
+  if (!(p->flags & TKV_F_HOST_Q))
+    return run_layer_dev(p, q, k_cache, v_cache, n_ctx, n_win, idx, scores, packed, out, gather, ws, L, st);
+  const int64_t nq = static_cast<int64_t>(p->batch) * p->n_q_heads * kD * 2 / 16;
+  const int64_t nkv = static_cast<int64_t>(p->batch) * p->n_kv_heads * kD * 2 / 16;
+  uint4* qs = at<uint4>(ws, L.qs);
+  StageParams sp{};
+  sp.src[0] = static_cast<const uint4*>(q);
+  sp.dst[0] = qs;
+  sp.n16[0] = nq;
+  if (g_fold.k_new) {  // decode step: the window append reads the staged rows
+    sp.src[1] = static_cast<const uint4*>(g_fold.k_new);
+    sp.dst[1] = qs + nq;
+    sp.n16[1] = nkv;
+    sp.src[2] = static_cast<const uint4*>(g_fold.v_new);
+    sp.dst[2] = qs + nq + nkv;
+    sp.n16[2] = nkv;
+    g_fold.k_new = qs + nq;
+    g_fold.v_new = qs + nq + nkv;
+  }
+  TKV_LAUNCH(launch_stage(sp, st));
+  g_staged = true;
+  const int rc = run_layer_dev(p, at<uint4>(ws, L.qs), k_cache, v_cache, n_ctx, n_win, idx, scores, packed, out,
+                               gather, ws, L, st);
+  g_staged = false;
+  return rc;
+}
+
+int run_layer_dev(const tkv_problem* p, const void* q, const void* k_cache, const void* v_cache,
+                  const int32_t* n_ctx, const int32_t* n_win, int32_t* idx, float* scores,
+                  uint64_t* packed, float* out, int gather, void* ws, const Layout& L, cudaStream_t st) {
   if (!(p->flags & TKV_F_FUSED)) {
     ScanParams cp;
     SelectParams sl;

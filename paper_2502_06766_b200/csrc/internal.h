@@ -77,7 +77,16 @@ struct SampleParams {
   __nv_bfloat16* k_dst;
   __nv_bfloat16* v_dst;
   int32_t* win_count;
+  int pdl;  // sample_kernel launched behind the q staging kernel (TKV_F_HOST_Q)
 };
+
+// TKV_F_HOST_Q: q copied from pinned host memory into the workspace by one small kernel
+struct StageParams {
+  const uint4* src[3];  // q, and for tkv_topk_decode_step k_new / v_new
+  uint4* dst[3];
+  int64_t n16[3];  // 16-byte words per segment (0 = unused)
+};
+cudaError_t launch_stage(const StageParams& p, cudaStream_t s);
 
 struct ScanParams {
   uint64_t* tl;  // diagnostics timeline (tkv_debug_timeline), nullptr normally

@@ -21,13 +21,35 @@
 // candidates survived (then the true top-k ⊆ candidates, since every top-k key >= the k-th
 // key >= t_h); if not, the head is re-scanned with t_h = 0 (scan_kernel fallback pass).
 #include <math.h>
+
+#include <algorithm>
 #include <stdlib.h>
 
 #include "scan_dev.cuh"
 
 namespace tkv {
 
+// TKV_F_HOST_Q: q from pinned host memory (PCIe reads) into the workspace copy every other
+// kernel reads. The sample kernel behind it is PDL-launched and waits for this grid.
+__global__ void __launch_bounds__(256) stage_kernel(StageParams p) {
+  pdl_trigger();
+  const int64_t n0 = p.n16[0], n1 = n0 + p.n16[1], n2 = n1 + p.n16[2];
+  for (int64_t i = blockIdx.x * 256 + threadIdx.x; i < n2; i += static_cast<int64_t>(gridDim.x) * 256) {
+    const int s = i < n0 ? 0 : (i < n1 ? 1 : 2);
+    const int64_t j = i - (s == 0 ? 0 : (s == 1 ? n0 : n1));
+    p.dst[s][j] = p.src[s][j];
+  }
+}
+
+cudaError_t launch_stage(const StageParams& p, cudaStream_t s) {
+  const int64_t n = p.n16[0] + p.n16[1] + p.n16[2];
+  const int grid = static_cast<int>(std::min<int64_t>((n + 1023) / 1024, 148));
+  stage_kernel<<<grid > 0 ? grid : 1, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
 __global__ void __launch_bounds__(kSampleThreads) sample_kernel(SampleParams p) {
+  pdl_wait();     // only when launched behind stage_kernel (TKV_F_HOST_Q): the staged q
   pdl_trigger();  // the threshold kernel may launch now; it waits for this grid's samples
   if (threadIdx.x == 0) tl_start(p.tl, 0);
   const int seg = blockIdx.y;
@@ -366,8 +388,7 @@ cudaError_t launch_sample(const SampleParams& p, cudaStream_t s) {
   }
   if (!p.no_filter) {
     dim3 grid(kSamples / kSampleThreads, p.B * p.Hkv);
-    sample_kernel<<<grid, kSampleThreads, 0, s>>>(p);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch_pdl(sample_kernel, grid, dim3(kSampleThreads), 0, s, p.pdl != 0, p);
     if (e != cudaSuccess) return e;
   }
   return launch_pdl(threshold_kernel, dim3(p.B * p.Hq), dim3(kThrThreads), 0, s, pdl_enabled() && !p.no_filter, p);

@@ -5,10 +5,11 @@ layer's bf16 K/V cache in HBM (context rows [0, n_ctx) followed by the generatio
 the reference's GenWindow, attention.py:76-104), the libtkv workspace, and pinned host
 staging buffers. `step(q, k_new, v_new)` mirrors one layer of `decode_step`
 (attention.py:203-230): append the token's k/v to the window (attention.py:210), then top-k
-attention for every q head. With host tensors it is the end-to-end path: q/k/v are copied
-host→device and the output device→host; the whole device part of a step (copies, KV append,
-the attention kernels) is captured once into a CUDA graph and replayed, so a step costs one
-graph launch plus the host copies.
+attention for every q head. With host tensors it is the end-to-end path: q/k/v go into pinned
+staging buffers that the call reads itself (TKV_F_HOST_Q: one small kernel stages them on the
+device) and the output is written straight into pinned host memory; the whole device part of
+a step (staging, KV append, the attention kernels) is captured once into a CUDA graph and
+replayed, so a step costs one graph launch plus the host-side copies into the staging buffers.
 """
 
 from __future__ import annotations
@@ -110,21 +111,24 @@ class TopkDecoder:
     def _host_step_body(self, with_kv: bool, with_idx: bool) -> None:
         """Everything a host-I/O step enqueues, reading/writing the pinned staging buffers."""
         b = self._bufs
-        if with_kv:  # one copy: q | k_new | v_new
-            b["in_d"].copy_(b["in_h"], non_blocking=True)
-        else:
-            b["q"].copy_(b["q_h"], non_blocking=True)
-        # the head-finishing CTAs write the output straight into the pinned host buffer (mapped
+        # inputs: read straight from the pinned host staging buffer by the call itself
+        # (TKV_F_HOST_Q: one small kernel stages q, the window append reads k/v over PCIe) —
+        # no H2D copy node; only the unfolded append path copies q | k_new | v_new first.
+        # The head-finishing CTAs write the output straight into the pinned host buffer (mapped
         # memory, 512 B per head): no device->host copy node on the step's critical path
         if with_kv and not self.fold_append:
+            b["in_d"].copy_(b["in_h"], non_blocking=True)
             ops.kv_append(self.k_cache, self.v_cache, b["k_new"], b["v_new"], self.n_win,
                           base=self.n_ctx, advance=True)
+            q_in = b["q"]
+        else:
+            q_in = b["q_h"]
         if with_kv and self.fold_append:  # window append folded into the attention call
-            ops.topk_decode_step(b["q"], b["k_new"], b["v_new"], self.k_cache, self.v_cache, self.n_ctx,
+            ops.topk_decode_step(q_in, b["k_h"], b["v_h"], self.k_cache, self.v_cache, self.n_ctx,
                                  self.n_win, self.k, out=b["out_h"], idx=b["idx"], scores=b["scores"],
                                  workspace=self.ws, **self.kw)
         else:
-            ops.topk_decode_attention(b["q"], self.k_cache, self.v_cache, self.n_ctx, self.k,
+            ops.topk_decode_attention(q_in, self.k_cache, self.v_cache, self.n_ctx, self.k,
                                       n_win=self.n_win, out=b["out_h"], idx=b["idx"], scores=b["scores"],
                                       workspace=self.ws, **self.kw)
         if with_idx:

@@ -45,7 +45,7 @@ def make_problem(B: int, Hq: int, Hkv: int, cache_rows: int, max_ctx: int, k: in
                  sorted: bool = False, no_filter: bool = False, row_offset: int = 0,
                  head_dim: int = HEAD_DIM, fused: bool = False,
                  tc_scan: bool | None = None, parts: int = 0, list_gather: bool = False,
-                 head: bool | None = None) -> _lib.Problem:
+                 head: bool | None = None, host_q: bool = False) -> _lib.Problem:
     p = _lib.Problem()
     p.batch, p.n_q_heads, p.n_kv_heads, p.head_dim = B, Hq, Hkv, head_dim
     p.cache_rows, p.max_ctx, p.k = cache_rows, max_ctx, k
@@ -65,6 +65,8 @@ def make_problem(B: int, Hq: int, Hkv: int, cache_rows: int, max_ctx: int, k: in
         p.flags |= _lib.F_GATHER_LIST
     if head is not None:  # per-head k-th + gather kernel forced on / off (None: automatic, k <= 1024)
         p.flags |= _lib.F_HEAD if head else _lib.F_NO_HEAD
+    if host_q:  # q in pinned host memory, staged on device inside the call
+        p.flags |= _lib.F_HOST_Q
     p.row_offset = row_offset
     return p
 
@@ -102,11 +104,16 @@ def workspace_for(problem: _lib.Problem, device: torch.device) -> Workspace:
     return ws
 
 
-def _check_cuda_bf16(name: str, t: torch.Tensor, ndim: int) -> None:
+def _is_host_pinned(t) -> bool:
+    return isinstance(t, torch.Tensor) and not t.is_cuda and t.is_pinned()
+
+
+def _check_cuda_bf16(name: str, t: torch.Tensor, ndim: int, allow_pinned: bool = False) -> None:
     if not isinstance(t, torch.Tensor):
         raise ShapeError(f"{name} must be a torch tensor")
-    if not t.is_cuda:
-        raise ShapeError(f"{name} must be a CUDA tensor (the B200 path has no CPU fallback)")
+    if not t.is_cuda and not (allow_pinned and t.is_pinned()):
+        raise ShapeError(f"{name} must be a CUDA tensor{' or pinned host memory' if allow_pinned else ''} "
+                         "(the B200 path has no CPU fallback)")
     if t.dtype != torch.bfloat16:
         raise ShapeError(f"{name} must be bfloat16, got {t.dtype}")
     if t.dim() != ndim or not t.is_contiguous():
@@ -133,7 +140,8 @@ class Shapes:
 
 
 def check_shapes(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor | None) -> Shapes:
-    _check_cuda_bf16("q", q, 3)
+    """q may be a pinned host tensor (TKV_F_HOST_Q: staged on device by the call itself)."""
+    _check_cuda_bf16("q", q, 3, allow_pinned=True)
     _check_cuda_bf16("k_cache", k_cache, 4)
     B, Hq, d = q.shape
     if d != HEAD_DIM:
@@ -147,7 +155,7 @@ def check_shapes(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor |
             raise ShapeError("v_cache shape must equal k_cache shape")
     if Hq % Hkv:
         raise ShapeError(f"Hq={Hq} is not a multiple of Hkv={Hkv}")
-    if q.device != k_cache.device:
+    if q.is_cuda and q.device != k_cache.device:
         raise ShapeError("q and k_cache live on different devices")
     return Shapes(B, Hq, Hkv, rows)
 
@@ -168,7 +176,7 @@ def topk_decode_attention(q, k_cache, v_cache, n_ctx, k: int, *, n_win=None, sca
     if k < 1:
         raise InputError("k must be >= 1")
     s = check_shapes(q, k_cache, v_cache)
-    dev = q.device
+    dev = k_cache.device
     n_ctx_t = _as_counts("n_ctx", n_ctx, s.B, dev)
     n_win_t = None if n_win is None else _as_counts("n_win", n_win, s.B, dev)
     if max_ctx is None:
@@ -176,7 +184,8 @@ def topk_decode_attention(q, k_cache, v_cache, n_ctx, k: int, *, n_win=None, sca
     prob = make_problem(s.B, s.Hq, s.Hkv, s.cache_rows, max_ctx, k, pinned_prefix=pinned_prefix,
                         scale=scale, combine=combine, sorted=sorted, no_filter=no_filter,
                         row_offset=row_offset, fused=fused, tc_scan=tc_scan, parts=parts,
-                        list_gather=list_gather, head=head)
+                        list_gather=list_gather, head=head,
+                        host_q=not q.is_cuda)
     ws = workspace or workspace_for(prob, dev)
     out = out if out is not None else torch.empty((s.B, s.Hq, HEAD_DIM), dtype=torch.float32, device=dev)
     idx = idx if idx is not None else torch.empty((s.B, s.Hq, k), dtype=torch.int32, device=dev)
@@ -198,19 +207,20 @@ def topk_decode_step(q, k_new, v_new, k_cache, v_cache, n_ctx, n_win, k: int, *,
     if k < 1:
         raise InputError("k must be >= 1")
     s = check_shapes(q, k_cache, v_cache)
-    dev = q.device
+    dev = k_cache.device
     n_ctx_t = _as_counts("n_ctx", n_ctx, s.B, dev)
     if not (isinstance(n_win, torch.Tensor) and n_win.dtype == torch.int32 and n_win.is_cuda and n_win.numel() == s.B):
         raise ShapeError("n_win must be a device int32 tensor of B counters (advanced in place)")
     for name, t in (("k_new", k_new), ("v_new", v_new)):
-        _check_cuda_bf16(name, t, 3)
+        _check_cuda_bf16(name, t, 3, allow_pinned=True)
         if tuple(t.shape) != (s.B, s.Hkv, HEAD_DIM):
             raise ShapeError(f"{name} must be [B, Hkv, {HEAD_DIM}]")
     if max_ctx is None:
         max_ctx = s.cache_rows if isinstance(n_ctx, torch.Tensor) else int(n_ctx_t.max().item())
     prob = make_problem(s.B, s.Hq, s.Hkv, s.cache_rows, max_ctx, k, pinned_prefix=pinned_prefix,
                         scale=scale, combine=combine, sorted=sorted, fused=fused, tc_scan=tc_scan,
-                        parts=parts, list_gather=list_gather, head=head)
+                        parts=parts, list_gather=list_gather, head=head,
+                        host_q=not q.is_cuda)
     ws = workspace or workspace_for(prob, dev)
     out = out if out is not None else torch.empty((s.B, s.Hq, HEAD_DIM), dtype=torch.float32, device=dev)
     idx = idx if idx is not None else torch.empty((s.B, s.Hq, k), dtype=torch.int32, device=dev)
@@ -230,13 +240,13 @@ def topk_search(q, k_cache, n_ctx, k: int, *, sorted: bool = True, max_ctx: int 
     if k < 1:
         raise InputError("k must be >= 1")
     s = check_shapes(q, k_cache, None)
-    dev = q.device
+    dev = k_cache.device
     n_ctx_t = _as_counts("n_ctx", n_ctx, s.B, dev)
     if max_ctx is None:
         max_ctx = s.cache_rows if isinstance(n_ctx, torch.Tensor) else int(n_ctx_t.max().item())
     prob = make_problem(s.B, s.Hq, s.Hkv, s.cache_rows, max_ctx, k, sorted=sorted,
                         no_filter=no_filter, row_offset=row_offset, fused=fused, tc_scan=tc_scan,
-                        parts=parts, head=head)
+                        parts=parts, head=head, host_q=not q.is_cuda)
     ws = workspace or workspace_for(prob, dev)
     idx = torch.empty((s.B, s.Hq, k), dtype=torch.int32, device=dev)
     scores = torch.empty((s.B, s.Hq, k), dtype=torch.float32, device=dev)

@@ -1,4 +1,3 @@
-timeout 1200 python -m pytest tests -x -q -m gpu 2>&1 | tail -3
-for c in cfg1 cfg2 cfg3; do TKV_PDL=1 timeout 120 python tools/scan_ab.py --config $c --steps 100 2>&1 | tail -1; done
-timeout 120 python tools/timeline.py --config cfg3 2>&1 | head -8
-timeout 300 python tools/e2e_probe.py 2>&1 | head -2
+timeout 1300 python -m pytest tests -x -q -m gpu --timeout 120 > gpurun_out/t.log 2>&1; tail -1 gpurun_out/t.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?
+python bench.py 2>/dev/null | tail -1 > gpurun_out/bench.json; python -c "import json; d=json.load(open('gpurun_out/bench.json')); print(d['value'], d['e2e']['value'], d['roofline']['frac'], d['step_roofline']['frac'], d['clocks'])"

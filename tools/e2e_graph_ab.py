@@ -28,6 +28,7 @@ def main():
     vn = torch.randn((B, 8, 128), device=dev).bfloat16()
     in_h = torch.empty(q.numel() + kn.numel() + vn.numel(), dtype=torch.bfloat16).pin_memory()
     in_d = torch.empty_like(in_h, device=dev)
+    qh, knh, vnh = q.cpu().pin_memory(), kn.cpu().pin_memory(), vn.cpu().pin_memory()
     prob = tkv.ops.make_problem(B, 32, 8, K.shape[2], n, k)
     ws = tkv.Workspace(prob, dev)
     kw = dict(max_ctx=n, idx=idx, scores=sc, workspace=ws)
@@ -52,6 +53,12 @@ def main():
         "attention, out -> pinned host": lambda: attn(out_h),
         "attention + D2H copy node of out": lambda: (attn(), out_h.copy_(out, non_blocking=True)),
         "H2D copy node + attention": lambda: (in_d.copy_(in_h, non_blocking=True), attn()),
+        "attention, q from pinned host (staged in-call)": lambda: tkv.topk_decode_attention(
+            qh, K, V, nc, k, n_win=nw, out=out, **kw),
+        "decode_step, q/k/v from pinned host": lambda: (nw.zero_(), tkv.topk_decode_step(
+            qh, knh, vnh, K, V, nc, nw, k, out=out, **kw)),
+        "decode_step, q/k/v pinned host, out -> pinned host": lambda: (nw.zero_(), tkv.topk_decode_step(
+            qh, knh, vnh, K, V, nc, nw, k, out=out_h, **kw)),
     }
     s = torch.cuda.Stream()
     for name, fn in variants.items():
