@@ -321,8 +321,8 @@ def main():
         d2h = B * HQ * D * 4
         e2e = {"value": round(e2e_us, 2), "unit": "us", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "steps": e2e_steps,
-               "path": "TopkDecoder.step: host q + new k/v row -> pinned staging -> CUDA-graph replay "
-                       "(a staging kernel reads q/k/v from pinned host memory, KV append, top-k "
+               "path": "TopkDecoder.step(q, k_new, v_new) with pinned host tensors -> CUDA-graph replay "
+                       "(a staging kernel reads q/k/v in place from pinned host memory, KV append, top-k "
                        "attention writing out into pinned host memory) -> host sync, every step"}
 
     if rank != 0:

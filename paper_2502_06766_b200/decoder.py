@@ -108,9 +108,11 @@ class TopkDecoder:
                                   **self.kw)
         return b["out"], b["idx"], b["scores"]
 
-    def _host_step_body(self, with_kv: bool, with_idx: bool) -> None:
-        """Everything a host-I/O step enqueues, reading/writing the pinned staging buffers."""
+    def _host_step_body(self, with_kv: bool, with_idx: bool, src=None) -> None:
+        """Everything a host-I/O step enqueues, reading/writing the pinned staging buffers (or,
+        with src = (q, k_new, v_new), the caller's own pinned tensors)."""
         b = self._bufs
+        q_h, k_h, v_h = src if src is not None else (b["q_h"], b["k_h"], b["v_h"])
         # inputs: read straight from the pinned host staging buffer by the call itself
         # (TKV_F_HOST_Q: one small kernel stages q, the window append reads k/v over PCIe) —
         # no H2D copy node; only the unfolded append path copies q | k_new | v_new first.
@@ -122,9 +124,9 @@ class TopkDecoder:
                           base=self.n_ctx, advance=True)
             q_in = b["q"]
         else:
-            q_in = b["q_h"]
+            q_in = q_h
         if with_kv and self.fold_append:  # window append folded into the attention call
-            ops.topk_decode_step(q_in, b["k_h"], b["v_h"], self.k_cache, self.v_cache, self.n_ctx,
+            ops.topk_decode_step(q_in, k_h, v_h, self.k_cache, self.v_cache, self.n_ctx,
                                  self.n_win, self.k, out=b["out_h"], idx=b["idx"], scores=b["scores"],
                                  workspace=self.ws, **self.kw)
         else:
@@ -146,30 +148,50 @@ class TopkDecoder:
             out, idx, _ = self.attend(q)
             return (out, idx) if return_idx else out
         b = self._bufs
-        b["q_h"].copy_(q)
         with_kv = k_new is not None
-        if with_kv:
-            b["k_h"].copy_(k_new)
-            b["v_h"].copy_(v_new)
-        key = (with_kv, return_idx)
+        Hq = q.shape[1]
+        # pinned bf16 inputs of the right shape are read in place by the call (no host copy);
+        # the step's graph is then keyed by their addresses (a few cached)
+        direct = ((self.fold_append or not with_kv) and self._pinned_ok(q, (self.B, Hq, ops.HEAD_DIM))
+                  and (not with_kv or (self._pinned_ok(k_new, (self.B, self.Hkv, ops.HEAD_DIM))
+                                       and self._pinned_ok(v_new, (self.B, self.Hkv, ops.HEAD_DIM)))))
+        if direct:
+            src = (q, k_new, v_new)
+            key = (with_kv, return_idx, q.data_ptr(), k_new.data_ptr() if with_kv else 0,
+                   v_new.data_ptr() if with_kv else 0)
+        else:
+            b["q_h"].copy_(q)
+            if with_kv:
+                b["k_h"].copy_(k_new)
+                b["v_h"].copy_(v_new)
+            src, key = None, (with_kv, return_idx)
         if self.use_graph:
             g = self._graphs.get(key)
             if g is None:
-                g = self._capture(key)
+                g = self._capture(key, src)
             g.replay()
         else:
-            self._host_step_body(with_kv, return_idx)
+            self._host_step_body(with_kv, return_idx, src)
         torch.cuda.current_stream(self.device).synchronize()
         return (b["out_h"], b["idx_h"]) if return_idx else b["out_h"]
 
-    def _capture(self, key) -> torch.cuda.CUDAGraph:
-        with_kv, with_idx = key
+    @staticmethod
+    def _pinned_ok(t, shape) -> bool:
+        return (isinstance(t, torch.Tensor) and not t.is_cuda and t.is_pinned() and t.dtype == torch.bfloat16
+                and t.is_contiguous() and tuple(t.shape) == shape)
+
+    def _capture(self, key, src=None) -> torch.cuda.CUDAGraph:
+        with_kv, with_idx = key[0], key[1]
+        if src is not None:  # graphs bound to caller tensors: keep only the most recent few
+            direct = [kk for kk in self._graphs if len(kk) > 2]
+            for kk in direct[:max(0, len(direct) - 7)]:
+                del self._graphs[kk]
         stream = torch.cuda.current_stream(self.device)
         # capture on a side stream; one eager run first so every lazy attribute/occupancy
         # query inside libtkv has happened before capture. The eager run's KV append is undone
         # by rewinding n_win, so the capture does not double-append.
         saved = self.n_win.clone()
-        self._host_step_body(with_kv, with_idx)
+        self._host_step_body(with_kv, with_idx, src)
         self.n_win.copy_(saved)
         stream.synchronize()
         g = torch.cuda.CUDAGraph()
@@ -177,7 +199,7 @@ class TopkDecoder:
         side.wait_stream(stream)
         with torch.cuda.stream(side):
             with torch.cuda.graph(g, stream=side):
-                self._host_step_body(with_kv, with_idx)
+                self._host_step_body(with_kv, with_idx, src)
         stream.wait_stream(side)
         self._graphs[key] = g
         return g

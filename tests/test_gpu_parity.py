@@ -345,6 +345,37 @@ def test_decoder_host_io_steps(cuda, use_graph, variant):
                pinned=variant.get("pinned_prefix", 0))
 
 
+@pytest.mark.parametrize("fresh_tensors", [False, True])
+def test_decoder_pinned_inputs_read_in_place(cuda, fresh_tensors):
+    """Pinned bf16 host inputs are read in place by the step (no staging copy; the CUDA graph is
+    keyed by their addresses): reused buffers refilled per step, or fresh tensors per step."""
+    from paper_2502_06766_b200 import TopkDecoder
+
+    rng = np.random.default_rng(78)
+    B, Hq, Hkv, N, k, steps = 2, 8, 2, 6000, 64, 4
+    _, K, V = _make(rng, B, Hq, Hkv, N + 16)
+    dec = TopkDecoder(_dev(K, cuda), _dev(V, cuda), N, k, max_ctx=N)
+    bufs = [torch.empty(s, dtype=torch.bfloat16).pin_memory() for s in ((B, Hq, 128), (B, Hkv, 128), (B, Hkv, 128))]
+    Kref, Vref = K.copy(), V.copy()
+    for s in range(steps):
+        arrs = [bf16_normal(rng, t.shape) for t in bufs]
+        if fresh_tensors:
+            ins = [torch.from_numpy(a).to(torch.bfloat16).pin_memory() for a in arrs]
+        else:
+            for t, a in zip(bufs, arrs):
+                t.copy_(torch.from_numpy(a).to(torch.bfloat16))
+            ins = bufs
+        out, idx = dec.step(*ins)
+        q, kn, vn = arrs
+        Kref[:, :, N + s] = kn
+        Vref[:, :, N + s] = vn
+        _check(q, Kref, Vref, [N] * B, k, out, idx, torch.zeros(B, Hq, k) + torch.from_numpy(
+            np.stack([[O.ip_scores_all(Kref[b, h // 4, :N], q[b, h])[idx.numpy()[b, h]] for h in range(Hq)]
+                      for b in range(B)]).astype(np.float32)), n_win=[s + 1] * B)
+    n_direct = sum(1 for kk in dec._graphs if len(kk) > 2)
+    assert (1 <= n_direct <= steps) if fresh_tensors else n_direct == 1  # pinned blocks may be reused
+
+
 def test_decode_step_folds_append(cuda):
     """tkv_topk_decode_step (append folded into the attention call) equals kv_append followed
     by topk_decode_attention, step after step, including n_win advancing on device."""

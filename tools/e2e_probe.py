@@ -33,6 +33,10 @@ def main():
 
     print(f"e2e step (q, k, v host -> out host): {timeit(lambda: dec.step(qh, kh, vh, return_idx=False)):.1f} us")
     print(f"e2e step (q host only):              {timeit(lambda: dec.step(qh, return_idx=False)):.1f} us")
+    qp, kp, vp = qh.pin_memory(), kh.pin_memory(), vh.pin_memory()
+    print(f"e2e step, pinned q/k/v read in place: {timeit(lambda: dec.step(qp, kp, vp, return_idx=False)):.1f} us")
+    print(f"e2e step (q, k, v host, again):      {timeit(lambda: dec.step(qh, kh, vh, return_idx=False)):.1f} us")
+    print(f"e2e step, pinned again:              {timeit(lambda: dec.step(qp, kp, vp, return_idx=False)):.1f} us")
     g = dec._graphs[(True, False)]
     print(f"graph replay + sync only:            {timeit(lambda: (g.replay(), torch.cuda.current_stream().synchronize())):.1f} us")
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
