@@ -13,7 +13,8 @@ NAMES = ["sample", "threshold", "threshold past wait", "scan", "scan epilogue pa
          "head: threshold found", "head: rows compacted", "head: V gathered"]
 PHASES = ["head CTA: start→params", "→hist+bucket", "→pass 1 (max, bucket members)", "→T",
           "→pads/meta + barriers", "→compaction loop", "→out_cnt reservation", "→V gather loop", "→ids written",
-          "→partial slot written", "→finished (last CTA)"]
+          "→partial slot written", "→finished (last CTA)",
+          "kth CTA: start→hist+bucket", "→slice scan", "→ticket (last CTA)", "→T written (last CTA)"]
 
 
 def main():
