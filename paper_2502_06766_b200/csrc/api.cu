@@ -488,8 +488,8 @@ int run_head(const tkv_problem* p, const void* q, const void* k_cache, const voi
   a.out = out;
   a.gather = gather;
   a.partial_only = 0;
-  // CTAs per head: enough heads x CTAs to cover the SMs (the gather is per-SM bound), at
-  // least ~256 selected rows per CTA, at most one partial slot each
+  // CTAs per head: enough heads x CTAs to cover the SMs in one wave (the gather is per-SM
+  // bound), at least ~128 selected rows per CTA, at most one partial slot each
   static const int sms = [] {
     int dev = 0, v = 0;
     cudaGetDevice(&dev);
@@ -501,7 +501,8 @@ int run_head(const tkv_problem* p, const void* q, const void* k_cache, const voi
     return e ? atoi(e) : 0;
   }();
   int C = env_c > 0 ? env_c : sms / nbh;  // one wave: the kernel holds one CTA per SM
-  if (env_c <= 0 && C > (p->k + 255) / 256) C = (p->k + 255) / 256;
+  const int c_rows = (p->k + 127) / 128 > 2 ? (p->k + 127) / 128 : 2;  // >= 128 rows per CTA, >= 2 CTAs
+  if (env_c <= 0 && C > c_rows) C = c_rows;  // cfg1 (k = 256): C = 2 37.0 us, C = 1 40.6-43.3 us
   if (C > 8) C = 8;
   if (C > L.nchunks) C = L.nchunks;
   hp.ctas_per_head = C < 1 ? 1 : C;
