@@ -212,6 +212,9 @@ def main():
     ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--narrow", type=float, default=None,
+                    help="N>1: narrow candidate exchange, each rank sends its top ceil(C*k/N) "
+                         "(exactness checked per step, full-k fallback)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     cfg = CONFIGS[args.config]
@@ -262,9 +265,14 @@ def main():
         stages = tkv.CudaStages(B, HQ, HKV, rows, n_local, k, row_offset=lo, device=dev)
         n_ctx = torch.full((B,), n_local, dtype=torch.int32, device=dev)
         gathered = torch.empty(world * B * HQ * k, dtype=torch.int64, device=dev)
+        narrow = None
+        if args.narrow:
+            narrow = tkv.CudaStages(B, HQ, HKV, rows, n_local, tkv.narrow_k(k, world, args.narrow),
+                                    row_offset=lo, device=dev)
 
         def step():
-            tkv.sharded_topk_attention(stages, q, K, V, n_ctx, None, gathered=gathered)
+            tkv.sharded_topk_attention(stages, q, K, V, n_ctx, None, gathered=gathered,
+                                       narrow=narrow)
 
     for _ in range(warm):
         step()
@@ -344,7 +352,7 @@ def main():
         "config": {"workload": args.config, "batch": B, "n_ctx": N, "k": k, "Hq": HQ, "Hkv": HKV,
                    "head_dim": D, "parallelism": f"token-shard{world}" if world > 1 else "single",
                    "l2": "inputs larger than L2 (K cache %.2f GB per GPU, L2 126 MB): no flush" % (kbytes / 1e9),
-                   "seed": args.seed},
+                   "seed": args.seed, **({"narrow_c": args.narrow} if world > 1 and args.narrow else {})},
         "roofline": {"bound": "hbm", "kernel": SCAN_DESC[SCAN_KERNEL],
                      "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": scan_traffic(args.config, world),

@@ -26,7 +26,7 @@ from .errors import (
     TopkKvError,
 )
 from .ops import Workspace, kv_append, topk_decode_attention, topk_decode_step, topk_search
-from .sharded import CudaStages, shard_range, sharded_topk_attention
+from .sharded import CudaStages, narrow_k, shard_range, sharded_topk_attention
 
 __version__ = "0.1.0"
 
@@ -35,6 +35,6 @@ __all__ = [
     "FormatError", "InfeasibleBudgetError", "InputError", "LayerBudget", "MipsIndex", "ShapeError",
     "TierAccounting", "TopKResult", "TopkDecoder", "TopkKvError", "VALUE_ROW_BYTES", "Workspace",
     "build_index", "entropy_budget", "knn_search", "kv_append", "linear_budget", "parse_budget_spec",
-    "recall_at_k", "shard_range", "uniform_budget",
+    "narrow_k", "recall_at_k", "shard_range", "uniform_budget",
     "sharded_topk_attention", "topk_attend", "topk_decode_attention", "topk_decode_step", "topk_search",
 ]

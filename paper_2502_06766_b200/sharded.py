@@ -76,17 +76,85 @@ class CudaStages:
         return self.out
 
 
+_U64_TO_I64 = torch.iinfo(torch.int64).min  # x ^ this maps unsigned order onto signed order
+
+
+def narrow_k(k: int, world: int, c: float = 1.5) -> int:
+    """Candidates each rank sends in the narrow exchange: ceil(c·k/world), at most k (SURVEY
+    §8e mitigation; c ≈ 1.25–2). With i.i.d. relevance each shard holds ≈ k/world of the
+    global top-k, so c·k/world covers it with margin."""
+    if world < 1 or k < 1 or c <= 0:
+        raise InputError(f"bad narrow_k arguments k={k} world={world} c={c}")
+    return min(k, -(-int(c * k) // world))
+
+
+def narrow_exchange_exact(gathered: torch.Tensor, world: int, k: int, kk: int) -> torch.Tensor:
+    """Per (b, q head): is the global top-k over the narrow gathered lists exact?
+
+    gathered: [world * BH * kk] packed composites (uint64 bit patterns in int64; 0 = empty
+    slot), rank-major. A rank whose list is full may have withheld rows; each withheld row's
+    composite is below that rank's smallest sent one (its floor t'_g — composites are unique).
+    The merged k-th composite is ≥ T = max over full ranks of t'_g iff at least k gathered
+    candidates are ≥ T; then no withheld row can enter the top-k and the result is exact.
+    Conservative (a rank with exactly kk rows counts as full), never optimistic. Every rank
+    evaluates this on identical data, so all ranks take the same branch without a collective."""
+    g = (gathered ^ _U64_TO_I64).view(world, -1, kk)                 # [world, BH, kk]
+    empty = torch.tensor(_U64_TO_I64, dtype=torch.int64, device=gathered.device)
+    full = (g != empty).all(dim=2)                                   # [world, BH]
+    floor = torch.where(full, g.min(dim=2).values, empty)             # [world, BH]
+    T = floor.max(dim=0).values                                       # [BH]
+    count = (g >= T.view(1, -1, 1)).sum(dim=(0, 2))                   # [BH]
+    return (~full.any(dim=0)) | (count >= k)
+
+
+def widen_candidates(small: torch.Tensor, world: int, kk: int, k: int,
+                     out: torch.Tensor | None = None) -> torch.Tensor:
+    """[world][BH][kk] narrow lists → the [world][BH][k] layout tkv_shard_merge reads, the
+    unsent slots zero (= empty, as a shard with fewer than k rows writes them)."""
+    bh = small.numel() // (world * kk)
+    if out is None:
+        out = torch.empty(world * bh * k, dtype=small.dtype, device=small.device)
+    wide = out.view(world, bh, k)
+    wide[:, :, kk:].zero_()
+    wide[:, :, :kk] = small.view(world, bh, kk)
+    return out
+
+
 def sharded_topk_attention(stages, q, k_shard, v_shard, n_ctx_local, n_win=None, *, group=None,
-                           gathered: torch.Tensor | None = None):
+                           gathered: torch.Tensor | None = None, narrow=None,
+                           stats: dict | None = None):
     """One layer's exact top-k attention with the context sharded by token range across the
     ranks of `group`. Every rank passes its shard (rows [row_offset, row_offset + n_local) in
     rows [0, n_local) of k_shard/v_shard, window rows after them, replicated) and receives the
-    full result: (out [B, Hq, 128] f32, idx [B, Hq, k] global ids, scores)."""
+    full result: (out [B, Hq, 128] f32, idx [B, Hq, k] global ids, scores).
+
+    narrow: optional stages object of the same layout built with k' = narrow_k(k, world) < k
+    (only its `candidates` and `k` are used). Each rank then all-gathers only its local
+    top-k' (traffic ÷ k/k'); if `narrow_exchange_exact` fails for any head (skewed data: one
+    shard holds more than k' of the global top-k) every rank re-runs the full-k exchange, so
+    the result is always exact. Costs one device→host read of the exactness flag. `stats`,
+    when given, receives {"narrow": bool used, "narrow_exact": bool}."""
     world = dist.get_world_size(group)
+    if narrow is not None and narrow.k < stages.k:
+        cand = narrow.candidates(q, k_shard, n_ctx_local)
+        small = torch.empty(world * cand.numel(), dtype=cand.dtype, device=cand.device)
+        dist.all_gather_into_tensor(small, cand, group=group)
+        exact = bool(narrow_exchange_exact(small, world, stages.k, narrow.k).all())
+        if stats is not None:
+            stats.update(narrow=True, narrow_exact=exact)
+        if exact:
+            gathered = widen_candidates(small, world, narrow.k, stages.k, gathered)
+            return _finish(stages, world, gathered, q, k_shard, v_shard, n_ctx_local, n_win, group)
+    elif stats is not None:
+        stats.update(narrow=False, narrow_exact=None)
     cand = stages.candidates(q, k_shard, n_ctx_local)
     if gathered is None:
         gathered = torch.empty(world * cand.numel(), dtype=cand.dtype, device=cand.device)
     dist.all_gather_into_tensor(gathered, cand, group=group)
+    return _finish(stages, world, gathered, q, k_shard, v_shard, n_ctx_local, n_win, group)
+
+
+def _finish(stages, world, gathered, q, k_shard, v_shard, n_ctx_local, n_win, group):
     idx, scores = stages.merge(gathered, world)
     partial = stages.partial_attend(q, k_shard, v_shard, n_ctx_local, idx, scores)
     dist.all_reduce(partial, op=dist.ReduceOp.SUM, group=group)

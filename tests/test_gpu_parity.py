@@ -259,6 +259,41 @@ def test_sharded_stages_emulated(cuda):
             assert float((o - out1).abs().max()) < 1e-5
 
 
+@pytest.mark.parametrize("skew", [False, True])
+def test_sharded_narrow_exchange_emulated(cuda, skew):
+    """Narrow candidate exchange on one GPU (collectives emulated): each shard sends its exact
+    local top-k' (k' = narrow_k(k, G)); when the exactness rule holds the merged ids equal the
+    unsharded ones, and skewed data (the relevant rows in shard 0) trips the rule."""
+    from paper_2502_06766_b200 import CudaStages, narrow_k, shard_range, topk_decode_attention
+    from paper_2502_06766_b200.sharded import narrow_exchange_exact, widen_candidates
+
+    rng = np.random.default_rng(23)
+    B, Hq, Hkv, N, k, G = 1, 32, 8, 40000, 512, 4
+    q, K, V = _make(rng, B, Hq, Hkv, N)
+    if skew:
+        K[:, :, :N // G] *= 4.0
+    qd, Kd, Vd = _dev(q, cuda), _dev(K, cuda), _dev(V, cuda)
+    _, idx1, _ = topk_decode_attention(qd, Kd, Vd, [N], k)
+    kk = narrow_k(k, G)
+    narrow, full, shards = [], [], []
+    for g in range(G):
+        lo, hi = shard_range(N, G, g)
+        narrow.append(CudaStages(B, Hq, Hkv, hi - lo, hi - lo, kk, row_offset=lo, device=cuda))
+        full.append(CudaStages(B, Hq, Hkv, hi - lo, hi - lo, k, row_offset=lo, device=cuda))
+        shards.append((Kd[:, :, lo:hi].contiguous(),
+                       torch.tensor([hi - lo], dtype=torch.int32, device=cuda)))
+    small = torch.cat([st.candidates(qd, s[0], s[1]).clone() for st, s in zip(narrow, shards)])
+    exact = narrow_exchange_exact(small, G, k, kk)
+    assert bool(exact.all()) == (not skew)
+    if skew:
+        return
+    idx, _ = full[0].merge(widen_candidates(small, G, kk, k), G)
+    torch.cuda.synchronize()
+    a, b = idx.cpu().numpy(), idx1.cpu().numpy()
+    for h in range(Hq):
+        assert set(a[0, h].tolist()) == set(b[0, h].tolist())
+
+
 @pytest.mark.slow
 def test_cfg3_full_size(cuda):
     """cfg3: N = 1M, k = 16384 (1.6 %), Llama-3-8B head shape — full oracle parity on all 32
