@@ -212,9 +212,9 @@ def main():
     ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--narrow", type=float, default=None,
+    ap.add_argument("--narrow", type=float, default=1.5,
                     help="N>1: narrow candidate exchange, each rank sends its top ceil(C*k/N) "
-                         "(exactness checked per step, full-k fallback)")
+                         "(exactness checked per step, full-k fallback); 0 = full-k exchange")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     cfg = CONFIGS[args.config]

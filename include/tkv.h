@@ -163,6 +163,19 @@ int tkv_shard_candidates(const tkv_problem* p, const void* q, const void* k_cach
 int tkv_shard_merge(const tkv_problem* p, const uint64_t* gathered, int32_t n_shards,
                     int32_t* idx, float* scores, void* workspace, size_t workspace_bytes,
                     void* stream);
+/*
+ * Narrow candidate exchange (sharded.py narrow_exchange_exact): every shard sent only its
+ * local top-list_len (list_len <= k), gathered[n_shards][B*Hq*list_len].
+ *   tkv_shard_narrow_check: ok[B*Hq] = 1 where the global top-k over the lists is provably
+ *     exact (no withheld row can enter it), else 0 — the caller then re-runs the full-k
+ *     exchange. tkv_shard_merge_lists: tkv_shard_merge over lists of list_len.
+ * (Replaces no reference interface: the reference is single-process.)
+ */
+int tkv_shard_narrow_check(const tkv_problem* p, const uint64_t* gathered, int32_t n_shards,
+                           int32_t list_len, int32_t* ok, void* stream);
+int tkv_shard_merge_lists(const tkv_problem* p, const uint64_t* gathered, int32_t n_shards,
+                          int32_t list_len, int32_t* idx, float* scores, void* workspace,
+                          size_t workspace_bytes, void* stream);
 int tkv_shard_partial(const tkv_problem* p, const void* q, const void* k_cache,
                       const void* v_cache, const int32_t* n_ctx, const int32_t* idx,
                       const float* scores, float* partial, void* workspace,

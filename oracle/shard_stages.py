@@ -42,8 +42,9 @@ class OracleStages:
                 out[b * self.Hq + h, :len(top)] = top
         return torch.from_numpy(out.reshape(-1).view(np.int64).copy())
 
-    def merge(self, gathered, n_shards):
-        g = gathered.numpy().view(np.uint64).reshape(n_shards, self.B * self.Hq, self.k)
+    def merge(self, gathered, n_shards, list_len=None):
+        L = self.k if list_len is None else list_len
+        g = gathered.numpy().view(np.uint64).reshape(n_shards, self.B * self.Hq, L)
         self.idx = np.full((self.B, self.Hq, self.k), -1, dtype=np.int32)
         self.scores = np.full((self.B, self.Hq, self.k), -np.inf, dtype=np.float32)
         self.meta = {}

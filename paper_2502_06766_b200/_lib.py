@@ -31,6 +31,8 @@ EXPORTS = (
     "tkv_kv_append",
     "tkv_shard_candidates",
     "tkv_shard_merge",
+    "tkv_shard_narrow_check",
+    "tkv_shard_merge_lists",
     "tkv_shard_partial",
     "tkv_shard_finalize",
     "tkv_last_launch_count",
@@ -99,6 +101,11 @@ _SIG = {
     "tkv_shard_candidates": ([ctypes.POINTER(Problem), _P, _P, _P, _P, _P, ctypes.c_size_t, _P], _I),
     "tkv_shard_merge": (
         [ctypes.POINTER(Problem), _P, ctypes.c_int32, _P, _P, _P, ctypes.c_size_t, _P], _I),
+    "tkv_shard_narrow_check": (
+        [ctypes.POINTER(Problem), _P, ctypes.c_int32, ctypes.c_int32, _P, _P], _I),
+    "tkv_shard_merge_lists": (
+        [ctypes.POINTER(Problem), _P, ctypes.c_int32, ctypes.c_int32, _P, _P, _P, ctypes.c_size_t,
+         _P], _I),
     "tkv_shard_partial": (
         [ctypes.POINTER(Problem), _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P], _I),
     "tkv_shard_finalize": (

@@ -863,6 +863,27 @@ int tkv_shard_candidates(const tkv_problem* p, const void* q, const void* k_cach
 
 int tkv_shard_merge(const tkv_problem* p, const uint64_t* gathered, int32_t n_shards, int32_t* idx,
                     float* scores, void* ws, size_t ws_bytes, void* stream) {
+  TRY(validate(p));
+  return tkv_shard_merge_lists(p, gathered, n_shards, p->k, idx, scores, ws, ws_bytes, stream);
+}
+
+int tkv_shard_narrow_check(const tkv_problem* p, const uint64_t* gathered, int32_t n_shards,
+                           int32_t list_len, int32_t* ok, void* stream) {
+  g_launches = 0;
+  TRY(validate(p));
+  TRY(check_ptr(gathered, "gathered", 8));
+  TRY(check_ptr(ok, "ok", 4));
+  if (n_shards < 1) return fail(TKV_EBADSHAPE, "n_shards must be >= 1");
+  if (list_len < 1 || list_len > p->k) return fail(TKV_EBADK, "list_len must be in [1, k]");
+  const int nbh = p->batch * p->n_q_heads;
+  TKV_LAUNCH(launch_narrow_check(gathered, n_shards, list_len, nbh, p->k, ok,
+                                 static_cast<cudaStream_t>(stream)));
+  return TKV_OK;
+}
+
+int tkv_shard_merge_lists(const tkv_problem* p, const uint64_t* gathered, int32_t n_shards,
+                          int32_t list_len, int32_t* idx, float* scores, void* ws, size_t ws_bytes,
+                          void* stream) {
   g_launches = 0;
   TRY(validate(p));
   Layout L;
@@ -871,13 +892,15 @@ int tkv_shard_merge(const tkv_problem* p, const uint64_t* gathered, int32_t n_sh
   TRY(check_ptr(idx, "idx", 4));
   TRY(check_ptr(scores, "scores", 4));
   if (n_shards < 1) return fail(TKV_EBADSHAPE, "n_shards must be >= 1");
-  // gathered is [n_shards][B*Hq*k] (all_gather_into_tensor layout), read in place.
+  if (list_len < 1 || list_len > p->k) return fail(TKV_EBADK, "list_len must be in [1, k]");
+  // gathered is [n_shards][B*Hq*list_len] (all_gather_into_tensor layout), read in place.
   const int G = p->n_q_heads / p->n_kv_heads;
   SelectParams sl{};
   sl.src = gathered;
-  sl.src_stride = static_cast<int64_t>(n_shards) * p->k;
-  sl.shard_stride = static_cast<int64_t>(p->batch) * p->n_q_heads * p->k;
-  sl.src_fixed = static_cast<int64_t>(n_shards) * p->k;
+  sl.merge_len = list_len;
+  sl.src_stride = static_cast<int64_t>(n_shards) * list_len;
+  sl.shard_stride = static_cast<int64_t>(p->batch) * p->n_q_heads * list_len;
+  sl.src_fixed = static_cast<int64_t>(n_shards) * list_len;
   sl.B = p->batch;
   sl.Hq = p->n_q_heads;
   sl.Hkv = p->n_kv_heads;

@@ -111,8 +111,9 @@ struct SelectParams {
   uint64_t* tl;  // diagnostics timeline (tkv_debug_timeline), nullptr normally
   const uint64_t* src;   // candidates: src + bh*src_stride (main/fallback)
   int64_t src_stride;    // merge: element i of head bh is
-  int64_t shard_stride;  //   src[(i / k) * shard_stride + bh * k + i % k]
-  int64_t src_fixed;     // merge: candidates per head (n_shards * k)
+  int64_t shard_stride;  //   src[(i / L) * shard_stride + bh * L + i % L], L = merge_len
+  int64_t src_fixed;     // merge: candidates per head (n_shards * merge_len)
+  int64_t merge_len;     // merge: list length per shard and head (k, or k' < k: narrow exchange)
   int B, Hq, Hkv, G, k;
   const int32_t* n_ctx;  // kb = min(k, n_ctx[b]) (main/fallback); merge: min(k, #valid)
   int32_t* idx;          // [B*Hq*k]
@@ -260,6 +261,8 @@ cudaError_t launch_scan_fma(const ScanParams& p, cudaStream_t s);
 bool scan_tc_supported(const ScanParams& p);
 void scan_launch_shape(const ScanParams& p, int* grid, int* smem_bytes);
 cudaError_t launch_select(const SelectParams& p, cudaStream_t s);
+cudaError_t launch_narrow_check(const uint64_t* gathered, int n_shards, int list_len, int nbh, int k,
+                                int32_t* ok, cudaStream_t s);
 cudaError_t launch_kth(const SelectParams& p, cudaStream_t s);
 cudaError_t launch_head_topk(const HeadParams& p, cudaStream_t s);
 cudaError_t launch_attend_cand(const AttendParams& p, cudaStream_t s);

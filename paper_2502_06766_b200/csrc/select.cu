@@ -75,14 +75,14 @@ __global__ void __launch_bounds__(SNT) select_kernel(SelectParams p) {
   if (p.pass == kPassFallback && p.hs.flag_fail[bh] == 0u) return;
 
   const bool merge = p.pass == kPassMerge;
-  const uint64_t* src = merge ? p.src + static_cast<int64_t>(bh) * p.k
+  const uint64_t* src = merge ? p.src + static_cast<int64_t>(bh) * p.merge_len
                               : p.src + static_cast<int64_t>(bh) * p.src_stride;
   int64_t n = merge ? p.src_fixed : static_cast<int64_t>(p.hs.cand_cnt[bh]);
   if (!merge && n > p.src_stride) n = p.src_stride;
   auto load = [&](int64_t i) -> uint64_t {
     if (!merge) return src[i];
-    const int64_t s = i / p.k;
-    return src[s * p.shard_stride + (i - s * p.k)];
+    const int64_t s = i / p.merge_len;
+    return src[s * p.shard_stride + (i - s * p.merge_len)];
   };
 
   // ---- histogram of the candidate keys: from the scan (main/fallback) or built here (merge)
@@ -936,6 +936,56 @@ cudaError_t launch_sort(const SortParams& p, int nbh, cudaStream_t s) {
     attr = true;
   }
   sort_kernel<<<nbh, SNT, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+// Narrow-exchange exactness rule (paper_2502_06766_b200/sharded.py narrow_exchange_exact), one
+// CTA per head: floor_g = the smallest composite of shard g's list (0 when the list has an
+// empty slot, i.e. the shard sent everything it has); T = max floor_g; exact iff T == 0 or at
+// least k gathered composites are >= T (then no withheld row can enter the global top-k).
+__global__ void __launch_bounds__(256) narrow_check_kernel(const uint64_t* __restrict__ g, int n_shards,
+                                                           int L, int nbh, int k, int32_t* ok) {
+  __shared__ unsigned long long s_min[8];
+  __shared__ uint32_t s_cnt[8];
+  const int bh = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  unsigned long long T = 0ull;
+  for (int s = 0; s < n_shards; ++s) {
+    const uint64_t* src = g + (static_cast<int64_t>(s) * nbh + bh) * L;
+    unsigned long long m = ~0ull;
+    for (int i = tid; i < L; i += 256) m = min(m, static_cast<unsigned long long>(src[i]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(kFull, m, o));
+    if (lane == 0) s_min[warp] = m;
+    __syncthreads();
+    unsigned long long f = s_min[0];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) f = min(f, s_min[w]);
+    T = max(T, f);  // f == 0: the shard's list has an empty slot, nothing withheld
+    __syncthreads();
+  }
+  if (T == 0ull) {
+    if (tid == 0) ok[bh] = 1;
+    return;
+  }
+  uint32_t c = 0;
+  for (int s = 0; s < n_shards; ++s) {
+    const uint64_t* src = g + (static_cast<int64_t>(s) * nbh + bh) * L;
+    for (int i = tid; i < L; i += 256) c += static_cast<unsigned long long>(src[i]) >= T ? 1u : 0u;
+  }
+  c = warp_sum(c);
+  if (lane == 0) s_cnt[warp] = c;
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t t = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += s_cnt[w];
+    ok[bh] = t >= static_cast<uint32_t>(k) ? 1 : 0;
+  }
+}
+
+cudaError_t launch_narrow_check(const uint64_t* gathered, int n_shards, int list_len, int nbh, int k,
+                                int32_t* ok, cudaStream_t s) {
+  narrow_check_kernel<<<nbh, 256, 0, s>>>(gathered, n_shards, list_len, nbh, k, ok);
   return cudaGetLastError();
 }
 

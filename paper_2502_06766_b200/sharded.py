@@ -58,10 +58,20 @@ class CudaStages:
                   ops._vp(n_ctx), ops._vp(self.cand), self.ws.ptr, self.ws.nbytes, self._s())
         return self.cand
 
-    def merge(self, gathered, n_shards: int):
-        _lib.call("tkv_shard_merge", ctypes.byref(self.prob), ops._vp(gathered), n_shards,
-                  ops._vp(self.idx), ops._vp(self.scores), self.ws.ptr, self.ws.nbytes, self._s())
+    def merge(self, gathered, n_shards: int, list_len: int | None = None):
+        """Exact global top-k over n_shards lists of list_len (default k) candidates per head."""
+        _lib.call("tkv_shard_merge_lists", ctypes.byref(self.prob), ops._vp(gathered), n_shards,
+                  self.k if list_len is None else list_len, ops._vp(self.idx),
+                  ops._vp(self.scores), self.ws.ptr, self.ws.nbytes, self._s())
         return self.idx, self.scores
+
+    def narrow_exact(self, gathered, n_shards: int, list_len: int) -> torch.Tensor:
+        """Per-head exactness of a narrow exchange (int32 [B*Hq], 1 = exact); device kernel
+        for narrow_exchange_exact."""
+        ok = torch.empty(self.B * self.Hq, dtype=torch.int32, device=self.device)
+        _lib.call("tkv_shard_narrow_check", ctypes.byref(self.prob), ops._vp(gathered), n_shards,
+                  list_len, ops._vp(ok), self._s())
+        return ok
 
     def partial_attend(self, q, k_cache, v_cache, n_ctx, idx, scores):
         _lib.call("tkv_shard_partial", ctypes.byref(self.prob), ops._vp(q), ops._vp(k_cache),
@@ -107,19 +117,6 @@ def narrow_exchange_exact(gathered: torch.Tensor, world: int, k: int, kk: int) -
     return (~full.any(dim=0)) | (count >= k)
 
 
-def widen_candidates(small: torch.Tensor, world: int, kk: int, k: int,
-                     out: torch.Tensor | None = None) -> torch.Tensor:
-    """[world][BH][kk] narrow lists → the [world][BH][k] layout tkv_shard_merge reads, the
-    unsent slots zero (= empty, as a shard with fewer than k rows writes them)."""
-    bh = small.numel() // (world * kk)
-    if out is None:
-        out = torch.empty(world * bh * k, dtype=small.dtype, device=small.device)
-    wide = out.view(world, bh, k)
-    wide[:, :, kk:].zero_()
-    wide[:, :, :kk] = small.view(world, bh, kk)
-    return out
-
-
 def sharded_topk_attention(stages, q, k_shard, v_shard, n_ctx_local, n_win=None, *, group=None,
                            gathered: torch.Tensor | None = None, narrow=None,
                            stats: dict | None = None):
@@ -139,12 +136,16 @@ def sharded_topk_attention(stages, q, k_shard, v_shard, n_ctx_local, n_win=None,
         cand = narrow.candidates(q, k_shard, n_ctx_local)
         small = torch.empty(world * cand.numel(), dtype=cand.dtype, device=cand.device)
         dist.all_gather_into_tensor(small, cand, group=group)
-        exact = bool(narrow_exchange_exact(small, world, stages.k, narrow.k).all())
+        if hasattr(stages, "narrow_exact"):
+            ok = stages.narrow_exact(small, world, narrow.k)
+        else:
+            ok = narrow_exchange_exact(small, world, stages.k, narrow.k)
+        exact = bool(ok.all())
         if stats is not None:
             stats.update(narrow=True, narrow_exact=exact)
         if exact:
-            gathered = widen_candidates(small, world, narrow.k, stages.k, gathered)
-            return _finish(stages, world, gathered, q, k_shard, v_shard, n_ctx_local, n_win, group)
+            return _finish(stages, world, small, q, k_shard, v_shard, n_ctx_local, n_win, group,
+                           list_len=narrow.k)
     elif stats is not None:
         stats.update(narrow=False, narrow_exact=None)
     cand = stages.candidates(q, k_shard, n_ctx_local)
@@ -154,8 +155,9 @@ def sharded_topk_attention(stages, q, k_shard, v_shard, n_ctx_local, n_win=None,
     return _finish(stages, world, gathered, q, k_shard, v_shard, n_ctx_local, n_win, group)
 
 
-def _finish(stages, world, gathered, q, k_shard, v_shard, n_ctx_local, n_win, group):
-    idx, scores = stages.merge(gathered, world)
+def _finish(stages, world, gathered, q, k_shard, v_shard, n_ctx_local, n_win, group,
+            list_len=None):
+    idx, scores = stages.merge(gathered, world, list_len)
     partial = stages.partial_attend(q, k_shard, v_shard, n_ctx_local, idx, scores)
     dist.all_reduce(partial, op=dist.ReduceOp.SUM, group=group)
     out = stages.finalize(q, k_shard, v_shard, n_ctx_local, n_win, partial)

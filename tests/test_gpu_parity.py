@@ -265,7 +265,7 @@ def test_sharded_narrow_exchange_emulated(cuda, skew):
     local top-k' (k' = narrow_k(k, G)); when the exactness rule holds the merged ids equal the
     unsharded ones, and skewed data (the relevant rows in shard 0) trips the rule."""
     from paper_2502_06766_b200 import CudaStages, narrow_k, shard_range, topk_decode_attention
-    from paper_2502_06766_b200.sharded import narrow_exchange_exact, widen_candidates
+    from paper_2502_06766_b200.sharded import narrow_exchange_exact
 
     rng = np.random.default_rng(23)
     B, Hq, Hkv, N, k, G = 1, 32, 8, 40000, 512, 4
@@ -284,10 +284,12 @@ def test_sharded_narrow_exchange_emulated(cuda, skew):
                        torch.tensor([hi - lo], dtype=torch.int32, device=cuda)))
     small = torch.cat([st.candidates(qd, s[0], s[1]).clone() for st, s in zip(narrow, shards)])
     exact = narrow_exchange_exact(small, G, k, kk)
+    ok = full[0].narrow_exact(small, G, kk)  # the rule's device kernel
+    assert (ok != 0).tolist() == exact.tolist()
     assert bool(exact.all()) == (not skew)
     if skew:
         return
-    idx, _ = full[0].merge(widen_candidates(small, G, kk, k), G)
+    idx, _ = full[0].merge(small, G, kk)  # merge over the narrow lists, read in place
     torch.cuda.synchronize()
     a, b = idx.cpu().numpy(), idx1.cpu().numpy()
     for h in range(Hq):
