@@ -17,7 +17,9 @@ no L2 flush is needed between steps.
 
 Multi-GPU (torchrun, N > 1): the context is sharded by token range (strong scaling: the 1M
 rows are split across ranks); candidates all-gather + partial all-reduce over NCCL; value =
-max over ranks of the per-step device time.
+max over ranks of the per-step device time. By default each rank sends only its top
+ceil(1.5*k/N) candidates (narrow exchange, exactness checked on the device every step, full-k
+fallback when it fails); `--narrow 0` all-gathers k per rank.
 `--impl reference`: times the reference algorithm's CPU port on rank 0 (others exit 0).
 """
 
