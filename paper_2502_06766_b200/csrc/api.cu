@@ -875,6 +875,8 @@ int tkv_shard_narrow_check(const tkv_problem* p, const uint64_t* gathered, int32
   TRY(check_ptr(ok, "ok", 4));
   if (n_shards < 1) return fail(TKV_EBADSHAPE, "n_shards must be >= 1");
   if (list_len < 1 || list_len > p->k) return fail(TKV_EBADK, "list_len must be in [1, k]");
+  if (static_cast<int64_t>(n_shards) * list_len > (1ll << 30))
+    return fail(TKV_EBADSHAPE, "n_shards * list_len too large");
   const int nbh = p->batch * p->n_q_heads;
   TKV_LAUNCH(launch_narrow_check(gathered, n_shards, list_len, nbh, p->k, ok,
                                  static_cast<cudaStream_t>(stream)));

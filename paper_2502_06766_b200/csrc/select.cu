@@ -945,23 +945,33 @@ cudaError_t launch_sort(const SortParams& p, int nbh, cudaStream_t s) {
 // least k gathered composites are >= T (then no withheld row can enter the global top-k).
 __global__ void __launch_bounds__(256) narrow_check_kernel(const uint64_t* __restrict__ g, int n_shards,
                                                            int L, int nbh, int k, int32_t* ok) {
-  __shared__ unsigned long long s_min[8];
+  // shard by shard, every thread keeping UNR loads in flight; one block reduction per shard
+  __shared__ unsigned long long s_min[2][8];
   __shared__ uint32_t s_cnt[8];
   const int bh = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int UNR = 8;
   unsigned long long T = 0ull;
   for (int s = 0; s < n_shards; ++s) {
     const uint64_t* src = g + (static_cast<int64_t>(s) * nbh + bh) * L;
     unsigned long long m = ~0ull;
-    for (int i = tid; i < L; i += 256) m = min(m, static_cast<unsigned long long>(src[i]));
+    for (int base = 0; base < L; base += 256 * UNR) {
+      unsigned long long v[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int i = base + u * 256 + tid;
+        v[u] = i < L ? src[i] : ~0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) m = min(m, v[u]);
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(kFull, m, o));
-    if (lane == 0) s_min[warp] = m;
+    if (lane == 0) s_min[s & 1][warp] = m;  // double-buffered: one barrier per shard
     __syncthreads();
-    unsigned long long f = s_min[0];
+    unsigned long long f = s_min[s & 1][0];
 #pragma unroll
-    for (int w = 1; w < 8; ++w) f = min(f, s_min[w]);
+    for (int w = 1; w < 8; ++w) f = min(f, s_min[s & 1][w]);
     T = max(T, f);  // f == 0: the shard's list has an empty slot, nothing withheld
-    __syncthreads();
   }
   if (T == 0ull) {
     if (tid == 0) ok[bh] = 1;
@@ -970,7 +980,16 @@ __global__ void __launch_bounds__(256) narrow_check_kernel(const uint64_t* __res
   uint32_t c = 0;
   for (int s = 0; s < n_shards; ++s) {
     const uint64_t* src = g + (static_cast<int64_t>(s) * nbh + bh) * L;
-    for (int i = tid; i < L; i += 256) c += static_cast<unsigned long long>(src[i]) >= T ? 1u : 0u;
+    for (int base = 0; base < L; base += 256 * UNR) {
+      unsigned long long v[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int i = base + u * 256 + tid;
+        v[u] = i < L ? src[i] : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) c += v[u] >= T ? 1u : 0u;
+    }
   }
   c = warp_sum(c);
   if (lane == 0) s_cnt[warp] = c;
