@@ -8,12 +8,14 @@ The K cache (2.15 GB) is far larger than L2 (126 MB), so every step streams it f
 no L2 flush is needed between steps.
 
   value     µs per layer-step, inputs resident in HBM, CUDA events over K steps
-  e2e       same metric through TopkDecoder.step() with pinned HOST buffers: H2D of q and
-            the new token's k/v rows, KV append, attention, D2H of out, every step (the whole
-            device part replayed as one CUDA graph; the host syncs on the result each step)
+  e2e       same metric through TopkDecoder.step() -> (out, idx) with pinned HOST buffers:
+            q and the new token's k/v rows read from host memory, KV append, attention, out and
+            the selected ids back in host memory, every step (the whole device part replayed as
+            one CUDA graph; the host syncs on the result each step); `out_only` = same without ids
   roofline  dominant kernel (key scan): algorithmic K bytes / scan-kernel time (events
             recorded around the scan launch on its stream, every timed step)
-  cpu_baseline  the oracle port (oracle/) on the host cores, bounded sample (1 KV group)
+  cpu_baseline  the reference algorithm's C port (oracle/) on the host cores: one full
+            layer-step on every host thread, plus a single-core sample (1 KV group, scaled)
 
 Multi-GPU (torchrun, N > 1): the context is sharded by token range (strong scaling: the 1M
 rows are split across ranks); candidates all-gather + partial all-reduce over NCCL; value =
@@ -160,46 +162,104 @@ def make_inputs(cfg, rows, seed, device, rank_lo=0, rank_hi=None):
     return q, K, V, n
 
 
-def cpu_baseline(cfg, seconds_budget=20.0, threads=None):
-    """The reference algorithm's CPU port (oracle/tkv_oracle.c: strict left-to-right f64 scan,
-    _flat_topk selection, f64 joint softmax — test infrastructure, timed here as the baseline)
-    on the host cores, on a bounded sample: one KV group (Hq/Hkv = 4 q heads) of one batch
-    entry at the workload's N and k, scaled to a full layer-step (x Hkv groups x B)."""
+def _cpu_inputs(cfg, kv_groups: int, seed: int = 1234):
+    """Standard-normal K/V/q rounded to bf16 values (what the GPU arm sees), f32 storage,
+    generated in row chunks so the 1M-row cache needs no f64 temporaries."""
     import numpy as np
 
     from oracle import oracle as O
 
-    N, k, B = cfg["N"], cfg["k"], cfg["B"]
+    B, N = cfg["B"], cfg["N"]
     G = HQ // HKV
-    rng = np.random.default_rng(1234)
-    K = O.to_bf16_f32(rng.standard_normal((1, 1, N, D), dtype=np.float32))
-    V = O.to_bf16_f32(rng.standard_normal((1, 1, N, D), dtype=np.float32))
-    q = O.to_bf16_f32(rng.standard_normal((1, G, D), dtype=np.float32))
-    t = threads or O.c_lib().tkv_oracle_max_threads()
+    rng = np.random.default_rng(seed)
+    K = np.empty((B, kv_groups, N, D), dtype=np.float32)
+    V = np.empty_like(K)
+    step = 1 << 16
+    for b in range(B):
+        for g in range(kv_groups):
+            for r0 in range(0, N, step):
+                r1 = min(N, r0 + step)
+                K[b, g, r0:r1] = O.to_bf16_f32(rng.standard_normal((r1 - r0, D), dtype=np.float32))
+                V[b, g, r0:r1] = O.to_bf16_f32(rng.standard_normal((r1 - r0, D), dtype=np.float32))
+    q = O.to_bf16_f32(rng.standard_normal((B, kv_groups * G, D), dtype=np.float32))
+    return q, K, V
+
+
+def _time_port(q, K, V, N, k, threads, reps_budget_s, max_reps):
+    """Repeated oracle/tkv_oracle.c layer calls; returns the per-call seconds."""
+    from oracle import oracle as O
+
     times = []
-    t_end = time.perf_counter() + seconds_budget
-    while not times or (time.perf_counter() < t_end and len(times) < 3):
+    t_end = time.perf_counter() + reps_budget_s
+    while not times or (time.perf_counter() < t_end and len(times) < max_reps):
         t0 = time.perf_counter()
-        O.c_decode_layer(q, K, V, [N], k, threads=t)
+        O.c_decode_layer(q, K, V, [N] * q.shape[0], k, threads=threads)
         times.append(time.perf_counter() - t0)
-    us = min(times) * HKV * B * 1e6
-    return {"value": round(us, 1), "unit": "us", "cores": t, "kind": "port",
-            "sample": f"1 KV group ({G} q heads) of 1 batch entry at N={N}, k={k}: oracle/tkv_oracle.c "
-                      f"(C port of ann_kernels.py:31-47, ann.py:154-167, attention.py:107-167), {t} OpenMP "
-                      f"threads, best of {len(times)}, scaled x{HKV * B} to one layer-step"}
+    return times
+
+
+PORT_DESC = ("oracle/tkv_oracle.c (C port of ann_kernels.py:31-47, ann.py:154-167, "
+             "attention.py:107-167: strict left-to-right f64 scan, _flat_topk, f64 joint softmax)")
+
+
+def cpu_baseline(cfg, seconds_budget=20.0):
+    """The reference algorithm's CPU port on the host cores (test infrastructure, timed as the
+    baseline): ONE FULL layer-step of the workload (every KV group and batch entry, all Hq
+    heads, all host threads), plus a single-core sample of one KV group (scaled to a layer-step
+    and labelled as such) for the per-core comparison BASELINE.md §3 plans."""
+    from oracle import oracle as O
+
+    N, k, B = cfg["N"], cfg["k"], cfg["B"]
+    t = int(O.c_lib().tkv_oracle_max_threads())
+    q, K, V = _cpu_inputs(cfg, HKV)
+    full = _time_port(q, K, V, N, k, t, seconds_budget / 2, 3)
+    G = HQ // HKV
+    one = _time_port(q[:1, :G].copy(), K[:1, :1], V[:1, :1], N, k, 1, seconds_budget / 4, 2)
+    return {"value": round(min(full) * 1e6, 1), "unit": "us", "cores": t, "kind": "port",
+            "sample": f"full layer-step (B={B}, Hq={HQ}, Hkv={HKV}, N={N}, k={k}) through {PORT_DESC}, "
+                      f"{t} OpenMP threads (one head per thread), best of {len(full)}",
+            "single_core": {"value": round(min(one) * HKV * B * 1e6, 1), "unit": "us", "cores": 1,
+                            "sample": f"1 KV group ({G} q heads) of 1 batch entry on 1 thread, best of "
+                                      f"{len(one)}, scaled x{HKV * B} to one layer-step"}}
+
+
+def our_config(args, cfg, world=1):
+    B, N, k = cfg["B"], cfg["N"], cfg["k"]
+    c = {"workload": args.config, "batch": B, "n_ctx": N, "k": k, "Hq": HQ, "Hkv": HKV, "head_dim": D,
+         "parallelism": f"token-shard{world}" if world > 1 else "single",
+         "l2": "inputs larger than L2 (K cache %.2f GB per GPU, L2 126 MB): no flush" % (B * N * HKV * D * 2 / world / 1e9),
+         "seed": args.seed}
+    if world > 1 and args.narrow:
+        c["narrow_c"] = args.narrow
+    return c
 
 
 def run_reference(args, cfg):
+    """--impl reference: the reference's algorithm on the host CPU (its CPU port; the reference
+    itself is Python/Numba with no compiled sources to build), timed on exactly
+    this arm's workload: every step is one FULL layer-step, repeated for up to ~2 minutes."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    cb = cpu_baseline(cfg, seconds_budget=max(5.0, 2.0 * args.steps))
+    from oracle import oracle as O
+
+    N, k, B = cfg["N"], cfg["k"], cfg["B"]
+    t = int(O.c_lib().tkv_oracle_max_threads())
+    q, K, V = _cpu_inputs(cfg, HKV)
+    # warm-up (page in the caches, OpenMP pool), then the timed steps
+    warm = _time_port(q, K, V, N, k, t, 0.0, 1)
+    per = warm[0]
+    steps = max(1, min(args.steps, int(120.0 / max(per, 1e-3))))
+    times = _time_port(q, K, V, N, k, t, 1e9, steps)
+    us = sum(times) / len(times) * 1e6
+    cb = {"value": round(us, 1), "unit": "us", "cores": t, "kind": "port",
+          "sample": f"{len(times)} full layer-steps (B={B}, Hq={HQ}, Hkv={HKV}, N={N}, k={k}) through {PORT_DESC}, "
+                    f"{t} OpenMP threads, mean"}
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "us",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": cb["value"] / 1e3, "higher_is_better": False, "scaling": "strong",
+            "n_gpus": args.gpus, "steps": len(times), "steps_requested": args.steps, "warmup": 1,
+            "ms_per_step": round(us / 1e3, 3), "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.config, **cfg, "Hq": HQ, "Hkv": HKV, "d": D},
-            "cpu_baseline": cb,
+            "config": our_config(args, cfg, 1), "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": "us", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
@@ -316,24 +376,31 @@ def main():
         qh = q.cpu().pin_memory()
         kn = torch.randn((B, HKV, D)).to(torch.bfloat16).pin_memory()
         vn = torch.randn((B, HKV, D)).to(torch.bfloat16).pin_memory()
-        e2e_steps = min(steps, WINDOW_CAP - warm - 1)
-        for _ in range(warm):
-            dec.step(qh, kn, vn, return_idx=False)
-        torch.cuda.synchronize()
-        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a0.record(stream)
-        for _ in range(e2e_steps):
-            dec.step(qh, kn, vn, return_idx=False)
-        a1.record(stream)
-        torch.cuda.synchronize()
-        e2e_us = a0.elapsed_time(a1) / e2e_steps * 1e3
+        e2e_steps = max(1, min(steps, (WINDOW_CAP - 2 * warm - 2) // 2))
+
+        def e2e_run(return_idx):
+            for _ in range(warm):
+                dec.step(qh, kn, vn, return_idx=return_idx)
+            torch.cuda.synchronize()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            for _ in range(e2e_steps):
+                dec.step(qh, kn, vn, return_idx=return_idx)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            return a0.elapsed_time(a1) / e2e_steps * 1e3
+
+        e2e_idx_us = e2e_run(True)
+        e2e_out_us = e2e_run(False)
         h2d = qh.numel() * 2 + kn.numel() * 2 + vn.numel() * 2
-        d2h = B * HQ * D * 4
-        e2e = {"value": round(e2e_us, 2), "unit": "us", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "steps": e2e_steps,
-               "path": "TopkDecoder.step(q, k_new, v_new) with pinned host tensors -> CUDA-graph replay "
-                       "(a staging kernel reads q/k/v in place from pinned host memory, KV append, top-k "
-                       "attention writing out into pinned host memory) -> host sync, every step"}
+        e2e = {"value": round(e2e_idx_us, 2), "unit": "us", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": B * HQ * D * 4 + B * HQ * k * 4, "steps": e2e_steps,
+               "path": "TopkDecoder.step(q, k_new, v_new) -> (out, idx) with pinned host tensors: CUDA-graph "
+                       "replay (a staging kernel reads q/k/v in place from pinned host memory, KV append, "
+                       "top-k attention writing out into pinned host memory, D2H copy of the selected ids) "
+                       "-> host sync, every step",
+               "out_only": {"value": round(e2e_out_us, 2), "d2h_bytes_per_step": B * HQ * D * 4,
+                            "path": "the same step with return_idx=False (ids stay on the device)"}}
 
     if rank != 0:
         if world > 1:
@@ -351,10 +418,7 @@ def main():
         "metric": METRIC, "value": round(ms * 1e3, 2), "unit": "us", "n_gpus": world,
         "steps": steps, "warmup": warm, "ms_per_step": round(ms, 5), "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": args.config, "batch": B, "n_ctx": N, "k": k, "Hq": HQ, "Hkv": HKV,
-                   "head_dim": D, "parallelism": f"token-shard{world}" if world > 1 else "single",
-                   "l2": "inputs larger than L2 (K cache %.2f GB per GPU, L2 126 MB): no flush" % (kbytes / 1e9),
-                   "seed": args.seed, **({"narrow_c": args.narrow} if world > 1 and args.narrow else {})},
+        "config": our_config(args, cfg, world),
         "roofline": {"bound": "hbm", "kernel": SCAN_DESC[SCAN_KERNEL],
                      "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": scan_traffic(args.config, world),

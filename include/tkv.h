@@ -60,7 +60,7 @@ extern "C" {
 /* flags */
 #define TKV_F_SORTED 1u    /* idx/scores ordered score-desc, id-asc (TopKResult order, ann.py:166) */
 #define TKV_F_NO_FILTER 2u /* disable the sampled-threshold pre-filter (emit every score)       */
-#define TKV_F_FUSED 4u     /* run the layer step as one persistent work-queue kernel (fused.cu)   */
+/* flag bit 4u is reserved (was a persistent single-kernel layer step, measured slower; removed) */
 #define TKV_F_PARTS(n) ((uint32_t)(n) << 8) /* pipeline parts: scan of part i+1 overlaps the  \
                               k-th selection + V gather of part i (1..15; 0 = automatic)         */
 #define TKV_F_PARTS_MASK 0xF00u
@@ -200,7 +200,7 @@ int tkv_last_launch_count(void);
  * Measurement hook: when both events are non-NULL (cudaEvent_t as void*), subsequent compute
  * calls on this thread record `start` / `stop` on their stream immediately before / after the
  * dominant kernel launch (the key-scan kernel: scan_tc_kernel, or scan_kernel with
- * TKV_F_SCAN_HMMA; with TKV_F_FUSED the fused layer-step kernel),
+ * TKV_F_SCAN_HMMA),
  * so a caller can time it with CUDA events on the stream it runs on. Pass NULLs to disable.
  */
 int tkv_profile_scan_events(void* start, void* stop);
@@ -218,12 +218,6 @@ int tkv_profile_scan_events(void* start, void* stop);
 #define TKV_TIMELINE_WORDS 64
 int tkv_debug_timeline(void* buf);
 
-/*
- * Measurement hook: with a non-NULL device buffer of n_items × 4 uint64, the fused layer-step
- * kernel records, per work item index i < n_items, {start ns, end ns, type << 32 | cta,
- * a << 32 | b} (%globaltimer). NULL disables. Diagnostic only.
- */
-int tkv_debug_trace(void* buf, uint32_t n_items);
 
 #ifdef __cplusplus
 }

@@ -38,7 +38,6 @@ EXPORTS = (
     "tkv_last_launch_count",
     "tkv_profile_scan_events",
     "tkv_debug_timeline",
-    "tkv_debug_trace",
     "tkv_convert_rows_f32",
 )
 
@@ -46,7 +45,6 @@ COMBINE_JOINT = 0
 COMBINE_ADDITIVE = 1
 F_SORTED = 1
 F_NO_FILTER = 2
-F_FUSED = 4
 F_SCAN_HMMA = 8
 F_PARTS_SHIFT = 8  # TKV_F_PARTS(n): bits 8..11
 F_GATHER_LIST = 16
@@ -86,7 +84,6 @@ _SIG = {
     "tkv_last_launch_count": ([], _I),
     "tkv_profile_scan_events": ([_P, _P], _I),
     "tkv_debug_timeline": ([_P], _I),
-    "tkv_debug_trace": ([_P, ctypes.c_uint32], _I),
     "tkv_convert_rows_f32": ([_P, ctypes.c_int64, ctypes.c_int32, _P, _P], _I),
     "tkv_workspace_bytes": ([ctypes.POINTER(Problem), ctypes.POINTER(ctypes.c_size_t)], _I),
     "tkv_workspace_init": ([ctypes.POINTER(Problem), _P, ctypes.c_size_t, _P], _I),

@@ -22,10 +22,8 @@ namespace {
 thread_local std::string g_err;
 thread_local int g_launches = 0;
 thread_local cudaEvent_t g_scan_start = nullptr, g_scan_stop = nullptr;
-thread_local uint64_t* g_trace = nullptr;
 thread_local uint64_t* g_tl = nullptr;
 thread_local bool g_staged = false;  // q staged by stage_kernel in this call (TKV_F_HOST_Q)
-thread_local uint32_t g_trace_cap = 0;
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -47,7 +45,7 @@ int fail(int code, const char* fmt, ...) {
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct Layout {
-  size_t ticket_g, ticket_k, flag, gflag, fctl, fbl, ctrl_end;
+  size_t ticket_g, ticket_k, flag, gflag, fbl, ctrl_end;
   size_t maxc, bktc, bkt, outc;
   size_t cnt, thr, hshift, hist, mmax, mkth, mkb, samp, cand, sidx, sscore, pl, po, pinm, qs, total;
   int pin_words;
@@ -69,7 +67,6 @@ Layout make_layout(const tkv_problem* p) {
   L.ticket_k = take(BH * 4);
   L.flag = take(BH * 4);
   L.gflag = take(BK * 4);
-  L.fctl = take(static_cast<size_t>(fused_ctl_words(static_cast<int>(BK), static_cast<int>(BH))) * 4);
   L.fbl = take(4 * kMaxParts);
   L.ctrl_end = off;
   L.cnt = take(BH * 4);
@@ -263,13 +260,7 @@ int run_prefix(const tkv_problem* p, const void* q, const void* k_cache, const i
 
 // Programmatic dependent launch between sample → threshold → scan → k-th (default on;
 // TKV_PDL=0 disables it, e.g. for A/B timing).
-bool tkv::pdl_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("TKV_PDL");
-    return !(e && atoi(e) == 0);
-  }();
-  return on;
-}
+bool tkv::pdl_enabled() { return diag_env("TKV_PDL", 1) != 0; }
 
 namespace {
 
@@ -282,11 +273,8 @@ int run_scan_part(const tkv_problem* p, ScanParams cp, int64_t s0, int64_t s1, c
   cp.seg_begin = s0;
   cp.seg_count = s1 - s0;
   cp.pdl = pdl ? 1 : 0;
-  static const bool fma = [] {  // the north star's CUDA-core FMA scan, for the ncu A/B
-    const char* e = getenv("TKV_SCAN");
-    return e && std::string(e) == "fma";
-  }();
-  if (fma)
+  // the north star's CUDA-core FMA scan, kept for the ncu A/B (TKV_DIAG builds: TKV_SCAN_FMA=1)
+  if (diag_env("TKV_SCAN_FMA", 0))
     TKV_LAUNCH(launch_scan_fma(cp, st));
   else if (use_tc_scan(p, cp))
     TKV_LAUNCH(launch_scan_tc(cp, st));
@@ -319,10 +307,7 @@ int run_kth_part(const tkv_problem* p, ScanParams cp, SelectParams sl, int64_t s
 // the k-th selection and the V gather of part i run on a side stream beside it (both fit on
 // an SM next to the tcgen05 scan CTA). One part when the scan is too short to hide them.
 int pipeline_parts(const tkv_problem* p, bool tc) {
-  static const int env = [] {
-    const char* e = getenv("TKV_PARTS");
-    return e ? atoi(e) : 0;
-  }();
+  const int env = diag_env("TKV_PARTS", 0);
   const int64_t nseg = static_cast<int64_t>(p->batch) * p->n_kv_heads;
   int P;
   const int forced = static_cast<int>((p->flags & TKV_F_PARTS_MASK) >> 8);
@@ -334,7 +319,7 @@ int pipeline_parts(const tkv_problem* p, bool tc) {
     // measured on cfg3 (2.1 GB of keys): each extra scan launch costs ~12 us of fill/drain, more
     // than the overlap hides, so one part; four parts only for very long scans (cfg5: 8.6 GB)
     const double kbytes = static_cast<double>(nseg) * static_cast<double>(p->max_ctx) * kD * 2;
-    P = tc && !(p->flags & TKV_F_FUSED) && kbytes >= 4e9 ? 4 : 1;
+    P = tc && kbytes >= 4e9 ? 4 : 1;
   }
   if (P > nseg) P = static_cast<int>(nseg);
   if (P > kMaxParts) P = kMaxParts;
@@ -423,10 +408,7 @@ int run_emit(const tkv_problem* p, const void* q, const void* k_cache, const voi
   // rows) a filter pass writing idx/scores followed by a streaming gather over those lists —
   // measured faster from ~1M selected rows per step (cfg5 family), slower below (cfg1-3).
   // TKV_LIST_GATHER=0/1 forces either.
-  static const int list_env = [] {
-    const char* e = getenv("TKV_LIST_GATHER");
-    return e ? atoi(e) : -1;
-  }();
+  const int list_env = diag_env("TKV_LIST_GATHER", -1);
   const double sel_rows = static_cast<double>(bh_count) * p->k;
   const bool list_gather =
       (p->flags & TKV_F_GATHER_LIST) ? true : (list_env >= 0 ? list_env != 0 : sel_rows >= 1.0e6);
@@ -453,10 +435,7 @@ int run_emit(const tkv_problem* p, const void* q, const void* k_cache, const voi
 // forces either (any k: the selected rows stream through a kHeadCap-row buffer); the
 // TKV_F_HEAD / TKV_F_NO_HEAD flags force it per call.
 bool use_head_topk(const tkv_problem* p, int gather) {
-  static const int env = [] {
-    const char* e = getenv("TKV_HEAD_TOPK");
-    return e ? atoi(e) : -1;
-  }();
+  const int env = diag_env("TKV_HEAD_TOPK", -1);
   if (p->flags & TKV_F_HEAD) return true;
   if ((p->flags & (TKV_F_GATHER_LIST | TKV_F_NO_HEAD)) || env == 0) return false;
   if (env > 0) return true;
@@ -490,16 +469,8 @@ int run_head(const tkv_problem* p, const void* q, const void* k_cache, const voi
   a.partial_only = 0;
   // CTAs per head: enough heads x CTAs to cover the SMs in one wave (the gather is per-SM
   // bound), at least ~128 selected rows per CTA, at most one partial slot each
-  static const int sms = [] {
-    int dev = 0, v = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v > 0 ? v : 148;
-  }();
-  static const int env_c = [] {
-    const char* e = getenv("TKV_HEAD_CTAS");
-    return e ? atoi(e) : 0;
-  }();
+  const int sms = device_sm_count();
+  const int env_c = diag_env("TKV_HEAD_CTAS", 0);
   int C = env_c > 0 ? env_c : sms / nbh;  // one wave: the kernel holds one CTA per SM
   const int c_rows = (p->k + 127) / 128 > 2 ? (p->k + 127) / 128 : 2;  // >= 128 rows per CTA, >= 2 CTAs
   if (env_c <= 0 && C > c_rows) C = c_rows;  // cfg1 (k = 256): C = 2 37.0 us, C = 1 40.6-43.3 us
@@ -514,8 +485,7 @@ int run_head(const tkv_problem* p, const void* q, const void* k_cache, const voi
   return TKV_OK;
 }
 
-// The whole layer step: the multi-kernel pipeline (default) or, with TKV_F_FUSED, the fused
-// persistent work-queue kernel (fused.cu).
+// The whole layer step (multi-kernel pipeline).
 int run_layer_dev(const tkv_problem* p, const void* q, const void* k_cache, const void* v_cache,
                   const int32_t* n_ctx, const int32_t* n_win, int32_t* idx, float* scores,
                   uint64_t* packed, float* out, int gather, void* ws, const Layout& L, cudaStream_t st);
@@ -555,7 +525,7 @@ int run_layer(const tkv_problem* p, const void* q, const void* k_cache, const vo
 int run_layer_dev(const tkv_problem* p, const void* q, const void* k_cache, const void* v_cache,
                   const int32_t* n_ctx, const int32_t* n_win, int32_t* idx, float* scores,
                   uint64_t* packed, float* out, int gather, void* ws, const Layout& L, cudaStream_t st) {
-  if (!(p->flags & TKV_F_FUSED)) {
+  {
     ScanParams cp;
     SelectParams sl;
     TRY(run_prefix(p, q, k_cache, n_ctx, ws, L, st, &cp, &sl));
@@ -578,10 +548,7 @@ int run_layer_dev(const tkv_problem* p, const void* q, const void* k_cache, cons
     }
     PipeRes* r = nullptr;
     TRY(pipe_res(&r));
-    static const bool serial = [] {  // diagnostics: split scans, no overlap
-      const char* e = getenv("TKV_PIPE_SERIAL");
-      return e && atoi(e) != 0;
-    }();
+    const bool serial = diag_env("TKV_PIPE_SERIAL", 0) != 0;  // diagnostics: split scans, no overlap
     if (serial) {
       if (prof) cudaEventRecord(g_scan_start, st);
       for (int part = 0; part < P; ++part)
@@ -597,10 +564,7 @@ int run_layer_dev(const tkv_problem* p, const void* q, const void* k_cache, cons
     }
     // part boundaries: even, or (TKV_PARTS_TAIL=1) a last part of one eighth of the groups so
     // less k-th + gather work remains after the final scan
-    static const bool tail_split = [] {
-      const char* e = getenv("TKV_PARTS_TAIL");
-      return e && atoi(e) != 0;
-    }();
+    const bool tail_split = diag_env("TKV_PARTS_TAIL", 0) != 0;
     auto bound = [&](int part) -> int64_t {
       if (!tail_split || P < 2) return nseg * part / P;
       int64_t last = nseg / 8;
@@ -609,10 +573,7 @@ int run_layer_dev(const tkv_problem* p, const void* q, const void* k_cache, cons
       return (nseg - last) * part / (P - 1);
     };
     if (prof) cudaEventRecord(g_scan_start, st);
-    static const bool chain = [] {  // experiments: PDL-chained part scans
-      const char* e = getenv("TKV_PARTS_CHAIN");
-      return !(e && atoi(e) == 0);
-    }();
+    const bool chain = diag_env("TKV_PARTS_CHAIN", 1) != 0;  // experiments: PDL-chained part scans
     for (int part = 0; part < P; ++part) {
       const int64_t s0 = bound(part), s1 = bound(part + 1);
       // the first part's scan overlaps sample / threshold (PDL); later parts' CTAs take over SMs
@@ -635,61 +596,6 @@ int run_layer_dev(const tkv_problem* p, const void* q, const void* k_cache, cons
       return fail(TKV_ECUDA, "pipeline join failed");
     return TKV_OK;
   }
-  FusedParams f{};
-  f.a = make_attend(p, q, k_cache, v_cache, n_ctx, n_win, idx, scores, ws, L);
-  f.a.idx_out = idx;
-  f.a.scores_out = scores;
-  f.a.packed_out = packed;
-  f.a.out = out;
-  f.a.gather = gather;
-  f.a.partial_only = 0;
-  f.hs = head_state(ws, L);
-  f.samp = at<uint32_t>(ws, L.samp);
-  f.ctl = at<uint32_t>(ws, L.fctl);
-  f.max_ctx = p->max_ctx;
-  f.no_filter = (p->flags & TKV_F_NO_FILTER) ? 1 : 0;
-  f.NS = f.no_filter ? 0 : kSamples / kSampleThreads;
-  const int NG = p->batch * p->n_kv_heads, NH = p->batch * p->n_q_heads;
-  int sms = 148, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = 2 * sms;
-  // tile size: 1024 rows per scan item when there are enough items to balance, else smaller
-  static const int tile_env = [] {
-    const char* e = getenv("TKV_TILE_ITERS");
-    return e ? atoi(e) : 0;
-  }();
-  f.tile_iters = tile_env > 0 ? tile_env : 8;
-  while (tile_env <= 0 && f.tile_iters > 1 &&
-         static_cast<int64_t>(NG) * ((p->max_ctx + f.tile_iters * kScanRows - 1) / (f.tile_iters * kScanRows)) <
-             4LL * grid)
-    f.tile_iters >>= 1;
-  f.T = static_cast<int>((p->max_ctx + f.tile_iters * kScanRows - 1) / (f.tile_iters * kScanRows));
-  f.KS = kFusedKS;
-  f.scan_target = f.T;
-  f.scan_flush_iters = 4;
-  int ka = (2 * grid + NH - 1) / NH;
-  static const int ka_env = [] {  // experiments: attend items per head
-    const char* e = getenv("TKV_KA");
-    return e ? atoi(e) : 0;
-  }();
-  const bool tc_fused = !(p->flags & TKV_F_SCAN_HMMA) && fused_tc_supported(f);
-  if (tc_fused) ka = (256 + NH - 1) / NH;  // tc kernel: 8 per head at NH = 32 (measured 8 > 4, 16)
-  if (ka_env > 0) ka = ka_env;
-  f.KA = ka < 1 ? 1 : (ka > 16 ? 16 : ka);
-  f.trace = g_trace;
-  f.trace_cap = g_trace_cap;
-  if (g_scan_start && g_scan_stop) cudaEventRecord(g_scan_start, st);
-  if (tc_fused)
-    TKV_LAUNCH(launch_fused_tc(f, st));
-  else
-    TKV_LAUNCH(launch_fused(f, st));
-  if (g_scan_start && g_scan_stop) cudaEventRecord(g_scan_stop, st);
-  if (p->flags & TKV_F_SORTED) {
-    SortParams so{idx, scores, at<int32_t>(ws, L.mkb), p->k, 0};
-    TKV_LAUNCH(launch_sort(so, p->batch * p->n_q_heads, st));
-  }
-  return TKV_OK;
 }
 
 }  // namespace
@@ -701,12 +607,6 @@ int tkv_version(void) { return TKV_VERSION; }
 const char* tkv_last_error(void) { return g_err.c_str(); }
 
 int tkv_last_launch_count(void) { return g_launches; }
-
-int tkv_debug_trace(void* buf, uint32_t n_items) {
-  g_trace = static_cast<uint64_t*>(buf);
-  g_trace_cap = buf ? n_items : 0u;
-  return TKV_OK;
-}
 
 int tkv_debug_timeline(void* buf) {
   g_tl = static_cast<uint64_t*>(buf);
@@ -803,14 +703,7 @@ int tkv_topk_decode_step(const tkv_problem* p, const void* q, const void* k_new,
   TRY(check_ptr(idx, "idx", 4));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   float* sc = scores ? scores : at<float>(ws, L.sscore);
-  if (p->flags & TKV_F_FUSED) {  // the fused kernels have no threshold_kernel: append first
-    AppendParams ap{p->batch, p->n_kv_heads, p->cache_rows, static_cast<__nv_bfloat16*>(k_cache),
-                    static_cast<__nv_bfloat16*>(v_cache), static_cast<const __nv_bfloat16*>(k_new),
-                    static_cast<const __nv_bfloat16*>(v_new), n_ctx, n_win, 1};
-    TKV_LAUNCH(launch_append(ap, st));
-  } else {
-    g_fold = AppendFold{k_new, v_new, k_cache, v_cache, n_win};
-  }
+  g_fold = AppendFold{k_new, v_new, k_cache, v_cache, n_win};
   const int rc = run_layer(p, q, k_cache, v_cache, n_ctx, n_win, idx, sc, nullptr, out, 1, ws, L, st);
   g_fold = AppendFold{};
   return rc;

@@ -223,16 +223,13 @@ __global__ void __launch_bounds__(NT, TKV_ATT_MINB) attend_list_kernel(AttendPar
 }
 
 cudaError_t launch_attend_list(const AttendParams& p, cudaStream_t s) {
-  static int grid = 0;
-  if (!grid) {
+  const int grid = per_device(reinterpret_cast<const void*>(attend_list_kernel), 0, [] {
     cudaFuncSetAttribute(attend_list_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int per = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, attend_list_kernel, NT, 8192);
-    grid = sms * (per > 0 ? per : 1);
-  }
+    return device_sm_count() * (per > 0 ? per : 1);
+  });
   const size_t nbh = p.bh_count ? static_cast<size_t>(p.bh_count) : static_cast<size_t>(p.B) * p.Hq;
   attend_list_kernel<<<grid, NT, (nbh + 1) * sizeof(uint32_t), s>>>(p);
   return cudaGetLastError();
@@ -273,7 +270,7 @@ __global__ void __launch_bounds__(256) append_kernel(AppendParams p) {
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0 && p.advance) p.count[b] = cnt + 1;
+  if (threadIdx.x == 0 && p.advance && pos >= 0 && pos < p.cache_rows) p.count[b] = cnt + 1;  // written rows only
 }
 
 cudaError_t launch_attend(const AttendParams& p, cudaStream_t s) {
@@ -283,17 +280,14 @@ cudaError_t launch_attend(const AttendParams& p, cudaStream_t s) {
 }
 
 cudaError_t launch_attend_cand(const AttendParams& p, cudaStream_t s) {
-  static int grid = 0;
-  if (!grid) {
+  const int grid = per_device(reinterpret_cast<const void*>(attend_cand_kernel), 0, [] {
     // same shared-memory carveout as the scan, so both can share an SM (parts pipeline)
     cudaFuncSetAttribute(attend_cand_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int per = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, attend_cand_kernel, NT, 8192);
-    grid = sms * (per > 0 ? per : 1);
-  }
+    return device_sm_count() * (per > 0 ? per : 1);
+  });
   const size_t nbh = p.bh_count ? static_cast<size_t>(p.bh_count) : static_cast<size_t>(p.B) * p.Hq;
   attend_cand_kernel<<<grid, NT, (nbh + 1) * sizeof(uint32_t), s>>>(p);
   return cudaGetLastError();

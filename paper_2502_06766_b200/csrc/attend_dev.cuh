@@ -1,5 +1,5 @@
 // attend_dev.cuh — device pieces of the V gather + softmax (attention.py:158-167, 107-122),
-// shared by attend.cu (multi-kernel pipeline) and fused.cu (persistent layer-step kernel).
+// shared by attend.cu and select.cu (head kernel, exactness-fallback gather).
 #pragma once
 
 #include <math.h>

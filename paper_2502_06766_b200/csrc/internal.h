@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <functional>
 #include <utility>
 
 namespace tkv {
@@ -210,28 +211,6 @@ struct AppendParams {
   int advance;
 };
 
-// Fused persistent layer-step kernel (fused.cu): `a` carries the problem, the caches, the
-// outputs and the attention workspace; the rest is the selection state and the schedule.
-struct FusedParams {
-  AttendParams a;
-  HeadState hs;
-  uint32_t* samp;  // [B*Hq*kSamples]
-  uint32_t* ctl;   // control block (zero at launch; the last CTA to exit re-zeroes it)
-  int64_t max_ctx;
-  int no_filter;
-  int NS;          // sample items per (b, kv head)
-  int T;           // scan tiles per (b, kv head)
-  int tile_iters;  // 256-row iterations per scan tile
-  int KS;          // k-th slices per head
-  int KA;          // attend items per head
-  int scan_target;       // scan_done(g) count that completes group g's scan
-  int scan_flush_iters;  // HMMA scan items: 256-row iterations per staging flush
-  uint64_t* trace;  // optional per-item timeline (tkv_debug_trace): [n][4] = t0, t1, type|cta, item
-  uint32_t trace_cap;
-};
-constexpr int kFusedKS = 4;
-__host__ __device__ inline int fused_ctl_words(int NG, int NH) { return 8 + 2 * NG + 5 * NH; }
-
 // Launch with programmatic stream serialisation (the kernel calls pdl_wait() before touching
 // its predecessor's outputs), or an ordinary launch when pdl is false.
 template <typename... KArgs, typename... Args>
@@ -251,9 +230,13 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 }
 bool pdl_enabled();
 
-cudaError_t launch_fused(const FusedParams& p, cudaStream_t s);
-cudaError_t launch_fused_tc(FusedParams p, cudaStream_t s);
-bool fused_tc_supported(const FusedParams& p);
+// host_state.cu: per-device memoisation (key, tag, current device) -> compute(), the current
+// device's SM count, and the TKV_DIAG-only environment overrides (release: always dflt)
+int current_device();
+int per_device(const void* key, int tag, const std::function<int()>& compute);
+int device_sm_count();
+int diag_env(const char* name, int dflt);
+
 cudaError_t launch_sample(const SampleParams& p, cudaStream_t s);
 cudaError_t launch_scan(const ScanParams& p, cudaStream_t s);
 cudaError_t launch_scan_tc(const ScanParams& p, cudaStream_t s);

@@ -127,7 +127,9 @@ __global__ void __launch_bounds__(kThrThreads) threshold_kernel(SampleParams p) 
       }
     }
     __syncthreads();
-    if (threadIdx.x == 0) p.win_count[b] = cnt + 1;
+    // the counter advances only over a written row (a full window stays full; the host layers
+    // raise InputError before enqueueing such a step, as GenWindow.append does)
+    if (threadIdx.x == 0 && pos >= 0 && pos < p.cache_rows) p.win_count[b] = cnt + 1;
   }
   const int bh = blockIdx.x;
   const int b = bh / p.Hq;
@@ -357,35 +359,26 @@ __global__ void __launch_bounds__(kScanWarps * 32, 2) scan_fma_kernel(ScanParams
 
 cudaError_t launch_scan_fma(const ScanParams& p, cudaStream_t s) {
   const size_t smem = static_cast<size_t>(p.G) * kScanStage * sizeof(uint64_t);
-  static int grid = 0;
-  if (!grid) {
-    cudaFuncSetAttribute(scan_fma_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         8 * kScanStage * static_cast<int>(sizeof(uint64_t)));
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, scan_fma_kernel<4>, kScanWarps * 32, smem);
-    grid = sms * (per > 0 ? per : 1);
-  }
-  auto k = p.G <= 1 ? scan_fma_kernel<1> : p.G <= 2 ? scan_fma_kernel<2> : p.G <= 4 ? scan_fma_kernel<4> : scan_fma_kernel<8>;
-  static bool attr = false;
-  if (!attr) {
+  const int grid = per_device(reinterpret_cast<const void*>(scan_fma_kernel<4>), p.G, [smem] {
     for (auto kk : {scan_fma_kernel<1>, scan_fma_kernel<2>, scan_fma_kernel<4>, scan_fma_kernel<8>})
       cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            8 * kScanStage * static_cast<int>(sizeof(uint64_t)));
-    attr = true;
-  }
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, scan_fma_kernel<4>, kScanWarps * 32, smem);
+    return device_sm_count() * (per > 0 ? per : 1);
+  });
+  auto k = p.G <= 1 ? scan_fma_kernel<1> : p.G <= 2 ? scan_fma_kernel<2> : p.G <= 4 ? scan_fma_kernel<4> : scan_fma_kernel<8>;
   return launch_pdl(k, dim3(grid), dim3(kScanWarps * 32), smem, s, p.pdl != 0, p);
 }
 
 cudaError_t launch_sample(const SampleParams& p, cudaStream_t s) {
-  static bool carve = false;
-  if (!carve) {  // same carveout as the scan: the scan's CTAs start beside these (PDL)
+  per_device(reinterpret_cast<const void*>(sample_kernel), 0, [] {
+    // same carveout as the scan: the scan's CTAs start beside these (PDL)
     cudaFuncSetAttribute(sample_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     cudaFuncSetAttribute(threshold_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
-    carve = true;
-  }
+    return 1;
+  });
   if (!p.no_filter) {
     dim3 grid(kSamples / kSampleThreads, p.B * p.Hkv);
     cudaError_t e = launch_pdl(sample_kernel, grid, dim3(kSampleThreads), 0, s, p.pdl != 0, p);
@@ -395,38 +388,21 @@ cudaError_t launch_sample(const SampleParams& p, cudaStream_t s) {
 }
 
 static int scan_grid(int G, size_t smem) {
-  static int cached[9] = {0};
-  static int dev_cached = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev != dev_cached) {
-    for (int i = 0; i < 9; ++i) cached[i] = 0;
-    dev_cached = dev;
-  }
-  if (cached[G] == 0) {
-    int sms = 0, per = 0;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return per_device(reinterpret_cast<const void*>(scan_kernel), G, [smem] {
+    cudaFuncSetAttribute(scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         8 * kScanStage * static_cast<int>(sizeof(uint64_t)));
+    int per = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, scan_kernel, kScanWarps * 32, smem);
-    static const int cap = [] {
-      const char* e = getenv("TKV_SCAN_CTAS_PER_SM");
-      return e ? atoi(e) : 0;
-    }();
+    const int cap = diag_env("TKV_SCAN_CTAS_PER_SM", 0);
     if (cap > 0 && per > cap) per = cap;
-    cached[G] = sms * (per > 0 ? per : 1);
-  }
-  return cached[G];
+    return device_sm_count() * (per > 0 ? per : 1);
+  });
 }
 
 // Grid and dynamic shared memory of the scan kernel (host), also used for the device-side
 // tail launch of the exactness fallback.
 void scan_launch_shape(const ScanParams& p, int* grid, int* smem_bytes) {
   const size_t smem = static_cast<size_t>(p.G) * kScanStage * sizeof(uint64_t);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         8 * kScanStage * static_cast<int>(sizeof(uint64_t)));
-    attr_set = true;
-  }
   const int64_t tps = (p.max_ctx + kScanRows - 1) / kScanRows;
   const int64_t total = (p.seg_count ? p.seg_count : static_cast<int64_t>(p.B) * p.Hkv) * tps;
   int g = scan_grid(p.G, smem);
@@ -437,12 +413,6 @@ void scan_launch_shape(const ScanParams& p, int* grid, int* smem_bytes) {
 
 cudaError_t launch_scan(const ScanParams& p, cudaStream_t s) {
   const size_t smem = static_cast<size_t>(p.G) * kScanStage * sizeof(uint64_t);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         8 * kScanStage * static_cast<int>(sizeof(uint64_t)));
-    attr_set = true;
-  }
   const int64_t tps = (p.max_ctx + kScanRows - 1) / kScanRows;
   const int64_t total = (p.seg_count ? p.seg_count : static_cast<int64_t>(p.B) * p.Hkv) * tps;
   if (total == 0) return cudaSuccess;

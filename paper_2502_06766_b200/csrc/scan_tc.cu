@@ -198,18 +198,11 @@ cudaError_t launch_scan_tc(const ScanParams& p, cudaStream_t s) {
   if (total == 0) return cudaSuccess;
   CUtensorMap map;
   if (!tc::make_kmap(p.kc, static_cast<int64_t>(p.B) * p.Hkv * p.cache_rows, &map)) return cudaErrorInvalidValue;
-  static const int mode = [] {  // diagnostics: bit 0 = no MMA, bit 1 = no emission, bit 2 = no TMA
-    const char* e = getenv("TKV_TC_MODE");
-    return e ? atoi(e) : 0;
-  }();
-  static const int stages_env = [] {  // experiments: force the ring depth (2 or 3)
-    const char* e = getenv("TKV_TC_STAGES");
-    return e ? atoi(e) : 0;
-  }();
-  static const int flush_env = [] {  // experiments: cap the units between flushes
-    const char* e = getenv("TKV_TC_FLUSH");
-    return e ? atoi(e) : 0;
-  }();
+  // TKV_DIAG builds only (release: 0): bit 0 = no MMA, bit 1 = no emission, bit 2 = no TMA —
+  // each gives wrong results by design (pipeline cost breakdown)
+  const int mode = diag_env("TKV_TC_MODE", 0);
+  const int stages_env = diag_env("TKV_TC_STAGES", 0);  // experiments: force the ring depth (2 or 3)
+  const int flush_env = diag_env("TKV_TC_FLUSH", 0);    // experiments: cap the units between flushes
   TcShape sh = tc_shape(p.G, kTcScanGroups);
   if (stages_env >= 2 && stages_env <= kTcMaxStages && stages_env != sh.stages) {
     sh.stages = stages_env;
@@ -224,22 +217,15 @@ cudaError_t launch_scan_tc(const ScanParams& p, cudaStream_t s) {
     sh.flush = flush_env < fit ? flush_env : fit;
   }
   const size_t smem = tc_smem_bytes(p.G, sh, kTcScanGroups);
-  static bool attr_set = false;
-  if (!attr_set) {
+  const int attr = per_device(reinterpret_cast<const void*>(scan_tc_kernel), 0, [] {
     cudaError_t e = cudaFuncSetAttribute(scan_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmemLimit);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(scan_tc_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                cudaSharedmemCarveoutMaxShared);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  static const int sms = [] {
-    int dev = 0, n = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    return n;
-  }();
-  int grid = sms;
+    return static_cast<int>(e);
+  });
+  if (attr != cudaSuccess) return static_cast<cudaError_t>(attr);
+  int grid = device_sm_count();
   if (total < grid) grid = static_cast<int>(total);
   return launch_pdl(scan_tc_kernel, dim3(grid), dim3(kTcScanThreads), smem, s, p.pdl != 0, map, p, sh.stages,
                     sh.flush, mode);

@@ -1,8 +1,7 @@
 // scan_tc_dev.cuh — building blocks of the TMA + tcgen05 key scan (see scan_tc.cu for the
 // pipeline): constants, PTX wrappers, the per-CTA pipeline state (mbarrier ring, TMEM
 // accumulators, q slots, warp-private candidate staging) and the per-unit steps of the three
-// roles. Used by scan_tc_kernel (scan_tc.cu) and by the warp-specialised layer kernel
-// (fused.cu), which runs the same roles group by group beside its work-queue warps.
+// roles, used by scan_tc_kernel (scan_tc.cu).
 #pragma once
 
 #include <cuda.h>
@@ -36,7 +35,6 @@ static_assert((kTcTmemCols & (kTcTmemCols - 1)) == 0 && kTcTmemCols <= 512, "TME
 constexpr int kTcQSlots = 4;                       // q slots, each released by a tcgen05.commit
 constexpr int kTcQBytes = kTcN * kD * 2;           // 2 KB: one 8-row swizzle atom per half
 constexpr int kTcEpiWarps = 4;                     // epilogue warps per unit (one per TMEM lane quarter)
-constexpr int kTcThreads = 64 + 32 * kTcEpiWarps;  // one epilogue group (fused_tc_kernel)
 constexpr int kTcScanGroups = 2;                   // scan_tc_kernel: two groups alternate units
 constexpr int kTcScanThreads = 64 + 32 * kTcEpiWarps * kTcScanGroups;
 constexpr int kTcWarpRows = kTcUnit / 4;           // rows per unit one epilogue warp handles

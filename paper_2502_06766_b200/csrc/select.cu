@@ -511,22 +511,21 @@ __global__ void __cluster_dims__(kKthCtas, 1, 1) __launch_bounds__(kKthThreads, 
 
 void prepare_fallback_kernels() {
 #ifndef TKV_NO_CDP
-  static bool done = false;
-  if (!done) {
+  per_device(reinterpret_cast<const void*>(fb_scan_kernel), 0, [] {
     cudaFuncSetAttribute(fb_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          8 * kScanStage * static_cast<int>(sizeof(uint64_t)));
-    done = true;
-  }
+    return 1;
+  });
 #endif
 }
 
 cudaError_t launch_kth(const SelectParams& p, cudaStream_t s) {
   prepare_fallback_kernels();
-  static bool carve = false;
-  if (!carve) {  // same shared-memory carveout as the scan, so both can share an SM (parts pipeline)
+  per_device(reinterpret_cast<const void*>(kth_kernel), 0, [] {
+    // same shared-memory carveout as the scan, so both can share an SM (parts pipeline)
     cudaFuncSetAttribute(kth_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-    carve = true;
-  }
+    return 1;
+  });
   return launch_pdl(kth_kernel, dim3(kKthCtas, p.bh_count ? p.bh_count : p.B * p.Hq), dim3(kKthThreads), kKthSmem, s,
                     p.pdl && p.pass == kPassMain, p);
 }
@@ -858,17 +857,14 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_topk_kernel(HeadParams h
 
 cudaError_t launch_head_topk(const HeadParams& p, cudaStream_t s) {
   prepare_fallback_kernels();
-  static int att_grid = 0;
-  if (!att_grid) {
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int att_grid = per_device(reinterpret_cast<const void*>(head_topk_kernel), 0, [] {
+    int per = 0;
 #ifndef TKV_NO_CDP
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, attend_cand_fb_kernel, NT, 8192);
 #endif
-    att_grid = sms * (per > 0 ? per : 1);
     cudaFuncSetAttribute(head_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHeadSmem);
-  }
+    return device_sm_count() * (per > 0 ? per : 1);
+  });
   HeadParams q = p;
   q.att_grid = att_grid;
   const int nbh = p.s.bh_count ? p.s.bh_count : p.s.B * p.s.Hq;
@@ -915,11 +911,10 @@ __global__ void __launch_bounds__(SNT) sort_kernel(SortParams p) {
 
 cudaError_t launch_select(const SelectParams& p, cudaStream_t s) {
   const int smem = kSelectBucketCap * static_cast<int>(sizeof(uint64_t));
-  static bool attr = false;
-  if (!attr) {
+  per_device(reinterpret_cast<const void*>(select_kernel), 0, [smem] {
     cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+    return 1;
+  });
   select_kernel<<<p.B * p.Hq, SNT, smem, s>>>(p);
   return cudaGetLastError();
 }
@@ -929,12 +924,11 @@ cudaError_t launch_sort(const SortParams& p, int nbh, cudaStream_t s) {
   const int kmax = p.k < kSortMax ? p.k : kSortMax;
   while (P < kmax) P <<= 1;
   const size_t smem = static_cast<size_t>(P) * sizeof(uint64_t);
-  static bool attr = false;
-  if (!attr) {
+  per_device(reinterpret_cast<const void*>(sort_kernel), 0, [] {
     cudaFuncSetAttribute(sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(kSortMax * sizeof(uint64_t)));
-    attr = true;
-  }
+    return 1;
+  });
   sort_kernel<<<nbh, SNT, smem, s>>>(p);
   return cudaGetLastError();
 }

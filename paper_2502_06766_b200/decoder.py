@@ -24,8 +24,8 @@ class TopkDecoder:
     def __init__(self, k_cache: torch.Tensor, v_cache: torch.Tensor, n_ctx, k: int, *,
                  n_win=0, scale: float | None = None, combine: str = "joint",
                  pinned_prefix: int = 0, sorted: bool = False, max_ctx: int | None = None,
-                 fused: bool = False, use_graph: bool = True, parts: int = 0, list_gather: bool = False,
-                 fold_append: bool = True):
+                 use_graph: bool = True, parts: int = 0, list_gather: bool = False,
+                 head: bool | None = None, fold_append: bool = True):
         if k < 1:
             raise InputError("k must be >= 1")
         ops._check_cuda_bf16("k_cache", k_cache, 4)
@@ -37,10 +37,14 @@ class TopkDecoder:
         self.device = k_cache.device
         self.n_ctx = ops._as_counts("n_ctx", n_ctx, self.B, self.device)
         self.n_win = ops._as_counts("n_win", n_win, self.B, self.device)
+        # host mirrors of the counters (one read at construction): the window's capacity is
+        # checked before a step is enqueued, as GenWindow.append does (attention.py:96-97)
+        self._ctx_host = [int(x) for x in self.n_ctx.tolist()]
+        self._win_host = [int(x) for x in self.n_win.tolist()]
         self.max_ctx = int(max_ctx if max_ctx is not None else self.rows)
         self.k = k
         self.kw = dict(scale=scale, combine=combine, pinned_prefix=pinned_prefix, sorted=sorted,
-                       max_ctx=self.max_ctx, fused=fused, parts=parts, list_gather=list_gather)
+                       max_ctx=self.max_ctx, parts=parts, list_gather=list_gather, head=head)
         ops.combine_code(combine)
         self.use_graph = use_graph
         self.fold_append = fold_append
@@ -59,8 +63,8 @@ class TopkDecoder:
         prob = ops.make_problem(self.B, Hq, self.Hkv, self.rows, self.max_ctx, self.k,
                                 pinned_prefix=self.kw["pinned_prefix"], scale=self.kw["scale"],
                                 combine=self.kw["combine"], sorted=self.kw["sorted"],
-                                fused=self.kw["fused"], parts=self.kw["parts"],
-                                list_gather=self.kw["list_gather"])
+                                parts=self.kw["parts"], list_gather=self.kw["list_gather"],
+                                head=self.kw["head"])
         self.ws = ops.Workspace(prob, dev)
         D = ops.HEAD_DIM
         bf, f32, i32 = torch.bfloat16, torch.float32, torch.int32
@@ -89,10 +93,16 @@ class TopkDecoder:
         self._graphs.clear()
 
     # ------------------------------------------------------------------ device-side pieces
+    def _reserve_row(self) -> None:
+        if any(c + w + 1 > self.rows for c, w in zip(self._ctx_host, self._win_host)):
+            raise InputError("generation window capacity exceeded")
+        self._win_host = [w + 1 for w in self._win_host]
+
     def append(self, k_new: torch.Tensor, v_new: torch.Tensor) -> None:
         """GenWindow.append (attention.py:94-100) on device: rows n_ctx + n_win, n_win += 1."""
         if self._bufs is None:
             raise InputError("call step() (or attend()) once before append-only use")
+        self._reserve_row()
         kd, vd = self._bufs["k_new"], self._bufs["v_new"]
         kd.copy_(k_new, non_blocking=True)
         vd.copy_(v_new, non_blocking=True)
@@ -149,6 +159,8 @@ class TopkDecoder:
             return (out, idx) if return_idx else out
         b = self._bufs
         with_kv = k_new is not None
+        if with_kv:
+            self._reserve_row()
         Hq = q.shape[1]
         # pinned bf16 inputs of the right shape are read in place by the call (no host copy);
         # the step's graph is then keyed by their addresses (a few cached)

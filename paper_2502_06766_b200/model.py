@@ -127,6 +127,7 @@ class TopkLlamaDecoder:
         self.idx, self.scores = self._sel[self.k]
         self.graph = None
         self.pos.fill_(n_ctx)
+        self.win_used = 0  # host mirror of n_win: capacity is checked before a step is enqueued
 
     def _layer(self, x: torch.Tensor, lw: dict, layer: int = 0) -> torch.Tensor:
         s = self.shape
@@ -169,6 +170,10 @@ class TopkLlamaDecoder:
 
     def step(self, token: int | None = None) -> torch.Tensor:
         """One decode step for every layer; returns the greedy next token (device tensor)."""
+        if self.n + self.win_used + 1 > self.rows:
+            # GenWindow.append raises on a full window (attention.py:96-97)
+            raise InputError("generation window capacity exceeded")
+        self.win_used += 1
         if token is not None:
             self.token.fill_(token)
         if self.graph is not None:

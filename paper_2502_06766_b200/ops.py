@@ -43,7 +43,7 @@ def combine_code(combine: str) -> int:
 def make_problem(B: int, Hq: int, Hkv: int, cache_rows: int, max_ctx: int, k: int, *,
                  pinned_prefix: int = 0, scale: float | None = None, combine: str = "joint",
                  sorted: bool = False, no_filter: bool = False, row_offset: int = 0,
-                 head_dim: int = HEAD_DIM, fused: bool = False,
+                 head_dim: int = HEAD_DIM,
                  tc_scan: bool | None = None, parts: int = 0, list_gather: bool = False,
                  head: bool | None = None, host_q: bool = False) -> _lib.Problem:
     p = _lib.Problem()
@@ -52,8 +52,7 @@ def make_problem(B: int, Hq: int, Hkv: int, cache_rows: int, max_ctx: int, k: in
     p.pinned_prefix = pinned_prefix
     p.scale = float(scale) if scale is not None else 1.0 / math.sqrt(head_dim)
     p.combine = combine_code(combine)
-    p.flags = ((_lib.F_SORTED if sorted else 0) | (_lib.F_NO_FILTER if no_filter else 0)
-               | (_lib.F_FUSED if fused else 0))
+    p.flags = (_lib.F_SORTED if sorted else 0) | (_lib.F_NO_FILTER if no_filter else 0)
     if tc_scan is None:  # the tcgen05 scan is the default; TKV_SCAN=hmma selects the mma.sync scan
         tc_scan = os.environ.get("TKV_SCAN", "") != "hmma"
     if not tc_scan:
@@ -164,7 +163,7 @@ def topk_decode_attention(q, k_cache, v_cache, n_ctx, k: int, *, n_win=None, sca
                           combine: str = "joint", pinned_prefix: int = 0, sorted: bool = False,
                           max_ctx: int | None = None, no_filter: bool = False, row_offset: int = 0,
                           out=None, idx=None, scores=None, workspace: Workspace | None = None,
-                          fused: bool = False, tc_scan: bool | None = None, parts: int = 0,
+                          tc_scan: bool | None = None, parts: int = 0,
                           list_gather: bool = False, head: bool | None = None):
     """Exact top-k decode attention for every (batch, q head) of one layer.
 
@@ -183,7 +182,7 @@ def topk_decode_attention(q, k_cache, v_cache, n_ctx, k: int, *, n_win=None, sca
         max_ctx = s.cache_rows if isinstance(n_ctx, torch.Tensor) else int(n_ctx_t.max().item())
     prob = make_problem(s.B, s.Hq, s.Hkv, s.cache_rows, max_ctx, k, pinned_prefix=pinned_prefix,
                         scale=scale, combine=combine, sorted=sorted, no_filter=no_filter,
-                        row_offset=row_offset, fused=fused, tc_scan=tc_scan, parts=parts,
+                        row_offset=row_offset, tc_scan=tc_scan, parts=parts,
                         list_gather=list_gather, head=head,
                         host_q=not q.is_cuda)
     ws = workspace or workspace_for(prob, dev)
@@ -199,7 +198,7 @@ def topk_decode_attention(q, k_cache, v_cache, n_ctx, k: int, *, n_win=None, sca
 def topk_decode_step(q, k_new, v_new, k_cache, v_cache, n_ctx, n_win, k: int, *, scale=None,
                      combine: str = "joint", pinned_prefix: int = 0, sorted: bool = False,
                      max_ctx: int | None = None, out=None, idx=None, scores=None,
-                     workspace: Workspace | None = None, fused: bool = False, tc_scan: bool | None = None,
+                     workspace: Workspace | None = None, tc_scan: bool | None = None,
                      parts: int = 0, list_gather: bool = False, head: bool | None = None):
     """One decode step of one layer (decode_step, attention.py:203-230): append this token's
     k_new/v_new [B, Hkv, 128] to the window (GenWindow.append, attention.py:210; n_win is a
@@ -218,7 +217,7 @@ def topk_decode_step(q, k_new, v_new, k_cache, v_cache, n_ctx, n_win, k: int, *,
     if max_ctx is None:
         max_ctx = s.cache_rows if isinstance(n_ctx, torch.Tensor) else int(n_ctx_t.max().item())
     prob = make_problem(s.B, s.Hq, s.Hkv, s.cache_rows, max_ctx, k, pinned_prefix=pinned_prefix,
-                        scale=scale, combine=combine, sorted=sorted, fused=fused, tc_scan=tc_scan,
+                        scale=scale, combine=combine, sorted=sorted, tc_scan=tc_scan,
                         parts=parts, list_gather=list_gather, head=head,
                         host_q=not q.is_cuda)
     ws = workspace or workspace_for(prob, dev)
@@ -232,7 +231,7 @@ def topk_decode_step(q, k_new, v_new, k_cache, v_cache, n_ctx, n_win, k: int, *,
 
 def topk_search(q, k_cache, n_ctx, k: int, *, sorted: bool = True, max_ctx: int | None = None,
                 no_filter: bool = False, row_offset: int = 0, workspace: Workspace | None = None,
-                fused: bool = False, tc_scan: bool | None = None, parts: int = 0, head: bool | None = None):
+                tc_scan: bool | None = None, parts: int = 0, head: bool | None = None):
     """Exact top-k rows per (batch, q head) without attention (knn_search flat, ann.py:203-218).
 
     Returns (idx [B, Hq, k] int32, scores [B, Hq, k] f32), TopKResult-ordered when sorted.
@@ -245,7 +244,7 @@ def topk_search(q, k_cache, n_ctx, k: int, *, sorted: bool = True, max_ctx: int 
     if max_ctx is None:
         max_ctx = s.cache_rows if isinstance(n_ctx, torch.Tensor) else int(n_ctx_t.max().item())
     prob = make_problem(s.B, s.Hq, s.Hkv, s.cache_rows, max_ctx, k, sorted=sorted,
-                        no_filter=no_filter, row_offset=row_offset, fused=fused, tc_scan=tc_scan,
+                        no_filter=no_filter, row_offset=row_offset, tc_scan=tc_scan,
                         parts=parts, head=head, host_q=not q.is_cuda)
     ws = workspace or workspace_for(prob, dev)
     idx = torch.empty((s.B, s.Hq, k), dtype=torch.int32, device=dev)

@@ -30,11 +30,8 @@ def _config(seed: int):
         list_gather=bool(r.random() < 0.3),
         tc_scan=bool(r.random() < 0.8),
         no_filter=bool(r.random() < 0.15),
-        fused=bool(r.random() < 0.25),
+        head=True if r.random() < 0.25 else None,  # force the per-head k-th + gather kernel
     )
-    if opts["fused"]:  # the fused kernels run the whole layer: no parts / list options
-        opts["parts"] = 0
-        opts["list_gather"] = False
     return B, G * Hkv, Hkv, N, k, W, pin, combine, n_ctx, opts
 
 
