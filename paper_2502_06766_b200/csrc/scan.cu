@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(kSampleThreads) sample_kernel(SampleParams p) 
   if (threadIdx.x == 0) tl_end(p.tl, 0);
 }
 
-__global__ void __launch_bounds__(kThrThreads) threshold_kernel(SampleParams p) {
+__global__ void __launch_bounds__(kThrThreads, 4) threshold_kernel(SampleParams p) {
   constexpr int NT = kThrThreads;
   __shared__ __align__(16) uint32_t s_keys[kSamples];
   __shared__ uint32_t s_hist[2048];
@@ -109,6 +109,17 @@ __global__ void __launch_bounds__(kThrThreads) threshold_kernel(SampleParams p) 
   if (threadIdx.x == 0) tl_start(p.tl, 1);
   pdl_wait();     // samples of the sample kernel
   if (threadIdx.x == 0) tl_start(p.tl, 2);
+#ifdef TKV_DIAG
+  if (threadIdx.x == 0) {
+    tl_start(p.tl, 45);  // diagnostics: first / last CTA past its wait
+    tl_end(p.tl, 45);
+  }
+  uint64_t t_ph = p.tl ? gtimer() : 0ull;
+#define TKV_THR_PHASE(e) \
+  if (tid == 0) tl_phase(p.tl, e, t_ph)
+#else
+#define TKV_THR_PHASE(e)
+#endif
   if (p.k_new && blockIdx.x % p.Hq == 0) {
     // GenWindow.append (attention.py:94-100, 210) for batch entry b = blockIdx.x / Hq: the rows
     // were written by the sample kernel (this kernel waited for it); with no sample kernel
@@ -149,12 +160,14 @@ __global__ void __launch_bounds__(kThrThreads) threshold_kernel(SampleParams p) 
   if (filter) {
     copy_g2s_u32<NT, kSamples>(s_keys, p.samp + static_cast<int64_t>(bh) * kSamples, (Sb + 3) & ~3);
     __syncthreads();
+    TKV_THR_PHASE(25);
     uint32_t mx = 0u;
     for (int i = tid; i < Sb; i += NT) mx = max(mx, s_keys[i]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(kFull, mx, o));
     if (lane == 0) s_max[warp] = mx;
     __syncthreads();
+    TKV_THR_PHASE(26);
     // r-th largest sampled key: MSB-first radix select (11/11/10-bit digits) in shared memory.
     // Stopping early when the digit's bucket is taken whole leaves the bucket's lower bound,
     // which is <= the r-th key (a threshold only has to be a lower bound).
@@ -200,6 +213,7 @@ __global__ void __launch_bounds__(kThrThreads) threshold_kernel(SampleParams p) 
       }
     }
     if (!exact) thr = sh > 0 ? prefix << sh : prefix;
+    TKV_THR_PHASE(27);
     uint32_t smax = 0u;
     for (int w = 0; w < NT / 32; ++w) smax = max(smax, s_max[w]);
     // histogram granularity: the sampled range [thr, smax] spans ~1/4 of the 4096 buckets,
@@ -219,6 +233,9 @@ __global__ void __launch_bounds__(kThrThreads) threshold_kernel(SampleParams p) 
     p.hs.bkt_cnt[bh] = 0u;
     p.hs.out_cnt[bh] = 0u;
     tl_end(p.tl, 1);
+  }
+  {
+    TKV_THR_PHASE(28);
   }
 }
 

@@ -90,7 +90,14 @@ __global__ void __launch_bounds__(kTcScanThreads, 1) scan_tc_kernel(const __grid
   __shared__ uint32_t s_tmem;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   pdl_trigger();  // the k-th kernel may launch now; it waits for this grid to complete
-  if (tid == 0) tl_start(p.tl, 3);
+#ifdef TKV_DIAG
+  const uint64_t t_cta = p.tl ? gtimer() : 0ull;
+#endif
+  if (tid == 0) {
+    tl_start(p.tl, 3);
+    tl_start(p.tl, 40);  // first / last CTA start
+    tl_end(p.tl, 40);
+  }
   TcPipe t = tc_setup(smem_raw, s_bar, &s_tmem, p.G, flush_every, n_stages, &kmap, tid == 0, warp == 1,
                       kTcScanGroups);
   tc_fence_before();
@@ -110,11 +117,28 @@ __global__ void __launch_bounds__(kTcScanThreads, 1) scan_tc_kernel(const __grid
       tc_produce(t, i, &kmap, static_cast<int>(w.cur_seg * p.cache_rows + w.cur_row0), lane, mode);
   } else if (warp == 1) {  // MMA issuer
     QRing qr;
+#ifdef TKV_DIAG
+    uint64_t d_wait = 0, n_units = 0;  // diagnostics (tl != nullptr): MMA warp's wait for TMA
+#endif
     for (uint32_t i = 0; w.next(p, new_seg); ++i) {
       tc_mma_acquire(t, i);
+#ifdef TKV_DIAG
+      if (p.tl) {
+        const uint64_t t_w = gtimer();
+        mbar_wait(t.full(static_cast<int>(i % t.n_stages)), (i / t.n_stages) & 1u);
+        d_wait += gtimer() - t_w;
+        ++n_units;
+      }
+#endif
       if (new_seg) tc_next_q(t, qr, p.q + (static_cast<int64_t>(w.cur_b) * p.Hq + w.cur_kvh * p.G) * kD, p.G, lane);
       tc_mma_issue(t, i, qr.slot, lane, mode);
     }
+#ifdef TKV_DIAG
+    if (p.tl && lane == 0 && n_units) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(p.tl + 88), static_cast<unsigned long long>(d_wait));
+      atomicAdd(reinterpret_cast<unsigned long long*>(p.tl + 89), static_cast<unsigned long long>(n_units));
+    }
+#endif
   } else {  // epilogue: two groups of four warps take alternate units
     pdl_wait();  // thresholds, zeroed counters and histograms of threshold_kernel (the TMA and
                  // MMA warps read only q and K and start streaming before it completes)
@@ -128,6 +152,9 @@ __global__ void __launch_bounds__(kTcScanThreads, 1) scan_tc_kernel(const __grid
     for (int n = 0; n < 8; ++n) cnt[n] = thr[n] = shift[n] = 0u;
     int since = 0;
     int64_t bh0 = -1;
+#ifdef TKV_DIAG
+    uint64_t d_wait = 0, d_work = 0, d_flush = 0, n_units = 0, n_flush = 0;  // diagnostics
+#endif
     for (uint32_t i = 0; w.next(p, new_seg); ++i) {
       if (new_seg) {
         if (bh0 >= 0) tc_warp_flush(p.cand, p.cap, p.hs.cand_cnt, p.hs.hist, p.G, bh0, wbuf, t.cap, cnt, thr, shift, lane);
@@ -141,22 +168,65 @@ __global__ void __launch_bounds__(kTcScanThreads, 1) scan_tc_kernel(const __grid
       }
       if (i % kTcScanGroups != group) continue;
       uint32_t v[16];
+#ifdef TKV_DIAG
+      uint64_t t_u = p.tl ? gtimer() : 0ull;
+      if (p.tl) {  // diagnostics: the epilogue's wait for the unit's scores
+        mbar_wait(t.tfull(static_cast<int>(i % kTcAcc)), (i / kTcAcc) & 1u);
+        const uint64_t t1 = gtimer();
+        d_wait += t1 - t_u;
+        t_u = t1;
+      }
+#endif
       tc_epi_load(t, i, quarter, lane, v, mode);
       tc_epi_emit(v, w.cur_row0, w.cur_nctx, quarter, lane, p.G, p.row_offset, thr, wbuf, t.cap, cnt,
                   !(mode & 3) /* diagnostics never emit */);
+#ifdef TKV_DIAG
+      if (p.tl) {
+        d_work += gtimer() - t_u;
+        ++n_units;
+      }
+      const uint64_t t_f = p.tl ? gtimer() : 0ull;
+#endif
       if (++since == flush_every) {
         tc_warp_flush(p.cand, p.cap, p.hs.cand_cnt, p.hs.hist, p.G, bh0, wbuf, t.cap, cnt, thr, shift, lane);
+#ifdef TKV_DIAG
+        if (p.tl) {
+          d_flush += gtimer() - t_f;
+          ++n_flush;
+        }
+#endif
         since = 0;
       }
     }
     if (bh0 >= 0) tc_warp_flush(p.cand, p.cap, p.hs.cand_cnt, p.hs.hist, p.G, bh0, wbuf, t.cap, cnt, thr, shift, lane);
     if (lane == 0) tl_end(p.tl, 4);
+#ifdef TKV_DIAG
+    if (p.tl && lane == 0) {  // slots 42, 43, 29: (sum ns, count) per warp, one atomic pair each
+      unsigned long long* tl = reinterpret_cast<unsigned long long*>(p.tl);
+      atomicAdd(tl + 84, static_cast<unsigned long long>(d_wait));
+      atomicAdd(tl + 85, static_cast<unsigned long long>(n_units));
+      atomicAdd(tl + 86, static_cast<unsigned long long>(d_work));
+      atomicAdd(tl + 87, static_cast<unsigned long long>(n_units));
+      atomicAdd(tl + 58, static_cast<unsigned long long>(d_flush));
+      atomicAdd(tl + 59, static_cast<unsigned long long>(n_flush));
+    }
+#endif
   }
 
   tc_fence_before();
   __syncthreads();
   tc_teardown(t.tmem, warp == 1);
-  if (tid == 0) tl_end(p.tl, 3);
+  if (tid == 0) {
+    tl_end(p.tl, 3);
+    tl_start(p.tl, 41);  // first / last CTA end
+    tl_end(p.tl, 41);
+  }
+#ifdef TKV_DIAG
+  if (tid == 0) {
+    uint64_t t0 = t_cta;
+    tl_phase(p.tl, 46, t0);  // CTA lifetime (mean)
+  }
+#endif
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {

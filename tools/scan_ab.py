@@ -46,6 +46,22 @@ def main():
     e1.record()
     torch.cuda.synchronize()
     step = e0.elapsed_time(e1) / args.steps * 1e3
+    # the same call captured once into a CUDA graph and replayed (no host launch cost per kernel)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(side), torch.cuda.graph(g, stream=side):
+        tkv.topk_decode_attention(q, K, V, nc, k, **kw)
+    torch.cuda.current_stream().wait_stream(side)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(args.steps):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    step_graph = e0.elapsed_time(e1) / args.steps * 1e3
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     for a, b in ev:
         a.record(); b.record()
@@ -57,7 +73,7 @@ def main():
     lib.tkv_profile_scan_events(None, None)
     scan = sum(a.elapsed_time(b) for a, b in ev) / args.steps * 1e3
     kbytes = B * 8 * n * 128 * 2
-    print(f"{args.config} tc={int(args.tc)} {args.label}: step {step:.1f} us, scan {scan:.1f} us "
+    print(f"{args.config} tc={int(args.tc)} {args.label}: step {step:.1f} us (graph replay {step_graph:.1f} us), scan {scan:.1f} us "
           f"({kbytes / scan / 1e3:.0f} GB/s)", flush=True)
 
 

@@ -14,13 +14,21 @@ NAMES = ["sample", "threshold", "threshold past wait", "scan", "scan epilogue pa
 PHASES = ["head CTA: start→params", "→hist+bucket", "→pass 1 (max, bucket members)", "→T",
           "→pads/meta + barriers", "→compaction loop", "→out_cnt reservation", "→V gather loop", "→ids written",
           "→partial slot written", "→finished (last CTA)",
-          "kth CTA: start→hist+bucket", "→slice scan", "→ticket (last CTA)", "→T written (last CTA)"]
+          "kth CTA: start→hist+bucket", "→slice scan", "→ticket (last CTA)", "→T written (last CTA)",
+          "threshold CTA: past wait→samples in smem", "→sample max", "→radix select (t_h)", "→hist zeroed, state written",
+          "scan epilogue: one warp flush"]
+
+
+EXTRA_EVENTS = {40: "scan CTA start", 41: "scan CTA end", 45: "threshold CTA past wait"}
+EXTRA_PHASES = {42: "scan epilogue: wait for a unit's scores", 43: "scan epilogue: ld+emit of a unit",
+                44: "scan MMA warp: wait for a unit's TMA", 46: "scan CTA lifetime"}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="cfg3")
     ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--graph", action="store_true", help="replay the step as a CUDA graph (no host launch gaps)")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -38,14 +46,39 @@ def main():
     lib = _lib.load()
     acc = np.zeros((len(NAMES), 2))
     ph = np.zeros(len(PHASES))
-    for it in range(args.steps + 3):
-        buf = torch.zeros(64,  # TKV_TIMELINE_WORDS
-                           dtype=torch.int64, device=dev)
-        buf[0:2 * len(NAMES):2] = -1  # UINT64_MAX (first-start slots); phase sums stay 0
-        tkv.topk_decode_attention(q, K, V, nc, k, **kw)  # previous step in flight: realistic
-        lib.tkv_debug_timeline(ctypes.c_void_p(buf.data_ptr()))
+    xe = {e: [0.0, 0.0] for e in EXTRA_EVENTS}
+    xp = {e: 0.0 for e in EXTRA_PHASES}
+    buf = torch.zeros(128, dtype=torch.int64, device=dev)  # TKV_TIMELINE_WORDS
+    init = torch.zeros_like(buf)
+    init[0:2 * len(NAMES):2] = -1  # UINT64_MAX (first-start slots); phase sums stay 0
+    for e in EXTRA_EVENTS:
+        init[2 * e] = -1
+    graphs = None
+    if args.graph:
         tkv.topk_decode_attention(q, K, V, nc, k, **kw)
-        lib.tkv_debug_timeline(None)
+        torch.cuda.synchronize()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        plain, timed = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(plain, stream=side):
+                tkv.topk_decode_attention(q, K, V, nc, k, **kw)
+            lib.tkv_debug_timeline(ctypes.c_void_p(buf.data_ptr()))
+            with torch.cuda.graph(timed, stream=side):
+                tkv.topk_decode_attention(q, K, V, nc, k, **kw)
+            lib.tkv_debug_timeline(None)
+        torch.cuda.current_stream().wait_stream(side)
+        graphs = (plain, timed)
+    for it in range(args.steps + 3):
+        buf.copy_(init)
+        if graphs:
+            graphs[0].replay()  # previous step in flight: realistic
+            graphs[1].replay()
+        else:
+            tkv.topk_decode_attention(q, K, V, nc, k, **kw)  # previous step in flight: realistic
+            lib.tkv_debug_timeline(ctypes.c_void_p(buf.data_ptr()))
+            tkv.topk_decode_attention(q, K, V, nc, k, **kw)
+            lib.tkv_debug_timeline(None)
         torch.cuda.synchronize()
         t = buf.cpu().numpy().view(np.uint64).astype(np.float64)
         t0 = t[0]
@@ -58,12 +91,24 @@ def main():
                 s, en = t[2 * e], t[2 * e + 1]
                 acc[e, 0] += (s - t0) / 1e3 if s < 1.8e19 else np.nan
                 acc[e, 1] += (en - t0) / 1e3 if en > 0 else np.nan
+            for e in EXTRA_EVENTS:
+                s, en = t[2 * e], t[2 * e + 1]
+                xe[e][0] += (s - t0) / 1e3 if s < 1.8e19 else np.nan
+                xe[e][1] += (en - t0) / 1e3 if en > 0 else np.nan
+            for e in EXTRA_PHASES:
+                if t[2 * e + 1] > 0:
+                    xp[e] += t[2 * e] / t[2 * e + 1] / 1e3
     acc /= args.steps
     for e, nm in enumerate(NAMES):
         print(f"  {nm:26s} start {acc[e, 0]:8.1f}  end {acc[e, 1]:8.1f} us")
     for j, nm in enumerate(PHASES):
         if ph[j] > 0:
             print(f"  {nm:34s} {ph[j] / args.steps:8.2f} us (mean)")
+    for e, nm in EXTRA_EVENTS.items():
+        print(f"  {nm:34s} first {xe[e][0] / args.steps:8.1f}  last {xe[e][1] / args.steps:8.1f} us")
+    for e, nm in EXTRA_PHASES.items():
+        if xp[e] > 0:
+            print(f"  {nm:34s} {xp[e] / args.steps:8.2f} us (mean)")
 
 
 if __name__ == "__main__":
