@@ -164,22 +164,14 @@ def _device_q(idx: MipsIndex, qv: np.ndarray) -> torch.Tensor:
     return torch.from_numpy(qp).to(idx.device, torch.bfloat16)
 
 
-def order_result(ids: np.ndarray, vals: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
-    """Score-desc / id-asc order of an already exact set (ann.py:166)."""
-    o = np.lexsort((ids, -vals.astype(np.float64)))
-    return ids[o], vals[o]
-
-
 def device_search(idx: MipsIndex, qv: np.ndarray, k: int) -> tuple[np.ndarray, np.ndarray]:
-    """Exact top-min(k, N) on the device; returns (ids int64, vals f32) TopKResult-ordered."""
+    """Exact top-min(k, N) on the device; returns (ids int64, vals f32) TopKResult-ordered
+    (score desc, id asc, ann.py:166 — ordered on the device for every k)."""
     k = min(k, idx.n_keys)
-    sorted_dev = k <= 16384
     q = _device_q(idx, qv)
-    ids_t, sc_t = ops.topk_search(q, idx.k_dev, idx.n_keys, k, sorted=sorted_dev, max_ctx=idx.n_keys)
+    ids_t, sc_t = ops.topk_search(q, idx.k_dev, idx.n_keys, k, sorted=True, max_ctx=idx.n_keys)
     ids = ids_t[0, 0].cpu().numpy().astype(np.int64)
     vals = sc_t[0, 0].cpu().numpy().astype(DTYPE)
-    if not sorted_dev:
-        ids, vals = order_result(ids, vals)
     return ids, vals
 
 

@@ -31,7 +31,7 @@ import numpy as np
 import torch
 
 from . import ops
-from .ann import DTYPE, DeviceValues, MipsIndex, _pad_rows, as_vector, default_scale, device_search, order_result
+from .ann import DTYPE, DeviceValues, MipsIndex, _pad_rows, as_vector, default_scale, device_search
 from .errors import ConfigError, InputError, ShapeError
 
 logger = logging.getLogger(__name__)
@@ -94,13 +94,10 @@ def topk_attend(q, index: MipsIndex, fetch_values, win_keys, win_values, k: int,
             index.k_dev[0, 0, N:N + n_gen] = _to_dev(wk, dev)
             index.v_dev[0, 0, N:N + n_gen] = _to_dev(wv, dev)
         qd = torch.from_numpy(_pad_rows(qv[None, :])[None]).to(dev, torch.bfloat16)
-        sorted_dev = k <= 16384
         out, idx_t, sc_t = ops.topk_decode_attention(
             qd, index.k_dev, index.v_dev, N, k, n_win=n_gen, scale=scale, combine=combine,
-            pinned_prefix=pinned_prefix, sorted=sorted_dev, max_ctx=N)
+            pinned_prefix=pinned_prefix, sorted=True, max_ctx=N)
         ids = idx_t[0, 0].cpu().numpy().astype(np.int64)
-        if not sorted_dev:
-            ids, _ = order_result(ids, sc_t[0, 0].cpu().numpy())
         result = out[0, 0, :d].cpu().numpy().astype(DTYPE)
     else:
         ids, _ = device_search(index, qv, k)

@@ -42,12 +42,21 @@ int fail(int code, const char* fmt, ...) {
     if (e__ != cudaSuccess) return fail(TKV_ECUDA, "%s: %s", #expr, cudaGetErrorString(e__)); \
   } while (0)
 
+// TopKResult ordering (one kernel up to kSortMax, chunk sort + merge passes above)
+#define TKV_SORT(so, nbh, st)                                                          \
+  do {                                                                              \
+    int n__ = 0;                                                                    \
+    cudaError_t e__ = launch_sort((so), (nbh), (st), &n__);                         \
+    g_launches += n__;                                                              \
+    if (e__ != cudaSuccess) return fail(TKV_ECUDA, "launch_sort: %s", cudaGetErrorString(e__)); \
+  } while (0)
+
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct Layout {
   size_t ticket_g, ticket_k, flag, gflag, fbl, ctrl_end;
   size_t maxc, bktc, bkt, outc;
-  size_t cnt, thr, hshift, hist, mmax, mkth, mkb, samp, cand, sidx, sscore, pl, po, pinm, qs, total;
+  size_t cnt, thr, hshift, hist, mmax, mkth, mkb, samp, cand, sidx, sscore, pl, po, pinm, qs, sortb, total;
   int pin_words;
   int64_t cap;
   int nchunks;
@@ -101,6 +110,8 @@ Layout make_layout(const tkv_problem* p) {
   L.qs = take((BH + 2 * BK) * kD * 2);  // TKV_F_HOST_Q staging copies of q | k_new | v_new
   L.pl = take(BH * L.nchunks * 4);
   L.po = take(BH * L.nchunks * kD * 4);
+  // large-k TopKResult ordering (k > kSortMax): merge ping-pong buffers
+  L.sortb = take((p->flags & TKV_F_SORTED) && p->k > kSortMax ? 2 * BH * static_cast<size_t>(p->k) * 8 : 0);
   L.total = off;
   return L;
 }
@@ -126,8 +137,6 @@ int validate(const tkv_problem* p) {
     return fail(TKV_EBADSHAPE, "row_offset=%lld out of range", static_cast<long long>(p->row_offset));
   if (p->combine != TKV_COMBINE_JOINT && p->combine != TKV_COMBINE_ADDITIVE)
     return fail(TKV_ECONFIG, "unknown combine mode %d", p->combine);
-  if ((p->flags & TKV_F_SORTED) && p->k > kSortMax)
-    return fail(TKV_ECONFIG, "sorted output supports k <= %d (got %d)", kSortMax, p->k);
   if (p->pinned_prefix < 0) return fail(TKV_EBADK, "pinned_prefix must be >= 0");
   return TKV_OK;
 }
@@ -421,8 +430,8 @@ int run_emit(const tkv_problem* p, const void* q, const void* k_cache, const voi
     TKV_LAUNCH(launch_attend_cand(a, st));
   }
   if (p->flags & TKV_F_SORTED) {
-    SortParams so{idx, scores, at<int32_t>(ws, L.mkb), p->k, bh_begin};
-    TKV_LAUNCH(launch_sort(so, bh_count, st));
+    SortParams so{idx, scores, at<int32_t>(ws, L.mkb), p->k, bh_begin, at<uint64_t>(ws, L.sortb)};
+    TKV_SORT(so, bh_count, st);
   }
   return TKV_OK;
 }
@@ -479,8 +488,8 @@ int run_head(const tkv_problem* p, const void* q, const void* k_cache, const voi
   hp.ctas_per_head = C < 1 ? 1 : C;
   TKV_LAUNCH(launch_head_topk(hp, st));
   if (p->flags & TKV_F_SORTED) {
-    SortParams so{idx, scores, at<int32_t>(ws, L.mkb), p->k, 0};
-    TKV_LAUNCH(launch_sort(so, nbh, st));
+    SortParams so{idx, scores, at<int32_t>(ws, L.mkb), p->k, 0, at<uint64_t>(ws, L.sortb)};
+    TKV_SORT(so, nbh, st);
   }
   return TKV_OK;
 }
@@ -813,8 +822,8 @@ int tkv_shard_merge_lists(const tkv_problem* p, const uint64_t* gathered, int32_
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   TKV_LAUNCH(launch_select(sl, st));
   if (p->flags & TKV_F_SORTED) {
-    SortParams so{idx, scores, sl.meta_kb, p->k};
-    TKV_LAUNCH(launch_sort(so, p->batch * p->n_q_heads, st));
+    SortParams so{idx, scores, sl.meta_kb, p->k, 0, at<uint64_t>(ws, L.sortb)};
+    TKV_SORT(so, p->batch * p->n_q_heads, st);
   }
   return TKV_OK;
 }

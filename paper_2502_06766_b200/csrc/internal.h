@@ -31,7 +31,7 @@ constexpr int kAttendChunk = 512;    // selected rows per gather CTA (list mode)
 #endif
 constexpr int kCandChunk = TKV_CAND_CHUNK;  // candidates per work item (candidate mode)
 constexpr int kFlatMinRows = 256;           // flat list gather: rows per CTA range, at least
-constexpr int kSortMax = 16384;      // sorted output supported up to this k
+constexpr int kSortMax = 16384;      // one-CTA shared-memory sort up to this k; chunk sort + merge passes above
 constexpr uint32_t kNoFilterShift = 20;  // histogram shift when every score is a candidate
 constexpr int kMinSampleStride = 8;      // small contexts sample at most every 8th row
 constexpr int kMaxParts = 16;            // KV-group parts of the overlapped layer pipeline
@@ -142,7 +142,9 @@ struct SortParams {
   const int32_t* meta_kb;
   int k;
   int bh_begin;
+  uint64_t* buf;  // k > kSortMax: 2 x [heads][k] composites (merge ping-pong), workspace
 };
+constexpr int kSortChunk = 8192;  // k > kSortMax: runs sorted in shared memory, then merged
 
 struct AttendParams {
   uint64_t* tl;  // diagnostics timeline (tkv_debug_timeline), nullptr normally
@@ -250,7 +252,7 @@ cudaError_t launch_kth(const SelectParams& p, cudaStream_t s);
 cudaError_t launch_head_topk(const HeadParams& p, cudaStream_t s);
 cudaError_t launch_attend_cand(const AttendParams& p, cudaStream_t s);
 cudaError_t launch_attend_list(const AttendParams& p, cudaStream_t s);
-cudaError_t launch_sort(const SortParams& p, int nbh, cudaStream_t s);
+cudaError_t launch_sort(const SortParams& p, int nbh, cudaStream_t s, int* launches);
 cudaError_t launch_attend(const AttendParams& p, cudaStream_t s);
 cudaError_t launch_finalize(const AttendParams& p, cudaStream_t s);
 cudaError_t launch_append(const AppendParams& p, cudaStream_t s);

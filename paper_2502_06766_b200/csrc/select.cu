@@ -919,18 +919,106 @@ cudaError_t launch_select(const SelectParams& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_sort(const SortParams& p, int nbh, cudaStream_t s) {
+// k > kSortMax (TopKResult order for large k, ann.py:166): every run of kSortChunk selected rows
+// is bitonic-sorted in shared memory, then log2(k / kSortChunk) merge passes double the runs.
+// A merge pass places each composite directly: its rank in its own run plus the number of
+// larger composites in the partner run (binary search; composites are unique, so ranks never
+// collide). The last pass writes idx / scores.
+__global__ void __launch_bounds__(SNT) sort_chunk_kernel(SortParams p) {
+  extern __shared__ uint64_t s_c[];
+  const int bh = p.bh_begin + blockIdx.y;
+  const int kb = p.meta_kb[bh];
+  const int c0 = blockIdx.x * kSortChunk;
+  if (c0 >= kb) return;
+  const int n = min(kSortChunk, kb - c0);
   int P = 1;
-  const int kmax = p.k < kSortMax ? p.k : kSortMax;
-  while (P < kmax) P <<= 1;
-  const size_t smem = static_cast<size_t>(P) * sizeof(uint64_t);
+  while (P < n) P <<= 1;
+  const int32_t* idx = p.idx + static_cast<int64_t>(bh) * p.k + c0;
+  const float* sc = p.scores + static_cast<int64_t>(bh) * p.k + c0;
+  for (int i = threadIdx.x; i < P; i += SNT)
+    s_c[i] = i < n ? make_comp(score_key(sc[i]), static_cast<uint32_t>(idx[i])) : 0ull;
+  __syncthreads();
+  for (int size = 2; size <= P; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < P / 2; i += SNT) {
+        const int lo = 2 * i - (i & (stride - 1));
+        const int hi = lo + stride;
+        const bool desc = (lo & size) == 0;
+        const uint64_t a = s_c[lo], bb = s_c[hi];
+        if ((a < bb) == desc) {
+          s_c[lo] = bb;
+          s_c[hi] = a;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  uint64_t* dst = p.buf + static_cast<int64_t>(bh) * p.k + c0;
+  for (int i = threadIdx.x; i < n; i += SNT) dst[i] = s_c[i];
+}
+
+__global__ void __launch_bounds__(256) sort_merge_kernel(SortParams p, const uint64_t* __restrict__ src,
+                                                         uint64_t* __restrict__ dst, int L, int last) {
+  const int bh = p.bh_begin + blockIdx.y;
+  const int kb = p.meta_kb[bh];
+  const int i = blockIdx.x * 256 + threadIdx.x;
+  if (i >= kb) return;
+  const uint64_t* run = src + static_cast<int64_t>(bh) * p.k;
+  const uint64_t x = run[i];
+  const int r = i / L, own = i - r * L;
+  const int ps = (r ^ 1) * L;
+  int larger = 0;
+  if (ps < kb) {  // partner run [ps, pe), descending: count its elements > x
+    int lo = ps, hi = min(ps + L, kb);
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (run[mid] > x) lo = mid + 1; else hi = mid;
+    }
+    larger = lo - ps;
+  }
+  const int pos = (r & ~1) * L + own + larger;
+  if (last) {
+    p.idx[static_cast<int64_t>(bh) * p.k + pos] = static_cast<int32_t>(comp_gid(x));
+    p.scores[static_cast<int64_t>(bh) * p.k + pos] = key_score(comp_key(x));
+  } else {
+    dst[static_cast<int64_t>(bh) * p.k + pos] = x;
+  }
+}
+
+cudaError_t launch_sort(const SortParams& p, int nbh, cudaStream_t s, int* launches) {
   per_device(reinterpret_cast<const void*>(sort_kernel), 0, [] {
     cudaFuncSetAttribute(sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(kSortMax * sizeof(uint64_t)));
+    cudaFuncSetAttribute(sort_chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kSortChunk * sizeof(uint64_t)));
     return 1;
   });
-  sort_kernel<<<nbh, SNT, smem, s>>>(p);
-  return cudaGetLastError();
+  *launches = 0;
+  if (p.k <= kSortMax) {
+    int P = 1;
+    while (P < p.k) P <<= 1;
+    sort_kernel<<<nbh, SNT, static_cast<size_t>(P) * sizeof(uint64_t), s>>>(p);
+    *launches = 1;
+    return cudaGetLastError();
+  }
+  if (!p.buf) return cudaErrorInvalidValue;
+  const int nchunk = (p.k + kSortChunk - 1) / kSortChunk;
+  sort_chunk_kernel<<<dim3(nchunk, nbh), SNT, kSortChunk * sizeof(uint64_t), s>>>(p);
+  *launches = 1;
+  cudaError_t e = cudaGetLastError();
+  // ping-pong: run buffer a at buf + bh * k, b shifted past every head this call covers
+  uint64_t* a = p.buf;
+  uint64_t* b = p.buf + static_cast<int64_t>(p.bh_begin + nbh) * p.k;
+  for (int L = kSortChunk; e == cudaSuccess && L < p.k; L <<= 1) {
+    const int last = 2 * L >= p.k;
+    sort_merge_kernel<<<dim3((p.k + 255) / 256, nbh), 256, 0, s>>>(p, a, b, L, last);
+    ++*launches;
+    e = cudaGetLastError();
+    uint64_t* t = a;
+    a = b;
+    b = t;
+  }
+  return e;
 }
 
 // Narrow-exchange exactness rule (paper_2502_06766_b200/sharded.py narrow_exchange_exact), one

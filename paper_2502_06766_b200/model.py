@@ -120,6 +120,7 @@ class TopkLlamaDecoder:
         self.ws = ops.Workspace(prob, dev)
         self.token = torch.zeros(1, dtype=torch.int64, device=dev)
         self.next_token = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.logits = torch.zeros((1, s.vocab), dtype=torch.float32, device=dev)  # last step's
         self.attn_out = torch.empty((1, s.n_heads, s.head_dim), dtype=torch.float32, device=dev)
         self._sel = {kl: (torch.empty((1, s.n_heads, kl), dtype=torch.int32, device=dev),
                           torch.empty((1, s.n_heads, kl), dtype=torch.float32, device=dev))
@@ -164,6 +165,7 @@ class TopkLlamaDecoder:
         for layer, lw in enumerate(self.layers):
             x = self._layer(x, lw, layer)
         logits = rmsnorm(x, self.norm_f, self.shape.eps) @ self.lm_head
+        self.logits.copy_(logits)
         self.next_token.copy_(logits.argmax(-1))
         self.n_win.add_(1)
         self.pos.add_(1)

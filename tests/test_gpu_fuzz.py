@@ -25,7 +25,7 @@ def _config(seed: int):
     combine = str(r.choice(["joint", "additive"]))
     n_ctx = [N] + [int(r.integers(1, N + 1)) for _ in range(B - 1)]
     opts = dict(
-        sorted=bool(r.random() < 0.3) and k <= 16384,
+        sorted=bool(r.random() < 0.3),
         parts=int(r.choice([0, 0, 2, 3])),
         list_gather=bool(r.random() < 0.3),
         tc_scan=bool(r.random() < 0.8),

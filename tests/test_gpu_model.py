@@ -27,11 +27,15 @@ def test_k_equals_n_matches_dense_reference(cuda):
         dec.token.fill_(tok)
         dec._step_body()
         torch.cuda.synchronize()
-        # our logits (recompute from the step's final state is not kept) → compare next token
-        # through the reference's argmax and the logits' correlation on a re-run of the layer stack
         assert int(dec.n_win.item()) == step + 1
+        # logits: the step computes its projections / MLP in bf16 (fp32 accumulate), the reference
+        # in fp32 with the same bf16 roundings of q/k/v and the attention output, so the
+        # difference is bf16 rounding of the activations: <= 2 % of the logits' range
+        err = float((dec.logits[0] - ref[0]).abs().max())
+        span = float(ref[0].abs().max())
+        assert err <= 2e-2 * span + 1e-3, (err, span)
         top = torch.topk(ref[0], 2).values
-        if float(top[0] - top[1]) > 1e-2:  # skip near-tied argmax
+        if float(top[0] - top[1]) > 3e-2 * span:  # argmax agrees unless near-tied
             assert int(dec.next_token.item()) == int(ref[0].argmax().item())
 
 
