@@ -71,9 +71,6 @@ extern "C" {
                               workspace, so a host-I/O step needs no H2D copy of its inputs      */
 #define TKV_F_HEAD 32u     /* k-th + V gather by the per-head kernel (head_topk_kernel) at any k   */
 #define TKV_F_NO_HEAD 64u  /* never the per-head kernel (automatic: k <= 1024, one part)          */
-#define TKV_F_GROUP 4096u    /* small-context path forced: one thread-block cluster per (b, kv head) does \
-                                scan + exact selection + gather (group.cu; automatic when it fits)  */
-#define TKV_F_NO_GROUP 8192u /* never the small-context cluster path                                  */
 #define TKV_F_SCAN_HMMA 8u /* key scan on register-staged mma.sync (scan.cu) instead of the TMA +  
                               tcgen05 pipeline (scan_tc.cu, the default)                         */
 
@@ -195,13 +192,6 @@ int tkv_shard_finalize(const tkv_problem* p, const void* q, const void* k_cache,
  * (header validation, section offsets, staging) is paper_2502_06766_b200/cache.py.
  */
 int tkv_convert_rows_f32(const float* src, int64_t rows, int32_t d, void* dst, void* stream);
-
-/*
- * The small-context plan for problem p on the current device (TKV_F_GROUP / automatic): the
- * cluster size (0 = the multi-kernel pipeline runs), rows per CTA, and how many such clusters
- * can be resident at once. Any output pointer may be NULL.
- */
-int tkv_group_plan(const tkv_problem* p, int32_t* cluster_size, int32_t* rows_per_cta, int32_t* resident_clusters);
 
 /* Number of kernels the last compute call on this thread enqueued (for launch accounting). */
 int tkv_last_launch_count(void);

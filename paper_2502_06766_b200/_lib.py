@@ -36,7 +36,6 @@ EXPORTS = (
     "tkv_shard_partial",
     "tkv_shard_finalize",
     "tkv_last_launch_count",
-    "tkv_group_plan",
     "tkv_profile_scan_events",
     "tkv_debug_timeline",
     "tkv_convert_rows_f32",
@@ -52,8 +51,6 @@ F_GATHER_LIST = 16
 F_HEAD = 32
 F_NO_HEAD = 64
 F_HOST_Q = 128
-F_GROUP = 4096
-F_NO_GROUP = 8192
 
 
 class Problem(ctypes.Structure):
@@ -85,7 +82,6 @@ _SIG = {
     "tkv_last_error": ([], ctypes.c_char_p),
     "tkv_device_check": ([], _I),
     "tkv_last_launch_count": ([], _I),
-    "tkv_group_plan": ([ctypes.POINTER(Problem), _P, _P, _P], _I),
     "tkv_profile_scan_events": ([_P, _P], _I),
     "tkv_debug_timeline": ([_P], _I),
     "tkv_convert_rows_f32": ([_P, ctypes.c_int64, ctypes.c_int32, _P, _P], _I),
@@ -160,13 +156,6 @@ def call(name: str, *args) -> None:
 
 def launches() -> int:
     return int(load().tkv_last_launch_count())
-
-
-def group_plan(p: Problem) -> tuple[int, int, int]:
-    """(cluster size, rows per CTA, resident clusters) of the small-context path (0 = pipeline)."""
-    v = [ctypes.c_int32(0) for _ in range(3)]
-    check(load().tkv_group_plan(ctypes.byref(p), *[ctypes.byref(x) for x in v]))
-    return tuple(int(x.value) for x in v)
 
 
 def workspace_bytes(p: Problem) -> int:

@@ -54,7 +54,7 @@ int fail(int code, const char* fmt, ...) {
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct Layout {
-  size_t ticket_g, ticket_k, flag, gflag, fbl, wtk, ctrl_end;
+  size_t ticket_g, ticket_k, flag, gflag, fbl, ctrl_end;
   size_t maxc, bktc, bkt, outc;
   size_t cnt, thr, hshift, hist, mmax, mkth, mkb, samp, cand, sidx, sscore, pl, po, pinm, qs, sortb, total;
   int pin_words;
@@ -77,7 +77,6 @@ Layout make_layout(const tkv_problem* p) {
   L.flag = take(BH * 4);
   L.gflag = take(BK * 4);
   L.fbl = take(4 * kMaxParts);
-  L.wtk = take(static_cast<size_t>(p->batch) * 4);  // group path: window-advance tickets
   L.ctrl_end = off;
   L.cnt = take(BH * 4);
   L.thr = take(BH * 4);
@@ -101,8 +100,7 @@ Layout make_layout(const tkv_problem* p) {
     const int64_t c = (L.cap + kCandChunk - 1) / kCandChunk + 1;
     const int64_t f = (p->k + kFlatMinRows - 1) / kFlatMinRows + 1;  // flat list gather ranges
     int64_t m = a > c ? a : c;
-    m = m > f ? m : f;
-    L.nchunks = static_cast<int>(m > 16 ? m : 16);  // >= the group path's cluster size
+    L.nchunks = static_cast<int>(m > f ? m : f);
   }
   {
     const int64_t pin = p->pinned_prefix < p->max_ctx ? p->pinned_prefix : p->max_ctx;
@@ -496,70 +494,7 @@ int run_head(const tkv_problem* p, const void* q, const void* k_cache, const voi
   return TKV_OK;
 }
 
-// Small-context path (group.cu): cluster size and rows per CTA when the whole step fits one
-// cluster per (b, kv head) with every score in shared memory; 0 when it does not.
-struct GroupShape {
-  int cs = 0, rows = 0, resident = 0;
-};
-GroupShape group_shape(const tkv_problem* p) {
-  GroupShape gs;
-  if (p->flags & (TKV_F_NO_GROUP | TKV_F_HEAD | TKV_F_GATHER_LIST)) return gs;
-  const int G = p->n_q_heads / p->n_kv_heads;
-  const int64_t n = p->max_ctx;
-  const int64_t clusters = static_cast<int64_t>(p->batch) * p->n_kv_heads;
-  for (int cs = 16; cs >= 4; cs >>= 1) {
-    int64_t r = (n + cs - 1) / cs;
-    r = (r + 31) / 32 * 32;
-    if (r < 32) r = 32;
-    if (r > group_max_rows(G)) break;  // smaller clusters only need more rows per CTA
-    const int resident = group_cluster_ok(cs, group_smem_bytes(G, static_cast<int>(r), cs));
-    if (resident < 1) continue;
-    // automatic only when every cluster of the call is resident at once (one wave: a second
-    // wave doubles the step) and the clusters keep enough SMs streaming keys
-    if (!(p->flags & TKV_F_GROUP) && (resident < clusters || clusters * cs < device_sm_count() / 2)) continue;
-    gs.cs = cs;
-    gs.rows = static_cast<int>(r);
-    gs.resident = resident;
-    return gs;
-  }
-  return gs;
-}
-
-int run_group(const tkv_problem* p, const GroupShape& gs, const void* q, const void* k_cache, const void* v_cache,
-              const int32_t* n_ctx, const int32_t* n_win, int32_t* idx, float* scores, uint64_t* packed, float* out,
-              int gather, void* ws, const Layout& L, cudaStream_t st) {
-  GroupParams gp{};
-  gp.a = make_attend(p, q, k_cache, v_cache, n_ctx, n_win, idx, scores, ws, L);
-  gp.a.idx_out = idx;
-  gp.a.scores_out = scores;
-  gp.a.packed_out = packed;
-  gp.a.out = out;
-  gp.a.gather = gather;
-  gp.a.partial_only = 0;
-  gp.cs = gs.cs;
-  gp.rows_per_cta = gs.rows;
-  gp.max_ctx = p->max_ctx;
-  if (g_fold.k_new) {  // decode step: the window append happens inside the kernel
-    gp.k_new = static_cast<const __nv_bfloat16*>(g_fold.k_new);
-    gp.v_new = static_cast<const __nv_bfloat16*>(g_fold.v_new);
-    gp.k_dst = static_cast<__nv_bfloat16*>(g_fold.k_cache);
-    gp.v_dst = static_cast<__nv_bfloat16*>(g_fold.v_cache);
-    gp.win_count = g_fold.n_win;
-    gp.win_ticket = at<uint32_t>(ws, L.wtk);
-    gp.a.win_extra = 1;
-  }
-  g_fold = AppendFold{};
-  if (g_scan_start && g_scan_stop) cudaEventRecord(g_scan_start, st);
-  TKV_LAUNCH(launch_group(gp, st));
-  if (g_scan_start && g_scan_stop) cudaEventRecord(g_scan_stop, st);
-  if (p->flags & TKV_F_SORTED) {
-    SortParams so{idx, scores, at<int32_t>(ws, L.mkb), p->k, 0, at<uint64_t>(ws, L.sortb)};
-    TKV_SORT(so, p->batch * p->n_q_heads, st);
-  }
-  return TKV_OK;
-}
-
-// The whole layer step (multi-kernel pipeline, or the small-context cluster path).
+// The whole layer step (multi-kernel pipeline).
 int run_layer_dev(const tkv_problem* p, const void* q, const void* k_cache, const void* v_cache,
                   const int32_t* n_ctx, const int32_t* n_win, int32_t* idx, float* scores,
                   uint64_t* packed, float* out, int gather, void* ws, const Layout& L, cudaStream_t st);
@@ -600,11 +535,6 @@ int run_layer_dev(const tkv_problem* p, const void* q, const void* k_cache, cons
                   const int32_t* n_ctx, const int32_t* n_win, int32_t* idx, float* scores,
                   uint64_t* packed, float* out, int gather, void* ws, const Layout& L, cudaStream_t st) {
   {
-    const GroupShape gs = group_shape(p);
-    if ((p->flags & TKV_F_GROUP) && !gs.cs)
-      return fail(TKV_ECONFIG, "TKV_F_GROUP: the small-context cluster path does not fit this problem (max_ctx=%lld, G=%d)",
-                  static_cast<long long>(p->max_ctx), p->n_q_heads / p->n_kv_heads);
-    if (gs.cs) return run_group(p, gs, q, k_cache, v_cache, n_ctx, n_win, idx, scores, packed, out, gather, ws, L, st);
     ScanParams cp;
     SelectParams sl;
     TRY(run_prefix(p, q, k_cache, n_ctx, ws, L, st, &cp, &sl));
@@ -682,15 +612,6 @@ int run_layer_dev(const tkv_problem* p, const void* q, const void* k_cache, cons
 extern "C" {
 
 int tkv_version(void) { return TKV_VERSION; }
-
-int tkv_group_plan(const tkv_problem* p, int32_t* cluster_size, int32_t* rows_per_cta, int32_t* resident_clusters) {
-  TRY(validate(p));
-  const GroupShape gs = group_shape(p);
-  if (cluster_size) *cluster_size = gs.cs;
-  if (rows_per_cta) *rows_per_cta = gs.rows;
-  if (resident_clusters) *resident_clusters = gs.resident;
-  return TKV_OK;
-}
 
 const char* tkv_last_error(void) { return g_err.c_str(); }
 

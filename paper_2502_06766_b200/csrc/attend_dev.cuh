@@ -150,7 +150,7 @@ __device__ void finalize_head(const AttendParams& p, int b, int h, int kvh, int6
   const int bh = b * p.Hq + h;
   // precondition n_ctx + n_win <= cache_rows (tkv.h); a window past the cache is clamped
   // rather than read from the next head's rows
-  int64_t nwin = (p.n_win ? p.n_win[b] : 0) + p.win_extra;
+  int64_t nwin = p.n_win ? p.n_win[b] : 0;
   if (nwin > p.cache_rows - nctx) nwin = p.cache_rows - nctx;
   float m_w = -INFINITY, l_w = 0.f, o_w = 0.f;
   if (nwin > 0)

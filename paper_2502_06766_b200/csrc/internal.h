@@ -187,7 +187,6 @@ struct AttendParams {
   uint32_t* pin_mask;  // [B*Hq][pin_words] or nullptr
   int pin_words;
   int bh_begin, bh_count;  // heads handled by attend_cand_kernel; bh_count 0 = all B*Hq
-  int win_extra;           // window rows beyond n_win[b] (1: this call appends the token's row)
 };
 
 // head_topk_kernel (select.cu): k-th selection + V gather + finish of a head by ctas_per_head
@@ -201,31 +200,6 @@ struct HeadParams {
   int ctas_per_head;  // <= nchunks (partial slots)
   int att_grid;
 };
-
-// group_topk_kernel (group.cu): the whole layer step of one (b, kv head) — its G q heads — by
-// one thread-block cluster of `cs` CTAs (small contexts: every score stays in shared memory).
-constexpr int kGrpThreads = 512;
-constexpr int kGrpBins = 2048;        // 11-bit radix digits
-constexpr int kGrpKeyBytes = 128 * 1024;  // shared-memory score keys per CTA: G x rows_per_cta x 4 B
-struct GroupParams {
-  AttendParams a;  // problem, caches, outputs, partial slots (slot = cluster rank), pin mask
-  int cs;            // CTAs per cluster: 2, 4, 8 or 16
-  int rows_per_cta;  // multiple of 32, G x rows_per_cta x 4 <= kGrpKeyBytes
-  int64_t max_ctx;
-  // optional window append (tkv_topk_decode_step): rows n_ctx[b] + win_count[b] of K/V <-
-  // k_new / v_new[b]; the call attends with that row (a.win_extra = 1) and the last cluster of
-  // batch entry b to finish advances win_count[b]
-  const __nv_bfloat16* k_new;
-  const __nv_bfloat16* v_new;
-  __nv_bfloat16* k_dst;
-  __nv_bfloat16* v_dst;
-  int32_t* win_count;
-  uint32_t* win_ticket;  // [B], self-resetting
-};
-size_t group_smem_bytes(int G, int rows_per_cta, int cs);
-int group_max_rows(int G);
-cudaError_t launch_group(const GroupParams& p, cudaStream_t s);
-int group_cluster_ok(int cs, size_t smem);  // clusters of cs CTAs that can be resident (0: none)
 
 struct AppendParams {
   int B, Hkv;

@@ -25,7 +25,7 @@ class TopkDecoder:
                  n_win=0, scale: float | None = None, combine: str = "joint",
                  pinned_prefix: int = 0, sorted: bool = False, max_ctx: int | None = None,
                  use_graph: bool = True, parts: int = 0, list_gather: bool = False,
-                 head: bool | None = None, group: bool | None = None, fold_append: bool = True):
+                 head: bool | None = None, fold_append: bool = True):
         if k < 1:
             raise InputError("k must be >= 1")
         ops._check_cuda_bf16("k_cache", k_cache, 4)
@@ -44,7 +44,7 @@ class TopkDecoder:
         self.max_ctx = int(max_ctx if max_ctx is not None else self.rows)
         self.k = k
         self.kw = dict(scale=scale, combine=combine, pinned_prefix=pinned_prefix, sorted=sorted,
-                       max_ctx=self.max_ctx, parts=parts, list_gather=list_gather, head=head, group=group)
+                       max_ctx=self.max_ctx, parts=parts, list_gather=list_gather, head=head)
         ops.combine_code(combine)
         self.use_graph = use_graph
         self.fold_append = fold_append
@@ -64,7 +64,7 @@ class TopkDecoder:
                                 pinned_prefix=self.kw["pinned_prefix"], scale=self.kw["scale"],
                                 combine=self.kw["combine"], sorted=self.kw["sorted"],
                                 parts=self.kw["parts"], list_gather=self.kw["list_gather"],
-                                head=self.kw["head"], group=self.kw["group"])
+                                head=self.kw["head"])
         self.ws = ops.Workspace(prob, dev)
         D = ops.HEAD_DIM
         bf, f32, i32 = torch.bfloat16, torch.float32, torch.int32

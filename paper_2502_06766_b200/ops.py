@@ -45,7 +45,7 @@ def make_problem(B: int, Hq: int, Hkv: int, cache_rows: int, max_ctx: int, k: in
                  sorted: bool = False, no_filter: bool = False, row_offset: int = 0,
                  head_dim: int = HEAD_DIM,
                  tc_scan: bool | None = None, parts: int = 0, list_gather: bool = False,
-                 head: bool | None = None, host_q: bool = False, group: bool | None = None) -> _lib.Problem:
+                 head: bool | None = None, host_q: bool = False) -> _lib.Problem:
     p = _lib.Problem()
     p.batch, p.n_q_heads, p.n_kv_heads, p.head_dim = B, Hq, Hkv, head_dim
     p.cache_rows, p.max_ctx, p.k = cache_rows, max_ctx, k
@@ -66,8 +66,6 @@ def make_problem(B: int, Hq: int, Hkv: int, cache_rows: int, max_ctx: int, k: in
         p.flags |= _lib.F_HEAD if head else _lib.F_NO_HEAD
     if host_q:  # q in pinned host memory, staged on device inside the call
         p.flags |= _lib.F_HOST_Q
-    if group is not None:  # small-context cluster path forced on / off (None: automatic)
-        p.flags |= _lib.F_GROUP if group else _lib.F_NO_GROUP
     p.row_offset = row_offset
     return p
 
@@ -166,7 +164,7 @@ def topk_decode_attention(q, k_cache, v_cache, n_ctx, k: int, *, n_win=None, sca
                           max_ctx: int | None = None, no_filter: bool = False, row_offset: int = 0,
                           out=None, idx=None, scores=None, workspace: Workspace | None = None,
                           tc_scan: bool | None = None, parts: int = 0,
-                          list_gather: bool = False, head: bool | None = None, group: bool | None = None):
+                          list_gather: bool = False, head: bool | None = None):
     """Exact top-k decode attention for every (batch, q head) of one layer.
 
     q [B, Hq, 128] bf16; k_cache/v_cache [B, Hkv, rows, 128] bf16 with the context in rows
@@ -185,7 +183,7 @@ def topk_decode_attention(q, k_cache, v_cache, n_ctx, k: int, *, n_win=None, sca
     prob = make_problem(s.B, s.Hq, s.Hkv, s.cache_rows, max_ctx, k, pinned_prefix=pinned_prefix,
                         scale=scale, combine=combine, sorted=sorted, no_filter=no_filter,
                         row_offset=row_offset, tc_scan=tc_scan, parts=parts,
-                        list_gather=list_gather, head=head, group=group,
+                        list_gather=list_gather, head=head,
                         host_q=not q.is_cuda)
     ws = workspace or workspace_for(prob, dev)
     out = out if out is not None else torch.empty((s.B, s.Hq, HEAD_DIM), dtype=torch.float32, device=dev)
@@ -201,8 +199,7 @@ def topk_decode_step(q, k_new, v_new, k_cache, v_cache, n_ctx, n_win, k: int, *,
                      combine: str = "joint", pinned_prefix: int = 0, sorted: bool = False,
                      max_ctx: int | None = None, out=None, idx=None, scores=None,
                      workspace: Workspace | None = None, tc_scan: bool | None = None,
-                     parts: int = 0, list_gather: bool = False, head: bool | None = None,
-                     group: bool | None = None):
+                     parts: int = 0, list_gather: bool = False, head: bool | None = None):
     """One decode step of one layer (decode_step, attention.py:203-230): append this token's
     k_new/v_new [B, Hkv, 128] to the window (GenWindow.append, attention.py:210; n_win is a
     device int32 counter advanced in place) and attend over context + window, in one call."""
@@ -221,7 +218,7 @@ def topk_decode_step(q, k_new, v_new, k_cache, v_cache, n_ctx, n_win, k: int, *,
         max_ctx = s.cache_rows if isinstance(n_ctx, torch.Tensor) else int(n_ctx_t.max().item())
     prob = make_problem(s.B, s.Hq, s.Hkv, s.cache_rows, max_ctx, k, pinned_prefix=pinned_prefix,
                         scale=scale, combine=combine, sorted=sorted, tc_scan=tc_scan,
-                        parts=parts, list_gather=list_gather, head=head, group=group,
+                        parts=parts, list_gather=list_gather, head=head,
                         host_q=not q.is_cuda)
     ws = workspace or workspace_for(prob, dev)
     out = out if out is not None else torch.empty((s.B, s.Hq, HEAD_DIM), dtype=torch.float32, device=dev)
@@ -234,8 +231,7 @@ def topk_decode_step(q, k_new, v_new, k_cache, v_cache, n_ctx, n_win, k: int, *,
 
 def topk_search(q, k_cache, n_ctx, k: int, *, sorted: bool = True, max_ctx: int | None = None,
                 no_filter: bool = False, row_offset: int = 0, workspace: Workspace | None = None,
-                tc_scan: bool | None = None, parts: int = 0, head: bool | None = None,
-                group: bool | None = None):
+                tc_scan: bool | None = None, parts: int = 0, head: bool | None = None):
     """Exact top-k rows per (batch, q head) without attention (knn_search flat, ann.py:203-218).
 
     Returns (idx [B, Hq, k] int32, scores [B, Hq, k] f32), TopKResult-ordered when sorted.
@@ -249,7 +245,7 @@ def topk_search(q, k_cache, n_ctx, k: int, *, sorted: bool = True, max_ctx: int 
         max_ctx = s.cache_rows if isinstance(n_ctx, torch.Tensor) else int(n_ctx_t.max().item())
     prob = make_problem(s.B, s.Hq, s.Hkv, s.cache_rows, max_ctx, k, sorted=sorted,
                         no_filter=no_filter, row_offset=row_offset, tc_scan=tc_scan,
-                        parts=parts, head=head, group=group, host_q=not q.is_cuda)
+                        parts=parts, head=head, host_q=not q.is_cuda)
     ws = workspace or workspace_for(prob, dev)
     idx = torch.empty((s.B, s.Hq, k), dtype=torch.int32, device=dev)
     scores = torch.empty((s.B, s.Hq, k), dtype=torch.float32, device=dev)

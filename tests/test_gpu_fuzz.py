@@ -32,8 +32,6 @@ def _config(seed: int):
         no_filter=bool(r.random() < 0.15),
         head=True if r.random() < 0.25 else None,  # force the per-head k-th + gather kernel
     )
-    # small-context cluster path: forced / automatic / off (drawn last: earlier draws unchanged)
-    opts["group"] = [True, None, False][int(r.integers(0, 3))]
     return B, G * Hkv, Hkv, N, k, W, pin, combine, n_ctx, opts
 
 

@@ -13,7 +13,6 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--scan", choices=["tc", "hmma"], default="tc")
     ap.add_argument("--label", default="")
-    ap.add_argument("--group", choices=["auto", "on", "off"], default="auto")
     args = ap.parse_args()
     args.tc = args.scan == "tc"
     import torch
@@ -30,10 +29,9 @@ def main():
     out = torch.empty((B, 32, 128), dtype=torch.float32, device=dev)
     idx = torch.empty((B, 32, k), dtype=torch.int32, device=dev)
     sc = torch.empty((B, 32, k), dtype=torch.float32, device=dev)
-    group = {"auto": None, "on": True, "off": False}[args.group]
-    prob = tkv.ops.make_problem(B, 32, 8, K.shape[2], n, k, tc_scan=args.tc, group=group)
+    prob = tkv.ops.make_problem(B, 32, 8, K.shape[2], n, k, tc_scan=args.tc)
     ws = tkv.Workspace(prob, dev)
-    kw = dict(max_ctx=n, out=out, idx=idx, scores=sc, workspace=ws, tc_scan=args.tc, group=group)
+    kw = dict(max_ctx=n, out=out, idx=idx, scores=sc, workspace=ws, tc_scan=args.tc)
     for _ in range(5):
         tkv.topk_decode_attention(q, K, V, nc, k, **kw)
     torch.cuda.synchronize()
@@ -75,7 +73,7 @@ def main():
     lib.tkv_profile_scan_events(None, None)
     scan = sum(a.elapsed_time(b) for a, b in ev) / args.steps * 1e3
     kbytes = B * 8 * n * 128 * 2
-    print(f"{args.config} tc={int(args.tc)} group={args.group} {args.label}: step {step:.1f} us (graph replay {step_graph:.1f} us), scan {scan:.1f} us "
+    print(f"{args.config} tc={int(args.tc)} {args.label}: step {step:.1f} us (graph replay {step_graph:.1f} us), scan {scan:.1f} us "
           f"({kbytes / scan / 1e3:.0f} GB/s)", flush=True)
 
 

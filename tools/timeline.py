@@ -21,10 +21,7 @@ PHASES = ["head CTA: start→params", "→hist+bucket", "→pass 1 (max, bucket 
 
 EXTRA_EVENTS = {40: "scan CTA start", 41: "scan CTA end", 45: "threshold CTA past wait"}
 EXTRA_PHASES = {42: "scan epilogue: wait for a unit's scores", 43: "scan epilogue: ld+emit of a unit",
-                44: "scan MMA warp: wait for a unit's TMA", 46: "scan CTA lifetime",
-                47: "group CTA: start→scan done", 48: "group: →radix levels", 49: "group: →members/T",
-                50: "group: →counts + cluster prefix", 51: "group: →emit + gather", 52: "group: →partials + barrier",
-                53: "group owner: →finish"}
+                44: "scan MMA warp: wait for a unit's TMA", 46: "scan CTA lifetime"}
 
 
 def main():
@@ -32,7 +29,6 @@ def main():
     ap.add_argument("--config", default="cfg3")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--graph", action="store_true", help="replay the step as a CUDA graph (no host launch gaps)")
-    ap.add_argument("--group", choices=["auto", "on", "off"], default="auto")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -46,7 +42,7 @@ def main():
     q, K, V, n = bench.make_inputs(cfg, cfg["N"] + 8, 0, dev)
     B, k = cfg["B"], cfg["k"]
     nc = torch.full((B,), n, dtype=torch.int32, device=dev)
-    kw = dict(max_ctx=n, group={"auto": None, "on": True, "off": False}[args.group])
+    kw = dict(max_ctx=n)
     lib = _lib.load()
     acc = np.zeros((len(NAMES), 2))
     ph = np.zeros(len(PHASES))
