@@ -95,9 +95,9 @@ Layout make_layout(const tkv_problem* p) {
   L.sidx = take(BH * static_cast<size_t>(p->k) * 4);
   L.sscore = take(BH * static_cast<size_t>(p->k) * 4);
   {
-    // partial slots per head: list mode (k / kAttendChunk) or candidate mode (cap / kCandChunk)
+    // partial slots per head: list mode (k / kAttendChunk) or candidate mode (cap / kCandQuant)
     const int64_t a = (p->k + kAttendChunk - 1) / kAttendChunk;
-    const int64_t c = (L.cap + kCandChunk - 1) / kCandChunk + 1;
+    const int64_t c = (L.cap + kCandQuant - 1) / kCandQuant + 1;
     const int64_t f = (p->k + kFlatMinRows - 1) / kFlatMinRows + 1;  // flat list gather ranges
     int64_t m = a > c ? a : c;
     L.nchunks = static_cast<int>(m > f ? m : f);

@@ -16,15 +16,18 @@ __device__ __forceinline__ void attend_cand_run(const AttendParams& p, AttSmem& 
   if (threadIdx.x == 0) tl_start(p.tl, 6);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int BH = p.bh_count ? p.bh_count : p.B * p.Hq;  // heads [bh_begin, bh_begin + BH)
-  auto chunks_of = [&](int lh) -> int {  // 1024-candidate chunks of a head
+  auto chunks_of = [&](int lh) -> int {  // kCandQuant-candidate quanta of a head
     int64_t n = p.cand_cnt[p.bh_begin + lh];
     if (n > p.cap) n = p.cap;
-    return static_cast<int>((n + kCandChunk - 1) / kCandChunk);
+    return static_cast<int>((n + kCandQuant - 1) / kCandQuant);
   };
-  // Work items: S consecutive chunks of one head, S = ceil(total chunks / grid), so the items
-  // fill the grid about once (the per-item fixed costs — candidate load, compaction, partial
-  // write, head ticket — are paid per S chunks, not per chunk). Every head gets >= 1 item so
-  // its output is always finalised. Exclusive prefix of items per head (block-wide).
+  // Work items: S consecutive quanta (256 candidates) of one head, S = ceil(total quanta /
+  // grid), so the items fill the grid about once (the per-item fixed costs — candidate load,
+  // compaction, partial write, head ticket — are paid per S quanta); an item's candidates go
+  // through the compaction + gather loop in batches of up to kCandChunk. Small selections
+  // (cfg2: ~4K candidates per head) thus spread over ~all CTAs instead of one item per 1024
+  // candidates. Every head gets >= 1 item so its output is always finalised. Exclusive prefix
+  // of items per head (block-wide).
   const int per = (BH + NT - 1) / NT;
   uint32_t csum = 0;
   for (int j = 0; j < per; ++j) {
@@ -98,10 +101,11 @@ __device__ __forceinline__ void attend_cand_run(const AttendParams& p, AttSmem& 
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[j] = 0.f;
     float lw = 0.f;
-    const int c_end = min(static_cast<int>((n + kCandChunk - 1) / kCandChunk), (slot + 1) * S);
-    for (int ch = slot * S; ch < c_end; ++ch) {
-      const uint64_t* src = p.cand + static_cast<int64_t>(bh) * p.cap + static_cast<int64_t>(ch) * kCandChunk;
-      int64_t cnt = n - static_cast<int64_t>(ch) * kCandChunk;
+    int64_t c_end = static_cast<int64_t>(slot + 1) * S * kCandQuant;
+    c_end = c_end < n ? c_end : n;
+    for (int64_t c0 = static_cast<int64_t>(slot) * S * kCandQuant; c0 < c_end; c0 += kCandChunk) {
+      const uint64_t* src = p.cand + static_cast<int64_t>(bh) * p.cap + c0;
+      int64_t cnt = c_end - c0;
       cnt = cnt > kCandChunk ? kCandChunk : cnt;
       constexpr int PER = kCandChunk / NT;
       uint64_t cv[PER];

@@ -206,6 +206,37 @@ __device__ __forceinline__ T block_rank_select(const T* vals, int m, int need, T
   return r;
 }
 
+// Same contract as block_rank_select, with the compare loop split over P = NT / m threads per
+// element (P a power of two <= 32, the element's threads adjacent lanes) so that small sets
+// (a few hundred elements) take a few hundred cycles instead of m dependent shared loads.
+template <int NT, typename T, class Gp = CtaGrp>
+__device__ __forceinline__ T block_rank_select_par(const T* vals, int m, int need, T* out) {
+  if (m > NT / 2) return block_rank_select<NT, T, Gp>(vals, m, need, out);
+  int P = 1;
+  while (P < 32 && P * 2 * m <= NT) P <<= 1;
+  const int tid = Gp::tid();
+  const int i = tid / P, sub = tid % P;
+  int gt = 0, ge = 0;
+  T v{};
+  if (i < m) {
+    v = vals[i];
+    for (int j = sub; j < m; j += P) {
+      const T w = vals[j];
+      gt += w > v;
+      ge += w >= v;
+    }
+  }
+  for (int o = 1; o < P; o <<= 1) {  // the P threads of element i are lanes of one warp
+    gt += __shfl_xor_sync(kFull, gt, o);
+    ge += __shfl_xor_sync(kFull, ge, o);
+  }
+  if (i < m && sub == 0 && gt < need && need <= ge) *out = v;
+  Gp::sync();
+  const T r = *out;
+  Gp::sync();
+  return r;
+}
+
 // ---------------------------------------------------------------- block helpers
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {

@@ -29,7 +29,8 @@ constexpr int kAttendChunk = 512;    // selected rows per gather CTA (list mode)
 #ifndef TKV_CAND_CHUNK
 #define TKV_CAND_CHUNK 1024
 #endif
-constexpr int kCandChunk = TKV_CAND_CHUNK;  // candidates per work item (candidate mode)
+constexpr int kCandChunk = TKV_CAND_CHUNK;  // candidates per compaction + gather batch (candidate mode)
+constexpr int kCandQuant = 256;             // candidate-mode work items are multiples of this
 constexpr int kFlatMinRows = 256;           // flat list gather: rows per CTA range, at least
 constexpr int kSortMax = 16384;      // one-CTA shared-memory sort up to this k; chunk sort + merge passes above
 constexpr uint32_t kNoFilterShift = 20;  // histogram shift when every score is a candidate

@@ -161,12 +161,7 @@ __global__ void __launch_bounds__(kThrThreads, 4) threshold_kernel(SampleParams 
     copy_g2s_u32<NT, kSamples>(s_keys, p.samp + static_cast<int64_t>(bh) * kSamples, (Sb + 3) & ~3);
     __syncthreads();
     TKV_THR_PHASE(25);
-    uint32_t mx = 0u;
-    for (int i = tid; i < Sb; i += NT) mx = max(mx, s_keys[i]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(kFull, mx, o));
-    if (lane == 0) s_max[warp] = mx;
-    __syncthreads();
+    uint32_t mx = 0u;  // the sample maximum, folded into the first histogram pass
     TKV_THR_PHASE(26);
     // r-th largest sampled key: MSB-first radix select (11/11/10-bit digits) in shared memory.
     // Stopping early when the digit's bucket is taken whole leaves the bucket's lower bound,
@@ -180,9 +175,17 @@ __global__ void __launch_bounds__(kThrThreads, 4) threshold_kernel(SampleParams 
       const uint32_t mask = (1u << w) - 1u;
       for (int i = tid; i <= static_cast<int>(mask); i += NT) s_hist[i] = 0u;
       __syncthreads();
+      // plain shared atomics: the hardware resolves same-bin lanes faster than a match.any
+      // aggregation (the samples spread over a few dozen bins of the first digit)
       for (int i = tid; i < Sb; i += NT) {
         const uint32_t k = s_keys[i];
-        if (sh == 32 || (k >> sh) == prefix) hist_add_aggregated(s_hist, (k >> nsh) & mask);
+        if (sh == 32) mx = max(mx, k);
+        if (sh == 32 || (k >> sh) == prefix) atomicAdd(&s_hist[(k >> nsh) & mask], 1u);
+      }
+      if (sh == 32) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(kFull, mx, o));
+        if (lane == 0) s_max[warp] = mx;
       }
       __syncthreads();
       if (w == 11)
@@ -207,7 +210,7 @@ __global__ void __launch_bounds__(kThrThreads, 4) threshold_kernel(SampleParams 
           if ((k >> sh) == prefix) s_hist[atomicAdd(&s_n, 1u)] = k;
         }
         __syncthreads();
-        thr = block_rank_select<NT>(s_hist, static_cast<int>(s_n), static_cast<int>(need), &s_res);
+        thr = block_rank_select_par<NT>(s_hist, static_cast<int>(s_n), static_cast<int>(need), &s_res);
         exact = true;
         break;
       }
