@@ -193,6 +193,14 @@ int tkv_shard_finalize(const tkv_problem* p, const void* q, const void* k_cache,
  */
 int tkv_convert_rows_f32(const float* src, int64_t rows, int32_t d, void* dst, void* stream);
 
+/*
+ * Diagnostics (synchronous): how many (b, q head) selections needed the exactness fallback (the
+ * sampled threshold admitted fewer than k rows, so the head was re-scanned with threshold 0)
+ * on this workspace since tkv_workspace_init.
+ */
+int tkv_workspace_fallbacks(const tkv_problem* p, const void* workspace, size_t workspace_bytes,
+                            uint32_t* heads);
+
 /* Number of kernels the last compute call on this thread enqueued (for launch accounting). */
 int tkv_last_launch_count(void);
 

@@ -36,6 +36,7 @@ EXPORTS = (
     "tkv_shard_partial",
     "tkv_shard_finalize",
     "tkv_last_launch_count",
+    "tkv_workspace_fallbacks",
     "tkv_profile_scan_events",
     "tkv_debug_timeline",
     "tkv_convert_rows_f32",
@@ -82,6 +83,7 @@ _SIG = {
     "tkv_last_error": ([], ctypes.c_char_p),
     "tkv_device_check": ([], _I),
     "tkv_last_launch_count": ([], _I),
+    "tkv_workspace_fallbacks": ([ctypes.POINTER(Problem), _P, ctypes.c_size_t, _P], _I),
     "tkv_profile_scan_events": ([_P, _P], _I),
     "tkv_debug_timeline": ([_P], _I),
     "tkv_convert_rows_f32": ([_P, ctypes.c_int64, ctypes.c_int32, _P, _P], _I),

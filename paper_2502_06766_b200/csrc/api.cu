@@ -54,7 +54,7 @@ int fail(int code, const char* fmt, ...) {
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct Layout {
-  size_t ticket_g, ticket_k, flag, gflag, fbl, ctrl_end;
+  size_t ticket_g, ticket_k, flag, gflag, fbl, fbh, ctrl_end;
   size_t maxc, bktc, bkt, outc;
   size_t cnt, thr, hshift, hist, mmax, mkth, mkb, samp, cand, sidx, sscore, pl, po, pinm, qs, sortb, total;
   int pin_words;
@@ -77,6 +77,7 @@ Layout make_layout(const tkv_problem* p) {
   L.flag = take(BH * 4);
   L.gflag = take(BK * 4);
   L.fbl = take(4 * kMaxParts);
+  L.fbh = take(4);
   L.ctrl_end = off;
   L.cnt = take(BH * 4);
   L.thr = take(BH * 4);
@@ -97,7 +98,10 @@ Layout make_layout(const tkv_problem* p) {
   {
     // partial slots per head: list mode (k / kAttendChunk) or candidate mode (cap / kCandQuant)
     const int64_t a = (p->k + kAttendChunk - 1) / kAttendChunk;
-    const int64_t c = (L.cap + kCandQuant - 1) / kCandQuant + 1;
+    // candidate-mode items per head: ceil(quanta_h / S) <= min(quanta_h, grid + 1) (S =
+    // ceil(all quanta / grid), grid <= kMaxGatherGrid)
+    int64_t c = (L.cap + kCandQuant - 1) / kCandQuant + 1;
+    c = c < kMaxGatherGrid + 1 ? c : kMaxGatherGrid + 1;
     const int64_t f = (p->k + kFlatMinRows - 1) / kFlatMinRows + 1;  // flat list gather ranges
     int64_t m = a > c ? a : c;
     L.nchunks = static_cast<int>(m > f ? m : f);
@@ -182,6 +186,7 @@ HeadState head_state(void* ws, const Layout& L) {
   hs.kth_ticket = at<uint32_t>(ws, L.ticket_k);
   hs.out_cnt = at<uint32_t>(ws, L.outc);
   hs.fb_launched = at<uint32_t>(ws, L.fbl);
+  hs.fb_heads = at<uint32_t>(ws, L.fbh);
   return hs;
 }
 
@@ -646,6 +651,16 @@ int tkv_workspace_bytes(const tkv_problem* p, size_t* bytes) {
   TRY(validate(p));
   if (!bytes) return fail(TKV_EBADSHAPE, "bytes is NULL");
   *bytes = make_layout(p).total;
+  return TKV_OK;
+}
+
+int tkv_workspace_fallbacks(const tkv_problem* p, const void* ws, size_t bytes, uint32_t* heads) {
+  TRY(validate(p));
+  Layout L;
+  TRY(check_ws(p, const_cast<void*>(ws), bytes, &L));
+  if (!heads) return fail(TKV_EBADSHAPE, "heads is NULL");
+  const cudaError_t e = cudaMemcpy(heads, static_cast<const char*>(ws) + L.fbh, 4, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return fail(TKV_ECUDA, "cudaMemcpy: %s", cudaGetErrorString(e));
   return TKV_OK;
 }
 

@@ -286,7 +286,8 @@ cudaError_t launch_attend_cand(const AttendParams& p, cudaStream_t s) {
                          cudaSharedmemCarveoutMaxShared);
     int per = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, attend_cand_kernel, NT, 8192);
-    return device_sm_count() * (per > 0 ? per : 1);
+    const int g = device_sm_count() * (per > 0 ? per : 1);
+    return g < kMaxGatherGrid ? g : kMaxGatherGrid;
   });
   const size_t nbh = p.bh_count ? static_cast<size_t>(p.bh_count) : static_cast<size_t>(p.B) * p.Hq;
   attend_cand_kernel<<<grid, NT, (nbh + 1) * sizeof(uint32_t), s>>>(p);

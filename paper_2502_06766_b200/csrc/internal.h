@@ -31,6 +31,7 @@ constexpr int kAttendChunk = 512;    // selected rows per gather CTA (list mode)
 #endif
 constexpr int kCandChunk = TKV_CAND_CHUNK;  // candidates per compaction + gather batch (candidate mode)
 constexpr int kCandQuant = 256;             // candidate-mode work items are multiples of this
+constexpr int kMaxGatherGrid = 1023;        // candidate-mode gather CTAs (bounds the partial slots)
 constexpr int kFlatMinRows = 256;           // flat list gather: rows per CTA range, at least
 constexpr int kSortMax = 16384;      // one-CTA shared-memory sort up to this k; chunk sort + merge passes above
 constexpr uint32_t kNoFilterShift = 20;  // histogram shift when every score is a candidate
@@ -41,6 +42,15 @@ constexpr int kMaxParts = 16;            // KV-group parts of the overlapped lay
 __host__ __device__ inline int64_t sample_stride(int64_t n) {
   const int64_t s = (n + kSamples - 1) / kSamples;
   return s > kMinSampleStride ? s : kMinSampleStride;
+}
+
+// Sampled row s of segment seg (= b * Hkv + kv head): one row per stride-wide window, at a
+// hashed offset inside it, so periodic structure in a cache (every stride-th row alike) cannot
+// line up with the sample. tests/conftest.py sample_rows() restates it for adversarial caches.
+__host__ __device__ inline int64_t sample_row(int64_t s, int64_t stride, int seg, int64_t n) {
+  const uint32_t h = static_cast<uint32_t>(s) * 2654435761u ^ static_cast<uint32_t>(seg) * 0x9E3779B9u;
+  const int64_t r = s * stride + static_cast<int64_t>((h >> 8) % static_cast<uint32_t>(stride));
+  return r < n ? r : n - 1;
 }
 
 // per-(b, q head) state shared by the kernels of one call, in the workspace
@@ -58,6 +68,7 @@ struct HeadState {
   uint32_t* out_cnt;     // [B*Hq] selected rows written so far (reset by threshold_kernel)
   uint32_t* fb_launched; // the exactness fallback has been tail-launched for this call (one flag
                          // per pipeline part; the part's SelectParams points at its own)
+  uint32_t* fb_heads;    // heads that needed the exactness fallback since tkv_workspace_init
 };
 
 struct SampleParams {

@@ -6,7 +6,8 @@
 // shared by the group) and, instead of materialising all N scores, emits only the rows
 // whose score can still be in the top-k:
 //
-//   sample_kernel    : scores a strided sample of S = 4096 rows per (b, kv head).
+//   sample_kernel    : scores a sample of S = 4096 rows per (b, kv head), one per stride-wide
+//                      window at a hashed offset (internal.h sample_row).
 //   threshold_kernel : per (b, q head), the threshold key t_h = the r-th largest sampled key,
 //                      r = ceil(mu + 6 sqrt(mu) + 16), mu = k·S_b/N_b (≈1.5–2·k survivors
 //                      expected; t_h = 0 = emit all when that would not filter), and the
@@ -83,8 +84,8 @@ __global__ void __launch_bounds__(kSampleThreads) sample_kernel(SampleParams p) 
     const int s0 = blockIdx.x * kSampleThreads + warp * 32 + u * 16;
     const int sA = s0 + g, sB = s0 + g + 8;
     uint4 a[2][4];
-    load_tile(a, kbase + static_cast<int64_t>(sA) * stride * kD, sA < Sb,
-              kbase + static_cast<int64_t>(sB) * stride * kD, sB < Sb, c);
+    load_tile(a, kbase + sample_row(sA, stride, seg, N) * kD, sA < Sb, kbase + sample_row(sB, stride, seg, N) * kD,
+              sB < Sb, c);
     float acc[4];
     score_tile(acc, a, f);
 #pragma unroll

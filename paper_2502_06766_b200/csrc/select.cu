@@ -182,6 +182,7 @@ __global__ void __launch_bounds__(SNT) select_kernel(SelectParams p) {
     for (int i = tid; i < kHistBins; i += SNT) gh[i] = 0u;
     if (tid == 0) {
       p.hs.flag_fail[bh] = 1u;
+      atomicAdd(p.hs.fb_heads, 1u);
       p.hs.group_fail[b * p.Hkv + h / p.G] = 1u;
       p.hs.cand_cnt[bh] = 0u;
       p.hs.thr[bh] = 0u;
@@ -358,6 +359,7 @@ __global__ void __cluster_dims__(kKthCtas, 1, 1) __launch_bounds__(kKthThreads, 
       for (int i = tid; i < kHistBins; i += KT) gh[i] = 0u;
       if (tid == 0) {
         p.hs.flag_fail[bh] = 1u;
+        atomicAdd(p.hs.fb_heads, 1u);
         p.hs.group_fail[b * p.Hkv + h / p.G] = 1u;
         p.hs.cand_cnt[bh] = 0u;
         p.hs.thr[bh] = 0u;
@@ -596,6 +598,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_topk_kernel(HeadParams h
       for (int i = tid; i < kHistBins; i += HT) gh[i] = 0u;
       if (tid == 0) {
         p.hs.flag_fail[bh] = 1u;
+        atomicAdd(p.hs.fb_heads, 1u);
         p.hs.group_fail[b * p.Hkv + h / p.G] = 1u;
         p.hs.cand_cnt[bh] = 0u;
         p.hs.thr[bh] = 0u;
@@ -863,7 +866,8 @@ cudaError_t launch_head_topk(const HeadParams& p, cudaStream_t s) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, attend_cand_fb_kernel, NT, 8192);
 #endif
     cudaFuncSetAttribute(head_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHeadSmem);
-    return device_sm_count() * (per > 0 ? per : 1);
+    const int g = device_sm_count() * (per > 0 ? per : 1);
+    return g < kMaxGatherGrid ? g : kMaxGatherGrid;
   });
   HeadParams q = p;
   q.att_grid = att_grid;

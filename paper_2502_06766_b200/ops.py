@@ -88,6 +88,12 @@ class Workspace:
     def fits(self, problem: _lib.Problem) -> bool:
         return _lib.workspace_bytes(problem) <= self.nbytes
 
+    def fallbacks(self, problem: _lib.Problem) -> int:
+        """Selections that needed the exactness fallback on this workspace (synchronous read)."""
+        n = ctypes.c_uint32(0)
+        _lib.call("tkv_workspace_fallbacks", ctypes.byref(problem), self.ptr, self.nbytes, ctypes.byref(n))
+        return int(n.value)
+
 
 _WS_CACHE: dict[tuple, Workspace] = {}
 

@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 import torch
 
+from tests.conftest import sample_rows
 from tests.test_gpu_parity import _check, _make, _run
 
 pytestmark = pytest.mark.gpu
@@ -46,7 +47,7 @@ def test_fuzz_against_oracle(cuda, seed):
     _check(q, K, V, n_ctx, k, out, idx, sc, n_win=n_win, combine=combine, pinned=pin)
 
 
-def _adversarial(seed, q, K):
+def _adversarial(seed, q, K, n_ctx):
     """Distributions that stress the sampled threshold, the tie rule and the fallback."""
     from oracle import oracle as O
 
@@ -62,8 +63,10 @@ def _adversarial(seed, q, K):
         K[:] = K[:, :, :1]
     elif kind == 2:  # sampled rows far above the rest: the sampled threshold admits < k rows
         K[:] = O.to_bf16_f32(K * 0.01)
-        stride = max(8, -(-rows // 4096))
-        K[:, :, ::stride] = O.to_bf16_f32(K[:, :, ::stride] + 2.0 * np.sign(q[:, :1, None, :]))
+        for b in range(B):
+            for h in range(Hkv):  # the rows the sampled threshold scores (n_ctx[b] rows)
+                rr = sample_rows(int(n_ctx[b]), b * Hkv + h)
+                K[b, h, rr] = O.to_bf16_f32(K[b, h, rr] + 2.0 * np.sign(q[b, :1, :]))
     elif kind == 3:  # large magnitudes
         K[:] = O.to_bf16_f32(K * 64.0)
     else:  # tiny magnitudes (scores near zero, -0.0 / +0.0 keys)
@@ -76,7 +79,7 @@ def test_fuzz_adversarial(cuda, seed):
     B, Hq, Hkv, N, k, W, pin, combine, n_ctx, opts = _config(500 + seed)
     rng = np.random.default_rng(20_000 + seed)
     q, K, V = _make(rng, B, Hq, Hkv, N + W + 4)
-    K = _adversarial(seed, q, K)
+    K = _adversarial(seed, q, K, n_ctx)
     n_win = [W] * B
     out, idx, sc = _run(q, K, V, n_ctx, k, cuda, n_win=n_win, pinned_prefix=pin, combine=combine, **opts)
     torch.cuda.synchronize()

@@ -14,7 +14,7 @@ import pytest
 import torch
 
 from oracle import oracle as O
-from tests.conftest import bf16_normal
+from tests.conftest import bf16_normal, sample_rows
 
 pytestmark = pytest.mark.gpu
 
@@ -169,11 +169,23 @@ def test_fallback_when_sample_overestimates(cuda, head):
     B, Hq, Hkv, N, k = 1, 4, 1, 65536, 2048
     q, K, V = _make(rng, B, Hq, Hkv, N)
     K = O.to_bf16_f32(K * 0.01)
-    stride = -(-N // 4096)
-    K[0, 0, ::stride] = O.to_bf16_f32(np.sign(q[0, 0])[None, :] * 2.0 + K[0, 0, ::stride])
-    out, idx, sc = _run(q, K, V, [N], k, cuda, head=head)
+    rr = sample_rows(N, 0)  # the rows the sampled threshold scores (b = 0, kv head 0)
+    K[0, 0, rr] = O.to_bf16_f32(np.sign(q[0, 0])[None, :] * 2.0 + K[0, 0, rr])
+    from paper_2502_06766_b200 import ops
+
+    prob = ops.make_problem(B, Hq, Hkv, N, N, k, head=head)
+    ws = ops.Workspace(prob, cuda)
+    out, idx, sc = _run(q, K, V, [N], k, cuda, head=head, workspace=ws)
     torch.cuda.synchronize()
     _check(q, K, V, [N], k, out, idx, sc)
+    assert ws.fallbacks(prob) >= 1, "the adversarial sample did not trigger the exactness fallback"
+    # a normal cache on the same workspace: no further fallback
+    q2, K2, V2 = _make(rng, B, Hq, Hkv, N)
+    _run(q2, K2, V2, [N], k, cuda, head=head, workspace=ws)
+    torch.cuda.synchronize()
+    n_fb = ws.fallbacks(prob)
+    _run(q2, K2, V2, [N], k, cuda, head=head, workspace=ws)
+    assert ws.fallbacks(prob) == n_fb
     # the unfiltered path (every score a candidate, no fallback) is exact as well; the two may
     # differ only on near-ties, since the fallback re-scan uses the mma.sync scan and the main
     # pass the tcgen05 scan (fp32 accumulation orders differ)

@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 import torch
 
+from tests.conftest import sample_rows
 from tests.test_gpu_parity import _check, _dev, _make, _run
 
 pytestmark = pytest.mark.gpu
@@ -62,8 +63,8 @@ def test_tc_scan_fallback(cuda):
     B, Hq, Hkv, N, k = 1, 4, 1, 65536, 2048
     q, K, V = _make(rng, B, Hq, Hkv, N)
     K = O.to_bf16_f32(K * 0.01)
-    stride = -(-N // 4096)
-    K[0, 0, ::stride] = O.to_bf16_f32(np.sign(q[0, 0])[None, :] * 2.0 + K[0, 0, ::stride])
+    rr = sample_rows(N, 0)  # the rows the sampled threshold scores (kv head 0)
+    K[0, 0, rr] = O.to_bf16_f32(np.sign(q[0, 0])[None, :] * 2.0 + K[0, 0, rr])
     out, idx, sc = _run(q, K, V, [N], k, cuda, tc_scan=True)
     torch.cuda.synchronize()
     _check(q, K, V, [N], k, out, idx, sc)
@@ -133,9 +134,8 @@ def test_overlapped_parts_fallback_and_graph(cuda):
     B, Hq, Hkv, N, k = 1, 16, 4, 65536, 2048
     q, K, V = _make(rng, B, Hq, Hkv, N)
     K = O.to_bf16_f32(K * 0.01)
-    stride = -(-N // 4096)
-    # adversarial sample for kv head 3 only (the last part)
-    K[0, 3, ::stride] = O.to_bf16_f32(np.sign(q[0, 12])[None, :] * 2.0 + K[0, 3, ::stride])
+    rr = sample_rows(N, 3)  # adversarial sample for kv head 3 only (the last part)
+    K[0, 3, rr] = O.to_bf16_f32(np.sign(q[0, 12])[None, :] * 2.0 + K[0, 3, rr])
     out, idx, sc = _run(q, K, V, [N], k, cuda, parts=4)
     torch.cuda.synchronize()
     _check(q, K, V, [N], k, out, idx, sc)
