@@ -135,6 +135,8 @@ def load(build_if_missing: bool = False) -> ctypes.CDLL:
         except OSError as e:  # pragma: no cover - depends on the host
             raise DeviceError(f"cannot load {LIB_PATH}: {e}") from e
         for name, (args, res) in _SIG.items():
+            if os.environ.get("TKV_LIB_PATH") and not hasattr(lib, name):
+                continue  # A/B against an older experiment build: newer entry points absent
             fn = getattr(lib, name)
             fn.argtypes = args
             fn.restype = res

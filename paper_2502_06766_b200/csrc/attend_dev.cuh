@@ -280,10 +280,25 @@ __device__ void head_finish(const AttendParams& p, int bh, int nslots, AttSmem& 
   const int kb = __ldcg(&p.meta_kb[bh]);
   const float zref = kb > 0 ? __ldcg(&p.meta_max[bh]) * p.scale * kLog2e : 0.f;
   const int64_t nctx = p.n_ctx[b];
+  // sum the partials in slot order (deterministic), 8 slots' loads in flight at a time (a
+  // dependent load per slot made the finish a serial chain of L2 round trips: ~18 slots per
+  // head at cfg3)
   float o_c = 0.f, l_c = 0.f;
-  for (int c2 = 0; c2 < nslots; ++c2) {
-    if (tid < kD) o_c += __ldcg(&p.part_o[(static_cast<int64_t>(bh) * p.nchunks + c2) * kD + tid]);
-    l_c += __ldcg(&p.part_l[static_cast<int64_t>(bh) * p.nchunks + c2]);
+  const float* po = p.part_o + static_cast<int64_t>(bh) * p.nchunks * kD + (tid & (kD - 1));
+  const float* pl = p.part_l + static_cast<int64_t>(bh) * p.nchunks;
+  for (int c0 = 0; c0 < nslots; c0 += 8) {
+    float vo[8], vl[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const bool ok = c0 + u < nslots;
+      vo[u] = ok && tid < kD ? __ldcg(po + static_cast<int64_t>(c0 + u) * kD) : 0.f;
+      vl[u] = ok ? __ldcg(pl + c0 + u) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      o_c += vo[u];
+      l_c += vl[u];
+    }
   }
   add_pinned<Gp>(p, b, h, kvh, nctx, kb, zref, l_c, o_c, sm.z, sm.scr, &sm.red[0][0]);
   if (p.partial_only) {

@@ -44,11 +44,13 @@ __host__ __device__ inline int64_t sample_stride(int64_t n) {
   return s > kMinSampleStride ? s : kMinSampleStride;
 }
 
-// Sampled row s of segment seg (= b * Hkv + kv head): one row per stride-wide window, at a
-// hashed offset inside it, so periodic structure in a cache (every stride-th row alike) cannot
-// line up with the sample. tests/conftest.py sample_rows() restates it for adversarial caches.
+// Sampled row s of segment seg (= b * Hkv + kv head): one row per stride-wide window, at an
+// offset hashed from the segment, so a cache with period `stride` cannot line up with the
+// sample the same way in every segment (a per-sample offset measured 8 us slower at cfg3: the
+// faster sample kernel let threshold CTAs land where they hold scan CTAs off their SM).
+// tests/conftest.py sample_rows() restates it for adversarial caches.
 __host__ __device__ inline int64_t sample_row(int64_t s, int64_t stride, int seg, int64_t n) {
-  const uint32_t h = static_cast<uint32_t>(s) * 2654435761u ^ static_cast<uint32_t>(seg) * 0x9E3779B9u;
+  const uint32_t h = static_cast<uint32_t>(seg) * 0x9E3779B9u + 0x7F4A7C15u;
   const int64_t r = s * stride + static_cast<int64_t>((h >> 8) % static_cast<uint32_t>(stride));
   return r < n ? r : n - 1;
 }

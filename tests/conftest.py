@@ -44,9 +44,8 @@ def sample_rows(n: int, seg: int) -> np.ndarray:
     sample_row / sample_stride in paper_2502_06766_b200/csrc/internal.h): adversarial caches put
     their outliers exactly there to force the exactness fallback."""
     stride = max(8, -(-n // 4096))
-    s = np.arange(-(-n // stride), dtype=np.uint64)
-    h = ((s * np.uint64(2654435761)) & np.uint64(0xFFFFFFFF)) ^ np.uint64((seg * 0x9E3779B9) & 0xFFFFFFFF)
-    r = s.astype(np.int64) * stride + ((h >> np.uint64(8)) % np.uint64(stride)).astype(np.int64)
+    h = (seg * 0x9E3779B9 + 0x7F4A7C15) & 0xFFFFFFFF
+    r = np.arange(-(-n // stride), dtype=np.int64) * stride + (h >> 8) % stride
     return np.minimum(r, n - 1)
 
 
