@@ -18,10 +18,12 @@ no L2 flush is needed between steps.
             layer-step on every host thread, plus a single-core sample (1 KV group, scaled)
 
 Multi-GPU (torchrun, N > 1): the context is sharded by token range (strong scaling: the 1M
-rows are split across ranks); candidates all-gather + partial all-reduce over NCCL; value =
-max over ranks of the per-step device time. By default each rank sends only its top
-ceil(1.5*k/N) candidates (narrow exchange, exactness checked on the device every step, full-k
-fallback when it fails); `--narrow 0` all-gathers k per rank.
+rows are split across ranks); value = max over ranks of the per-step device time. Default
+exchange (`--exchange symm`): every rank publishes its narrow (top ~ceil(1.5*k/N)) and full
+candidate lists in torch symmetric memory, the merge kernel reads the peers' lists over NVLink
+and picks narrow or full per head on the device, the finishing kernel sums the peers' partials
+(DeviceShardedStep: no host round trip). `--exchange nccl`: all-gather + all-reduce through
+NCCL collectives (sharded_topk_attention, one host read of the exactness flag per step).
 `--impl reference`: times the reference algorithm's CPU port on rank 0 (others exit 0).
 """
 
@@ -231,6 +233,9 @@ def our_config(args, cfg, world=1):
          "seed": args.seed}
     if world > 1 and args.narrow:
         c["narrow_c"] = args.narrow
+    if world > 1:
+        c["exchange"] = ("device-driven, torch symmetric memory (DeviceShardedStep)" if args.exchange == "symm"
+                         else "NCCL all-gather + all-reduce (sharded_topk_attention)")
     return c
 
 
@@ -274,6 +279,9 @@ def main():
     ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--exchange", default="symm", choices=["symm", "nccl"],
+                    help="N>1: device-driven exchange over torch symmetric memory (DeviceShardedStep; "
+                         "falls back to nccl when unavailable) or NCCL collectives (sharded_topk_attention)")
     ap.add_argument("--narrow", type=float, default=1.5,
                     help="N>1: narrow candidate exchange, each rank sends its top ceil(C*k/N) "
                          "(exactness checked per step, full-k fallback); 0 = full-k exchange")
@@ -326,15 +334,29 @@ def main():
     else:
         stages = tkv.CudaStages(B, HQ, HKV, rows, n_local, k, row_offset=lo, device=dev)
         n_ctx = torch.full((B,), n_local, dtype=torch.int32, device=dev)
-        gathered = torch.empty(world * B * HQ * k, dtype=torch.int64, device=dev)
-        narrow = None
-        if args.narrow:
-            narrow = tkv.CudaStages(B, HQ, HKV, rows, n_local, tkv.narrow_k(k, world, args.narrow),
-                                    row_offset=lo, device=dev)
+        kk = tkv.narrow_k(k, world, args.narrow) if args.narrow else k
+        step = None
+        if args.exchange == "symm":
+            try:
+                exch = tkv.SymmetricExchange(B, HQ, k, kk, dev)
+                dstep = tkv.DeviceShardedStep(stages, exch, rank, kk)
+                n_win0 = torch.zeros(B, dtype=torch.int32, device=dev)
 
-        def step():
-            tkv.sharded_topk_attention(stages, q, K, V, n_ctx, None, gathered=gathered,
-                                       narrow=narrow)
+                def step():
+                    dstep(q, K, V, n_ctx, n_win0)
+            except Exception as e:  # pragma: no cover - depends on the node's symmetric memory support
+                print(f"[bench] symmetric-memory exchange unavailable ({e!r}); using NCCL collectives",
+                      file=sys.stderr)
+                args.exchange = "nccl"
+        if step is None:
+            gathered = torch.empty(world * B * HQ * k, dtype=torch.int64, device=dev)
+            narrow = None
+            if args.narrow:
+                narrow = tkv.CudaStages(B, HQ, HKV, rows, n_local, kk, row_offset=lo, device=dev)
+
+            def step():
+                tkv.sharded_topk_attention(stages, q, K, V, n_ctx, None, gathered=gathered,
+                                           narrow=narrow)
 
     for _ in range(warm):
         step()

@@ -176,6 +176,33 @@ int tkv_shard_narrow_check(const tkv_problem* p, const uint64_t* gathered, int32
 int tkv_shard_merge_lists(const tkv_problem* p, const uint64_t* gathered, int32_t n_shards,
                           int32_t list_len, int32_t* idx, float* scores, void* workspace,
                           size_t workspace_bytes, void* stream);
+/*
+ * Device-driven exchange (no host round trip, CUDA-graph capturable). Every rank publishes its
+ * lists in buffers its peers can read (symmetric memory over NVLink; in a one-GPU emulation,
+ * plain device buffers):
+ *   tkv_shard_candidates2: one key scan; cand_full[B*Hq*k] = the exact local top-k (as
+ *     tkv_shard_candidates); cand_narrow[B*Hq*narrow_k] = its entries >= a bound t2 (fewer
+ *     than narrow_k of them, zero-padded); bounds[B*Hq*3] = {t2 (every withheld row is below
+ *     it), the local k-th composite when the shard has >= k rows else 0, the largest composite}.
+ *   tkv_shard_exchange_merge: narrow_lists / full_lists / bounds are DEVICE arrays of n_shards
+ *     (<= 16) pointers to the ranks' buffers. Per head, on the device: when at least k narrow
+ *     candidates clear T* = max of the ranks' t2, the global top-k is merged from the narrow
+ *     lists (exact: no withheld row can enter it), else from the full lists (used_full[B*Hq],
+ *     optional, records which). Outputs as tkv_shard_merge; with TKV_F_SORTED, TopKResult order.
+ *   tkv_shard_combine: partials is a device array of n_shards pointers to the ranks'
+ *     tkv_shard_partial outputs; sums them (the all-reduce) and finishes as tkv_shard_finalize.
+ * (Replace no reference interface: the reference is single-process.)
+ */
+int tkv_shard_candidates2(const tkv_problem* p, int32_t narrow_k, const void* q, const void* k_cache,
+                          const int32_t* n_ctx, uint64_t* cand_narrow, uint64_t* cand_full, uint64_t* bounds,
+                          void* workspace, size_t workspace_bytes, void* stream);
+int tkv_shard_exchange_merge(const tkv_problem* p, const uint64_t* const* narrow_lists,
+                             const uint64_t* const* full_lists, const uint64_t* const* bounds, int32_t n_shards,
+                             int32_t narrow_k, int32_t* idx, float* scores, int32_t* used_full, void* workspace,
+                             size_t workspace_bytes, void* stream);
+int tkv_shard_combine(const tkv_problem* p, const float* const* partials, int32_t n_shards, const void* q,
+                      const void* k_cache, const void* v_cache, const int32_t* n_ctx, const int32_t* n_win,
+                      float* out, void* workspace, size_t workspace_bytes, void* stream);
 int tkv_shard_partial(const tkv_problem* p, const void* q, const void* k_cache,
                       const void* v_cache, const int32_t* n_ctx, const int32_t* idx,
                       const float* scores, float* partial, void* workspace,

@@ -26,12 +26,13 @@ from .errors import (
     TopkKvError,
 )
 from .ops import Workspace, kv_append, topk_decode_attention, topk_decode_step, topk_search
-from .sharded import CudaStages, narrow_k, shard_range, sharded_topk_attention
+from .sharded import (CudaStages, DeviceShardedStep, LocalExchange, SymmetricExchange, narrow_k, shard_range,
+                      sharded_topk_attention)
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "ConfigError", "CudaStages", "DegenerateError", "DeviceError", "DeviceValues", "DomainError",
+    "ConfigError", "CudaStages", "DeviceShardedStep", "LocalExchange", "SymmetricExchange", "DegenerateError", "DeviceError", "DeviceValues", "DomainError",
     "FormatError", "InfeasibleBudgetError", "InputError", "LayerBudget", "MipsIndex", "ShapeError",
     "TierAccounting", "TopKResult", "TopkDecoder", "TopkKvError", "VALUE_ROW_BYTES", "Workspace",
     "build_index", "entropy_budget", "knn_search", "kv_append", "linear_budget", "parse_budget_spec",

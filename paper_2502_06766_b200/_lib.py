@@ -33,6 +33,9 @@ EXPORTS = (
     "tkv_shard_merge",
     "tkv_shard_narrow_check",
     "tkv_shard_merge_lists",
+    "tkv_shard_candidates2",
+    "tkv_shard_exchange_merge",
+    "tkv_shard_combine",
     "tkv_shard_partial",
     "tkv_shard_finalize",
     "tkv_last_launch_count",
@@ -105,6 +108,13 @@ _SIG = {
     "tkv_shard_merge_lists": (
         [ctypes.POINTER(Problem), _P, ctypes.c_int32, ctypes.c_int32, _P, _P, _P, ctypes.c_size_t,
          _P], _I),
+    "tkv_shard_candidates2": (
+        [ctypes.POINTER(Problem), ctypes.c_int32, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P], _I),
+    "tkv_shard_exchange_merge": (
+        [ctypes.POINTER(Problem), _P, _P, _P, ctypes.c_int32, ctypes.c_int32, _P, _P, _P, _P, ctypes.c_size_t,
+         _P], _I),
+    "tkv_shard_combine": (
+        [ctypes.POINTER(Problem), _P, ctypes.c_int32, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P], _I),
     "tkv_shard_partial": (
         [ctypes.POINTER(Problem), _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P], _I),
     "tkv_shard_finalize": (

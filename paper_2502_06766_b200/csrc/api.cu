@@ -54,9 +54,9 @@ int fail(int code, const char* fmt, ...) {
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct Layout {
-  size_t ticket_g, ticket_k, flag, gflag, fbl, fbh, ctrl_end;
+  size_t ticket_g, ticket_k, flag, gflag, fbl, fbh, mout, ctrl_end;
   size_t maxc, bktc, bkt, outc;
-  size_t cnt, thr, hshift, hist, mmax, mkth, mkb, samp, cand, sidx, sscore, pl, po, pinm, qs, sortb, total;
+  size_t cnt, thr, hshift, hist, mmax, mkth, mkb, mt2, samp, cand, sidx, sscore, pl, po, pinm, qs, sortb, total;
   int pin_words;
   int64_t cap;
   int nchunks;
@@ -78,6 +78,7 @@ Layout make_layout(const tkv_problem* p) {
   L.gflag = take(BK * 4);
   L.fbl = take(4 * kMaxParts);
   L.fbh = take(4);
+  L.mout = take(BH * 4);  // sharded merge output counters (self-resetting)
   L.ctrl_end = off;
   L.cnt = take(BH * 4);
   L.thr = take(BH * 4);
@@ -90,6 +91,7 @@ Layout make_layout(const tkv_problem* p) {
   L.mmax = take(BH * 4);
   L.mkth = take(BH * 8);
   L.mkb = take(BH * 4);
+  L.mt2 = take(BH * 8);  // sharded narrow-list bound t2 per head
   L.samp = take(BH * kSamples * 4);
   L.cap = p->max_ctx > 0 ? p->max_ctx : 1;
   L.cand = take(BH * static_cast<size_t>(L.cap) * 8);
@@ -776,6 +778,105 @@ int tkv_shard_candidates(const tkv_problem* p, const void* q, const void* k_cach
   pu.flags &= ~TKV_F_SORTED;
   return run_layer(&pu, q, k_cache, k_cache, n_ctx, nullptr, at<int32_t>(ws, L.sidx), at<float>(ws, L.sscore),
                   cand, nullptr, 0, ws, L, st);
+}
+
+int tkv_shard_candidates2(const tkv_problem* p, int32_t narrow_k, const void* q, const void* k_cache,
+                          const int32_t* n_ctx, uint64_t* cand_narrow, uint64_t* cand_full, uint64_t* bounds,
+                          void* ws, size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  TRY(validate(p));
+  Layout L;
+  TRY(check_ws(p, ws, ws_bytes, &L));
+  TRY(check_ptr(q, "q", 16));
+  TRY(check_ptr(k_cache, "k_cache", 16));
+  TRY(check_ptr(n_ctx, "n_ctx", 4));
+  TRY(check_ptr(cand_narrow, "cand_narrow", 8));
+  TRY(check_ptr(cand_full, "cand_full", 8));
+  TRY(check_ptr(bounds, "bounds", 8));
+  if (narrow_k < 1 || narrow_k > p->k) return fail(TKV_EBADK, "narrow_k must be in [1, k] (got %d)", narrow_k);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // one key scan and one exact k-th selection for k; the k-th kernel also marks the narrow
+  // bound t2 (fewer than narrow_k candidates above it) from the same histogram; the emit pass
+  // writes the full list, a small filter kernel the narrow list and the bounds
+  tkv_problem pu = *p;
+  pu.flags = (pu.flags & ~(TKV_F_SORTED | TKV_F_PARTS_MASK | TKV_F_HEAD | TKV_F_HOST_Q)) | TKV_F_NO_HEAD;
+  ScanParams cp;
+  SelectParams sl;
+  TRY(run_prefix(&pu, q, k_cache, n_ctx, ws, L, st, &cp, &sl));
+  const int64_t nseg = static_cast<int64_t>(p->batch) * p->n_kv_heads;
+  const int nbh = p->batch * p->n_q_heads;
+  sl.k2 = narrow_k;
+  sl.meta_t2 = at<uint64_t>(ws, L.mt2);
+  TRY(run_scan_part(&pu, cp, 0, nseg, st, pdl_enabled()));
+  TRY(run_kth_part(&pu, cp, sl, 0, nseg, 0, st, pdl_enabled()));
+  TRY(run_emit(&pu, q, k_cache, k_cache, n_ctx, nullptr, at<int32_t>(ws, L.sidx), at<float>(ws, L.sscore), cand_full,
+               nullptr, 0, ws, L, st, 0, nbh));
+  TKV_LAUNCH(launch_narrow_filter(cand_full, p->k, cand_narrow, narrow_k, at<uint64_t>(ws, L.mt2),
+                                  at<uint64_t>(ws, L.mkth), at<int32_t>(ws, L.mkb), p->k, bounds, nbh, st));
+  return TKV_OK;
+}
+
+int tkv_shard_exchange_merge(const tkv_problem* p, const uint64_t* const* narrow_lists,
+                             const uint64_t* const* full_lists, const uint64_t* const* bounds, int32_t n_shards,
+                             int32_t narrow_k, int32_t* idx, float* scores, int32_t* used_full, void* ws,
+                             size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  TRY(validate(p));
+  Layout L;
+  TRY(check_ws(p, ws, ws_bytes, &L));
+  TRY(check_ptr(narrow_lists, "narrow_lists", 8));
+  TRY(check_ptr(full_lists, "full_lists", 8));
+  TRY(check_ptr(bounds, "bounds", 8));
+  TRY(check_ptr(idx, "idx", 4));
+  TRY(check_ptr(scores, "scores", 4));
+  if (n_shards < 1 || n_shards > kMaxShards) return fail(TKV_EBADSHAPE, "n_shards must be in [1, %d]", kMaxShards);
+  if (narrow_k < 1 || narrow_k > p->k) return fail(TKV_EBADK, "narrow_k must be in [1, k] (got %d)", narrow_k);
+  ShardMergeParams mp{};
+  mp.narrow = narrow_lists;
+  mp.full = full_lists;
+  mp.bound = bounds;
+  mp.n_shards = n_shards;
+  mp.narrow_len = narrow_k;
+  mp.full_len = p->k;
+  mp.k = p->k;
+  mp.idx = idx;
+  mp.scores = scores;
+  mp.meta_max = at<float>(ws, L.mmax);
+  mp.meta_kth = at<uint64_t>(ws, L.mkth);
+  mp.meta_kb = at<int32_t>(ws, L.mkb);
+  mp.out_cnt = at<uint32_t>(ws, L.mout);
+  mp.used_full = used_full;
+  mp.tl = g_tl;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int nbh = p->batch * p->n_q_heads;
+  TKV_LAUNCH(launch_shard_merge(mp, nbh, st));
+  if (p->flags & TKV_F_SORTED) {
+    SortParams so{idx, scores, mp.meta_kb, p->k, 0, at<uint64_t>(ws, L.sortb)};
+    TKV_SORT(so, nbh, st);
+  }
+  return TKV_OK;
+}
+
+int tkv_shard_combine(const tkv_problem* p, const float* const* partials, int32_t n_shards, const void* q,
+                      const void* k_cache, const void* v_cache, const int32_t* n_ctx, const int32_t* n_win,
+                      float* out, void* ws, size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  TRY(validate(p));
+  Layout L;
+  TRY(check_ws(p, ws, ws_bytes, &L));
+  TRY(check_ptr(partials, "partials", 8));
+  TRY(check_ptr(q, "q", 16));
+  TRY(check_ptr(k_cache, "k_cache", 16));
+  TRY(check_ptr(v_cache, "v_cache", 16));
+  TRY(check_ptr(n_ctx, "n_ctx", 4));
+  TRY(check_ptr(out, "out", 4));
+  if (n_shards < 1 || n_shards > kMaxShards) return fail(TKV_EBADSHAPE, "n_shards must be in [1, %d]", kMaxShards);
+  AttendParams a = make_attend(p, q, k_cache, v_cache, n_ctx, n_win, nullptr, nullptr, ws, L);
+  a.partial_peers = partials;
+  a.n_peers = n_shards;
+  a.out = out;
+  TKV_LAUNCH(launch_finalize(a, static_cast<cudaStream_t>(stream)));
+  return TKV_OK;
 }
 
 int tkv_shard_merge(const tkv_problem* p, const uint64_t* gathered, int32_t n_shards, int32_t* idx,

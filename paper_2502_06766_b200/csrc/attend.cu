@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(NT, 4) attend_kernel(AttendParams p) {
     sm.w[i] = owned ? exp2f(fmaf(s, zs, -zref)) : 0.f;
   }
   __syncthreads();
-  chunk_body(p, bh, ch, p.nchunks, nrows, sm);
+  chunk_body(p, bh, ch, gridDim.x, nrows, sm);  // one partial slot per chunk of the k list
 }
 
 // Candidate mode (single GPU): persistent CTAs walk (head, chunk of kCandChunk candidates)
@@ -247,9 +247,18 @@ __global__ void __launch_bounds__(NT) finalize_kernel(AttendParams p) {
   const int kb = p.meta_kb[bh];
   const float zs = p.scale * kLog2e;
   const float zref = kb > 0 ? p.meta_max[bh] * zs : 0.f;
-  const float* src = p.partial_in + static_cast<int64_t>(bh) * (kD + 1);
-  const float l_c = kb > 0 ? src[0] : 0.f;
-  const float o_c = (kb > 0 && tid < kD) ? src[1 + tid] : 0.f;
+  float l_c = 0.f, o_c = 0.f;
+  if (kb > 0 && p.n_peers > 0) {  // every rank's partial, read from its buffer (peer memory)
+    for (int g = 0; g < p.n_peers; ++g) {
+      const float* src = p.partial_peers[g] + static_cast<int64_t>(bh) * (kD + 1);
+      l_c += src[0];
+      if (tid < kD) o_c += src[1 + tid];
+    }
+  } else if (kb > 0) {
+    const float* src = p.partial_in + static_cast<int64_t>(bh) * (kD + 1);
+    l_c = src[0];
+    o_c = tid < kD ? src[1 + tid] : 0.f;
+  }
   finalize_head(p, b, h, kvh, p.n_ctx[b], zref, l_c, o_c, s_z, s_scr, s_o, s_red);
 }
 
@@ -274,7 +283,11 @@ __global__ void __launch_bounds__(256) append_kernel(AppendParams p) {
 }
 
 cudaError_t launch_attend(const AttendParams& p, cudaStream_t s) {
-  dim3 grid(p.nchunks, p.B * p.Hq);
+  // chunks of kAttendChunk selected rows: the k-list needs ceil(k / kAttendChunk) of them (the
+  // workspace's partial slots, nchunks, are sized for the candidate-mode gather and can be far
+  // more: launching nchunks CTAs per head would mostly launch empty ones)
+  const int nch = (p.k + kAttendChunk - 1) / kAttendChunk;
+  dim3 grid(nch < p.nchunks ? nch : p.nchunks, p.B * p.Hq);
   attend_kernel<<<grid, NT, 0, s>>>(p);
   return cudaGetLastError();
 }

@@ -141,6 +141,11 @@ struct SelectParams {
   int pass;
   int bh_begin, bh_count;  // heads handled (kth_kernel); bh_count 0 = all B*Hq
   int pdl;                 // launch kth_kernel with programmatic dependent launch
+  // sharded narrow list (tkv_shard_candidates2): k2 > 0 → kth_kernel also writes, per head, a
+  // composite t2 with fewer than k2 candidates >= t2 (the lower bound of the histogram bucket
+  // above the one holding the k2-th largest; T itself when every candidate is selected)
+  int k2;
+  uint64_t* meta_t2;
   // exactness fallback, tail-launched by kth_kernel (main pass) when a head failed
   ScanParams fb_scan;
   int fb_scan_grid;
@@ -201,7 +206,34 @@ struct AttendParams {
   uint32_t* pin_mask;  // [B*Hq][pin_words] or nullptr
   int pin_words;
   int bh_begin, bh_count;  // heads handled by attend_cand_kernel; bh_count 0 = all B*Hq
+  // sharded finalize (finalize_kernel): partial_in is replaced by the sum over n_peers ranks'
+  // (l, o[128]) partials read through device pointers, when n_peers > 0
+  const float* const* partial_peers;
+  int n_peers;
 };
+
+// shard_merge_kernel (shard.cu): exact global top-k over every rank's published candidate lists
+// (device pointers: peers' buffers over NVLink, or local buffers in the one-GPU emulation), the
+// narrow-vs-full choice made per head on the device
+constexpr int kMaxShards = 16;
+struct ShardMergeParams {
+  const uint64_t* const* narrow;  // [n_shards] → [B*Hq][narrow_len]
+  const uint64_t* const* full;    // [n_shards] → [B*Hq][full_len]
+  const uint64_t* const* bound;   // [n_shards] → [B*Hq][3]: narrow floor t2, full floor, max
+  int n_shards, narrow_len, full_len, k;
+  int32_t* idx;
+  float* scores;
+  float* meta_max;
+  uint64_t* meta_kth;
+  int32_t* meta_kb;
+  uint32_t* out_cnt;
+  int32_t* used_full;  // [B*Hq] or nullptr: 1 where the head was merged from the full lists
+  uint64_t* tl;        // diagnostics timeline (TKV_DIAG builds: per-phase means)
+};
+cudaError_t launch_shard_merge(const ShardMergeParams& p, int nbh, cudaStream_t s);
+cudaError_t launch_narrow_filter(const uint64_t* full, int full_len, uint64_t* narrow, int narrow_len,
+                                 const uint64_t* meta_t2, const uint64_t* meta_kth, const int32_t* meta_kb, int k,
+                                 uint64_t* bound, int nbh, cudaStream_t s);
 
 // head_topk_kernel (select.cu): k-th selection + V gather + finish of a head by ctas_per_head
 // CTAs (selected rows streamed through a kHeadCap-row shared buffer). att_grid: grid of the candidate-mode gather the exactness fallback

@@ -387,6 +387,7 @@ __global__ void __cluster_dims__(kKthCtas, 1, 1) __launch_bounds__(kKthThreads, 
       p.meta_kth[bh] = ~0ull;
       p.meta_kb[bh] = 0;
       p.meta_max[bh] = -INFINITY;
+      if (p.k2 > 0) p.meta_t2[bh] = 0ull;  // no rows: nothing withheld
       if (p.pass == kPassFallback) {
         p.hs.flag_fail[bh] = 0u;
         p.hs.group_fail[b * p.Hkv + h / p.G] = 0u;
@@ -400,15 +401,26 @@ __global__ void __cluster_dims__(kKthCtas, 1, 1) __launch_bounds__(kKthThreads, 
   const bool all = kb >= n;
   uint32_t dstar = 0, need = 0, bcnt = 0;
   bool whole = true;
-  if (!all) {
+  const bool narrow2 = p.k2 > 0 && p.k2 < kb;  // a narrow list shorter than the selection
+  if (!all || narrow2) {
     const uint32_t* gh = p.hs.hist + static_cast<int64_t>(bh) * kHistBins;
     copy_g2s_u32<KT, kHistBins>(s_hist, gh, kHistBins);
     __syncthreads();
+  }
+  if (!all) {
     find_bucket<KT, kHistBins>(s_hist, static_cast<uint32_t>(kb), s_out, s_scr);
     dstar = s_out[0];
     need = static_cast<uint32_t>(kb) - s_out[1];
     bcnt = s_hist[dstar];
     whole = bcnt == need;
+  }
+  if (narrow2 && part == 0) {  // sharded narrow list bound (tkv_shard_candidates2)
+    find_bucket<KT, kHistBins>(s_hist, static_cast<uint32_t>(p.k2), s_out, s_scr);
+    const uint32_t d2 = s_out[0];
+    if (tid == 0)
+      p.meta_t2[bh] = d2 + 1 < static_cast<uint32_t>(kHistBins)
+                          ? static_cast<uint64_t>(thr + ((d2 + 1) << shift)) << 32
+                          : ~0ull;  // the k2-th sits in the top (clamped) bucket: send none
   }
   const bool refine = !all && !whole;
   // bucket members are collected in this CTA's shared memory; more than fit (heavy exact
@@ -502,6 +514,7 @@ __global__ void __cluster_dims__(kKthCtas, 1, 1) __launch_bounds__(kKthThreads, 
     p.meta_kth[bh] = T;
     p.meta_kb[bh] = static_cast<int32_t>(kb);
     p.meta_max[bh] = key_score(comp_key(vmax));
+    if (p.k2 > 0 && !narrow2) p.meta_t2[bh] = T;  // the narrow list is the whole selection
     if (p.pass == kPassFallback) {
       p.hs.flag_fail[bh] = 0u;
       p.hs.group_fail[b * p.Hkv + h / p.G] = 0u;

@@ -137,3 +137,24 @@ def test_narrow_exchange_exact_rule():
     r1 = [hi + 60, hi + 10, 5, 0]
     assert narrow_exchange_exact(g(r0, r1), 2, 3, 2).tolist() == [True, False]
     assert narrow_k(16384, 8) == 3072 and narrow_k(100, 1) == 100 and narrow_k(10, 4, 2.0) == 5
+
+
+def test_publish_layout_views_tile_the_buffer():
+    """DeviceShardedStep's publish buffer (narrow | full | bounds | partial): the views are
+    disjoint, in order, and cover the buffer; the pointer arrays add the same offsets."""
+    sys.path.insert(0, str(ROOT))
+    from paper_2502_06766_b200.sharded import _PublishLayout, _pointer_arrays, _views
+
+    B, Hq, k, kk = 2, 8, 100, 37
+    lay = _PublishLayout(B, Hq, k, kk)
+    buf = torch.zeros(lay.nbytes, dtype=torch.uint8)
+    nar, full, bound, part = _views(buf, lay)
+    assert nar.numel() == B * Hq * kk and full.numel() == B * Hq * k and bound.numel() == B * Hq * 3
+    assert part.numel() == B * Hq * 129
+    base = buf.data_ptr()
+    offs = [t.data_ptr() - base for t in (nar, full, bound, part)]
+    ends = [o + t.numel() * t.element_size() for o, t in zip(offs, (nar, full, bound, part))]
+    assert offs[0] == 0 and all(ends[i] == offs[i + 1] for i in range(3)) and ends[3] == lay.nbytes
+    ptrs = _pointer_arrays([base, base + 1000], lay, "cpu")
+    for arr, o in zip(ptrs, offs):
+        assert arr.tolist() == [base + o, base + 1000 + o]

@@ -21,7 +21,10 @@ PHASES = ["head CTA: start→params", "→hist+bucket", "→pass 1 (max, bucket 
 
 EXTRA_EVENTS = {40: "scan CTA start", 41: "scan CTA end", 45: "threshold CTA past wait"}
 EXTRA_PHASES = {42: "scan epilogue: wait for a unit's scores", 43: "scan epilogue: ld+emit of a unit",
-                44: "scan MMA warp: wait for a unit's TMA", 46: "scan CTA lifetime"}
+                44: "scan MMA warp: wait for a unit's TMA", 46: "scan CTA lifetime",
+                47: "merge: start→bounds + narrow count + rule", 48: "→histogram + cluster sums + bucket",
+                49: "→bucket count", 50: "→members + barrier", 51: "→rank select + barrier",
+                52: "→emit (2 passes) + barrier"}
 
 
 def main():
