@@ -365,11 +365,20 @@ __device__ __forceinline__ uint64_t gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// durations inside one CTA: the SM clock (%globaltimer ticks too coarsely for sub-us phases),
+// scaled to ~ns at the B200's 1965 MHz boost clock
+__device__ __forceinline__ uint64_t ptimer() { return static_cast<uint64_t>(clock64()) * 509ull / 1000ull; }
 __device__ __forceinline__ void tl_start(uint64_t* tl, int e) {
   if (tl) atomicMin(reinterpret_cast<unsigned long long*>(tl + 2 * e), static_cast<unsigned long long>(gtimer()));
 }
 __device__ __forceinline__ void tl_end(uint64_t* tl, int e) {
   if (tl) atomicMax(reinterpret_cast<unsigned long long*>(tl + 2 * e + 1), static_cast<unsigned long long>(gtimer()));
+}
+// diagnostics: set this CTA's SM in the 3-word SM bitmask at tl[w]
+__device__ __forceinline__ void tl_smid(uint64_t* tl, int w) {
+  uint32_t sm;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+  if (tl && sm < 192) atomicOr(reinterpret_cast<unsigned long long*>(tl + w + sm / 64), 1ull << (sm % 64));
 }
 
 // ---------------------------------------------------------------- mbarrier / bulk-copy PTX (sm_100a)
@@ -412,7 +421,7 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
 // per-CTA phase durations: slot e accumulates (sum of ns, count) — averaged by tools/timeline.py
 __device__ __forceinline__ void tl_phase(uint64_t* tl, int e, uint64_t& t_prev) {
   if (tl) {
-    const uint64_t t = gtimer();
+    const uint64_t t = ptimer();
     atomicAdd(reinterpret_cast<unsigned long long*>(tl + 2 * e), static_cast<unsigned long long>(t - t_prev));
     atomicAdd(reinterpret_cast<unsigned long long*>(tl + 2 * e + 1), 1ull);
     t_prev = t;

@@ -12,7 +12,10 @@ namespace tkv {
 
 constexpr int kSamples = 4096;       // sampled rows per (b, kv head) for the threshold estimate
 constexpr int kSampleThreads = 256;  // sample-scoring CTA
-constexpr int kThrThreads = 512;     // threshold CTA (one per (b, q head)); 512 so it fits beside a scan CTA (registers)
+#ifndef TKV_THR_THREADS
+#define TKV_THR_THREADS 512
+#endif
+constexpr int kThrThreads = TKV_THR_THREADS;  // threshold CTA (one per (b, q head))
 constexpr int kScanWarps = 8;        // scan kernel CTA = 8 warps
 constexpr int kScanU = 2;            // 16-row tiles per warp per iteration
 constexpr int kScanRows = kScanWarps * 16 * kScanU;  // rows per CTA iteration

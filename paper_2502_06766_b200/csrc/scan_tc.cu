@@ -82,7 +82,14 @@ struct UnitWalk {
   }
 };
 
-__global__ void __launch_bounds__(kTcScanThreads, 1) scan_tc_kernel(const __grid_constant__ CUtensorMap kmap,
+// (diagnostic builds cap the registers at the release count: the timers would otherwise push
+// the kernel past the register budget that lets threshold / k-th CTAs share its SMs)
+#ifdef TKV_DIAG
+__global__ void __launch_bounds__(kTcScanThreads) __maxnreg__(120) scan_tc_kernel(
+#else
+__global__ void __launch_bounds__(kTcScanThreads, 1) scan_tc_kernel(
+#endif
+    const __grid_constant__ CUtensorMap kmap,
                                                                 ScanParams p, int n_stages, int flush_every,
                                                                 int mode) {
   extern __shared__ uint8_t smem_raw[];
@@ -91,12 +98,17 @@ __global__ void __launch_bounds__(kTcScanThreads, 1) scan_tc_kernel(const __grid
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   pdl_trigger();  // the k-th kernel may launch now; it waits for this grid to complete
 #ifdef TKV_DIAG
-  const uint64_t t_cta = p.tl ? gtimer() : 0ull;
+  const uint64_t t_cta = p.tl ? ptimer() : 0ull;
 #endif
   if (tid == 0) {
     tl_start(p.tl, 3);
     tl_start(p.tl, 40);  // first / last CTA start
     tl_end(p.tl, 40);
+#ifdef TKV_DIAG
+    // SMs whose scan CTA started > 6 us after the step's first kernel
+    if (p.tl && gtimer() > p.tl[0] + 6000ull) tl_smid(p.tl, 122);
+    tl_smid(p.tl, 125);  // SMs hosting a scan CTA
+#endif
   }
   TcPipe t = tc_setup(smem_raw, s_bar, &s_tmem, p.G, flush_every, n_stages, &kmap, tid == 0, warp == 1,
                       kTcScanGroups);
@@ -124,9 +136,9 @@ __global__ void __launch_bounds__(kTcScanThreads, 1) scan_tc_kernel(const __grid
       tc_mma_acquire(t, i);
 #ifdef TKV_DIAG
       if (p.tl) {
-        const uint64_t t_w = gtimer();
+        const uint64_t t_w = ptimer();
         mbar_wait(t.full(static_cast<int>(i % t.n_stages)), (i / t.n_stages) & 1u);
-        d_wait += gtimer() - t_w;
+        d_wait += ptimer() - t_w;
         ++n_units;
       }
 #endif
@@ -169,10 +181,10 @@ __global__ void __launch_bounds__(kTcScanThreads, 1) scan_tc_kernel(const __grid
       if (i % kTcScanGroups != group) continue;
       uint32_t v[16];
 #ifdef TKV_DIAG
-      uint64_t t_u = p.tl ? gtimer() : 0ull;
+      uint64_t t_u = p.tl ? ptimer() : 0ull;
       if (p.tl) {  // diagnostics: the epilogue's wait for the unit's scores
         mbar_wait(t.tfull(static_cast<int>(i % kTcAcc)), (i / kTcAcc) & 1u);
-        const uint64_t t1 = gtimer();
+        const uint64_t t1 = ptimer();
         d_wait += t1 - t_u;
         t_u = t1;
       }
@@ -182,16 +194,16 @@ __global__ void __launch_bounds__(kTcScanThreads, 1) scan_tc_kernel(const __grid
                   !(mode & 3) /* diagnostics never emit */);
 #ifdef TKV_DIAG
       if (p.tl) {
-        d_work += gtimer() - t_u;
+        d_work += ptimer() - t_u;
         ++n_units;
       }
-      const uint64_t t_f = p.tl ? gtimer() : 0ull;
+      const uint64_t t_f = p.tl ? ptimer() : 0ull;
 #endif
       if (++since == flush_every) {
         tc_warp_flush(p.cand, p.cap, p.hs.cand_cnt, p.hs.hist, p.G, bh0, wbuf, t.cap, cnt, thr, shift, lane);
 #ifdef TKV_DIAG
         if (p.tl) {
-          d_flush += gtimer() - t_f;
+          d_flush += ptimer() - t_f;
           ++n_flush;
         }
 #endif

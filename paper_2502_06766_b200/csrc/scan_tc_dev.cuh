@@ -76,6 +76,22 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
       : "memory");
 }
+// the same with an L2 eviction-priority policy (createpolicy): the K stream is read exactly
+// once, so it goes in evict-first and does not push the candidates, histograms, per-head state
+// and the later kernels' code out of L2
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void tma_load_2d_hint(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar,
+                                                 uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+      "%3}], [%4], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar), "l"(pol)
+      : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
@@ -192,8 +208,14 @@ __device__ __forceinline__ void tc_produce(const TcPipe& t, uint32_t i, const CU
     mbar_arrive(t.full(st));
   } else if (lane == 0) {
     mbar_expect_tx(t.full(st), kTcUnitBytes);
+#ifndef TKV_TC_NO_EVICT_FIRST
+    const uint64_t pol = l2_evict_first_policy();
+    tma_load_2d_hint(t.sA + st * kTcUnitBytes, kmap, 0, grow, t.full(st), pol);
+    tma_load_2d_hint(t.sA + st * kTcUnitBytes + kTcHalfBytes, kmap, 64, grow, t.full(st), pol);
+#else
     tma_load_2d(t.sA + st * kTcUnitBytes, kmap, 0, grow, t.full(st));
     tma_load_2d(t.sA + st * kTcUnitBytes + kTcHalfBytes, kmap, 64, grow, t.full(st));
+#endif
   }
   __syncwarp();
 }

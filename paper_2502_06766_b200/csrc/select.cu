@@ -339,8 +339,25 @@ __global__ void __cluster_dims__(kKthCtas, 1, 1) __launch_bounds__(kKthThreads, 
   __shared__ uint32_t s_nb;     // this CTA's bucket members
   __shared__ uint64_t s_vmax;   // this CTA's largest candidate
 
+#ifdef TKV_DIAG
+  if (threadIdx.x == 0) {
+    tl_start(p.tl, 53);  // first / last CTA resident (before the wait)
+    tl_end(p.tl, 53);
+  }
+#endif
   pdl_wait();  // candidates and histograms of the scan
   if (threadIdx.x == 0) tl_start(p.tl, 5);
+#ifdef TKV_DIAG
+  if (threadIdx.x == 0) {
+    tl_start(p.tl, 54);  // first / last CTA past the wait
+    tl_end(p.tl, 54);
+  }
+  uint64_t t_ph = p.tl ? ptimer() : 0ull;
+#define TKV_KTH_PHASE(e) \
+  if (threadIdx.x == 0) tl_phase(p.tl, e, t_ph)
+#else
+#define TKV_KTH_PHASE(e)
+#endif
   const int bh = p.bh_begin + blockIdx.y, part = blockIdx.x, P = gridDim.x;
   const int b = bh / p.Hq, h = bh % p.Hq;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -402,11 +419,13 @@ __global__ void __cluster_dims__(kKthCtas, 1, 1) __launch_bounds__(kKthThreads, 
   uint32_t dstar = 0, need = 0, bcnt = 0;
   bool whole = true;
   const bool narrow2 = p.k2 > 0 && p.k2 < kb;  // a narrow list shorter than the selection
+  TKV_KTH_PHASE(55);
   if (!all || narrow2) {
     const uint32_t* gh = p.hs.hist + static_cast<int64_t>(bh) * kHistBins;
     copy_g2s_u32<KT, kHistBins>(s_hist, gh, kHistBins);
     __syncthreads();
   }
+  TKV_KTH_PHASE(56);
   if (!all) {
     find_bucket<KT, kHistBins>(s_hist, static_cast<uint32_t>(kb), s_out, s_scr);
     dstar = s_out[0];
@@ -423,6 +442,7 @@ __global__ void __cluster_dims__(kKthCtas, 1, 1) __launch_bounds__(kKthThreads, 
                           : ~0ull;  // the k2-th sits in the top (clamped) bucket: send none
   }
   const bool refine = !all && !whole;
+  TKV_KTH_PHASE(21);
   // bucket members are collected in this CTA's shared memory; more than fit (heavy exact
   // ties) → radix passes over the head's candidates in the cluster's rank 0
   const bool big = refine && bcnt > static_cast<uint32_t>(kKthSmemBucket);
@@ -463,6 +483,7 @@ __global__ void __cluster_dims__(kKthCtas, 1, 1) __launch_bounds__(kKthThreads, 
     for (int w = 0; w < KW; ++w) m = s_rmax[w] > m ? s_rmax[w] : m;
     s_vmax = m;
   }
+  TKV_KTH_PHASE(22);
   // ---- the head's CTAs form a cluster: rank 0 pulls the other CTAs' maxima and bucket members
   // through distributed shared memory (no global atomics, no head ticket)
   cg::cluster_group cluster = cg::this_cluster();
@@ -485,6 +506,7 @@ __global__ void __cluster_dims__(kKthCtas, 1, 1) __launch_bounds__(kKthThreads, 
   }
   cluster.sync();  // remote reads done: the other CTAs may exit
   if (!lead) return;
+  TKV_KTH_PHASE(23);
 
   // ---- rank 0: exact threshold
   uint64_t T;
@@ -515,6 +537,7 @@ __global__ void __cluster_dims__(kKthCtas, 1, 1) __launch_bounds__(kKthThreads, 
     p.meta_kb[bh] = static_cast<int32_t>(kb);
     p.meta_max[bh] = key_score(comp_key(vmax));
     if (p.k2 > 0 && !narrow2) p.meta_t2[bh] = T;  // the narrow list is the whole selection
+    TKV_KTH_PHASE(24);
     if (p.pass == kPassFallback) {
       p.hs.flag_fail[bh] = 0u;
       p.hs.group_fail[b * p.Hkv + h / p.G] = 0u;
@@ -592,7 +615,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_topk_kernel(HeadParams h
   __shared__ float s_l[HW];
 
   pdl_wait();  // candidates and histograms of the scan
-  uint64_t t_ph = p.tl ? gtimer() : 0ull;
+  uint64_t t_ph = p.tl ? ptimer() : 0ull;
   if (threadIdx.x == 0) tl_start(p.tl, 5);
   const int C = hp.ctas_per_head;
   const int bh = p.bh_begin + static_cast<int>(blockIdx.x) / C, c = static_cast<int>(blockIdx.x) % C;

@@ -176,7 +176,7 @@ __device__ __forceinline__ uint32_t block_excl(uint32_t v, uint32_t* wsum, uint3
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(MT, 1) shard_merge_kernel(ShardMergeParams p) {
   extern __shared__ __align__(16) uint8_t dyn[];
 #ifdef TKV_DIAG
-  uint64_t t_ph = p.tl ? gtimer() : 0ull;
+  uint64_t t_ph = p.tl ? ptimer() : 0ull;
 #endif
   MergeSmem& s = *reinterpret_cast<MergeSmem*>(dyn);
   cg::cluster_group cluster = cg::this_cluster();

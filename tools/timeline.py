@@ -14,17 +14,19 @@ NAMES = ["sample", "threshold", "threshold past wait", "scan", "scan epilogue pa
 PHASES = ["head CTA: start→params", "→hist+bucket", "→pass 1 (max, bucket members)", "→T",
           "→pads/meta + barriers", "→compaction loop", "→out_cnt reservation", "→V gather loop", "→ids written",
           "→partial slot written", "→finished (last CTA)",
-          "kth CTA: start→hist+bucket", "→slice scan", "→ticket (last CTA)", "→T written (last CTA)",
+          "kth CTA: past wait→hist+bucket", "→slice scan + max", "→cluster sync + pulls (rank 0)", "→T written (rank 0)",
           "threshold CTA: past wait→samples in smem", "→sample max", "→radix select (t_h)", "→hist zeroed, state written",
           "scan epilogue: one warp flush"]
 
 
-EXTRA_EVENTS = {40: "scan CTA start", 41: "scan CTA end", 45: "threshold CTA past wait"}
+EXTRA_EVENTS = {40: "scan CTA start", 41: "scan CTA end", 45: "threshold CTA past wait",
+                53: "k-th CTA resident", 54: "k-th CTA past wait"}
 EXTRA_PHASES = {42: "scan epilogue: wait for a unit's scores", 43: "scan epilogue: ld+emit of a unit",
                 44: "scan MMA warp: wait for a unit's TMA", 46: "scan CTA lifetime",
                 47: "merge: start→bounds + narrow count + rule", 48: "→histogram + cluster sums + bucket",
                 49: "→bucket count", 50: "→members + barrier", 51: "→rank select + barrier",
-                52: "→emit (2 passes) + barrier"}
+                52: "→emit (2 passes) + barrier",
+                55: "kth CTA: past wait→state loads", 56: "kth CTA: →hist in smem (then bucket)"}
 
 
 def main():
@@ -83,7 +85,8 @@ def main():
             tkv.topk_decode_attention(q, K, V, nc, k, **kw)
             lib.tkv_debug_timeline(None)
         torch.cuda.synchronize()
-        t = buf.cpu().numpy().view(np.uint64).astype(np.float64)
+        raw = buf.cpu().numpy().view(np.uint64)
+        t = raw.astype(np.float64)
         t0 = t[0]
         if it >= 3:
             for j in range(len(PHASES)):
@@ -102,6 +105,14 @@ def main():
                 if t[2 * e + 1] > 0:
                     xp[e] += t[2 * e] / t[2 * e + 1] / 1e3
     acc /= args.steps
+
+    def sms(w):  # SM bitmask words (tl_smid) of the last step
+        return {64 * i + b for i in range(3) for b in range(64) if (int(raw[w + i]) >> b) & 1}
+
+    thr_sms, late_sms, scan_sms = sms(119), sms(122), sms(125)
+    if scan_sms:
+        print(f"  SMs: scan CTAs on {len(scan_sms)}, threshold CTAs on {len(thr_sms)}, scan CTAs starting "
+              f">6 us late on {len(late_sms)} (of which {len(late_sms & thr_sms)} host a threshold CTA)")
     for e, nm in enumerate(NAMES):
         print(f"  {nm:26s} start {acc[e, 0]:8.1f}  end {acc[e, 1]:8.1f} us")
     for j, nm in enumerate(PHASES):
