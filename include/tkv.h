@@ -228,6 +228,29 @@ int tkv_convert_rows_f32(const float* src, int64_t rows, int32_t d, void* dst, v
 int tkv_workspace_fallbacks(const tkv_problem* p, const void* workspace, size_t workspace_bytes,
                             uint32_t* heads);
 
+/* ---- Decode-step integration helpers (paper_2502_06766_b200/model.py, BASELINE cfg4): the
+ * non-attention elementwise work of one batch-1 layer step, fused (csrc/model_glue.cu). They
+ * replace the reference model's per-step NumPy glue around decode_step (reference
+ * model.py:255-263 projections / MLP, attention.py:202-233 per-layer loop); all tensors are
+ * device pointers, bf16 unless noted, batch 1.
+ *   add_rmsnorm:      x[d] += delta[d] (delta may be NULL), h[d] = RMSNorm(x) * w (w f32)
+ *   qkv_rope_append:  qkv = [Hq + 2 Hkv][head_dim] projections of this token; RoPE (cos/sin f32
+ *                     tables [rows][head_dim/2], row *pos) of q -> q_out [Hq][head_dim] and of k;
+ *                     k, v written to the caches' row n_ctx[0] + n_win[0] (caches
+ *                     [Hkv][cache_rows][head_dim]); the window counter is not advanced
+ *   silu_mul:         out[f] = silu(gate_up[f]) * gate_up[ffn + f]
+ *   logits_argmax:    token[0] = first index of the maximum of logits[n] (bf16); logits_f32
+ *                     (may be NULL) receives the f32 copy; scratch: 2 zeroed uint64 words,
+ *                     left zeroed for the next call */
+int tkv_model_add_rmsnorm(void* x, const void* delta, const float* w, float eps, void* h, int32_t d, void* stream);
+int tkv_model_qkv_rope_append(const void* qkv, const float* cos_t, const float* sin_t, const int64_t* pos,
+                              void* q_out, void* k_cache, void* v_cache, const int32_t* n_ctx,
+                              const int32_t* n_win, int64_t cache_rows, int32_t n_heads, int32_t n_kv_heads,
+                              int32_t head_dim, void* stream);
+int tkv_model_silu_mul(const void* gate_up, void* out, int32_t ffn, void* stream);
+int tkv_model_logits_argmax(const void* logits, int32_t n, float* logits_f32, int64_t* token, uint64_t* scratch,
+                            void* stream);
+
 /* Number of kernels the last compute call on this thread enqueued (for launch accounting). */
 int tkv_last_launch_count(void);
 

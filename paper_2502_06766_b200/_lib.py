@@ -43,6 +43,10 @@ EXPORTS = (
     "tkv_profile_scan_events",
     "tkv_debug_timeline",
     "tkv_convert_rows_f32",
+    "tkv_model_add_rmsnorm",
+    "tkv_model_qkv_rope_append",
+    "tkv_model_silu_mul",
+    "tkv_model_logits_argmax",
 )
 
 COMBINE_JOINT = 0
@@ -119,6 +123,12 @@ _SIG = {
         [ctypes.POINTER(Problem), _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P], _I),
     "tkv_shard_finalize": (
         [ctypes.POINTER(Problem), _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P], _I),
+    "tkv_model_add_rmsnorm": ([_P, _P, _P, ctypes.c_float, _P, ctypes.c_int32, _P], _I),
+    "tkv_model_qkv_rope_append": (
+        [_P, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _P],
+        _I),
+    "tkv_model_silu_mul": ([_P, _P, ctypes.c_int32, _P], _I),
+    "tkv_model_logits_argmax": ([_P, ctypes.c_int32, _P, _P, _P, _P], _I),
 }
 
 _lock = threading.Lock()

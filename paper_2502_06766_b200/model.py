@@ -20,7 +20,7 @@ from dataclasses import dataclass
 
 import torch
 
-from . import ops
+from . import _lib, ops
 from .budget import LayerBudget
 from .errors import ConfigError, InputError
 
@@ -170,11 +170,27 @@ class TopkLlamaDecoder:
         self.graph = None
         self.pos.fill_(n_ctx)
         self.win_used = 0  # host mirror of n_win: capacity is checked before a step is enqueued
+        if dev.type == "cuda":  # persistent activations of the fused CUDA step (_step_body_cuda)
+            nqkv = (self.hq + 2 * self.hkv) * hd
+            self._x = torch.empty((1, s.d_model), dtype=bf, device=dev)  # residual stream
+            self._h = torch.empty((1, s.d_model), dtype=bf, device=dev)
+            self._qkv = torch.empty((1, nqkv), dtype=bf, device=dev)
+            self._q = torch.empty((1, self.hq, hd), dtype=bf, device=dev)
+            self._a = torch.empty((1, self.hq * hd), dtype=bf, device=dev)
+            self._o = torch.empty((1, s.d_model), dtype=bf, device=dev)
+            self._gu = torch.empty((1, 2 * self.ffn), dtype=bf, device=dev)
+            self._act = torch.empty((1, self.ffn), dtype=bf, device=dev)
+            self._d = torch.empty((1, s.d_model), dtype=bf, device=dev)
+            self._lg = torch.empty((1, s.vocab), dtype=bf, device=dev)
+            self._am = torch.zeros(2, dtype=torch.int64, device=dev)  # argmax scratch (self-resetting)
+            self._n_win_next = torch.empty_like(self.n_win)
 
-    def _attend(self, layer: int, lw: dict, q: torch.Tensor, kk: torch.Tensor, v: torch.Tensor) -> torch.Tensor:
+    def _attend(self, layer: int, lw: dict, q: torch.Tensor, kk, v) -> torch.Tensor:
         """Window append of this token's k/v (attention.py:210; n_win advances once per step,
-        after the last layer) + top-k attention of this rank's heads (libtkv, one call)."""
-        ops.kv_append(lw["K"], lw["V"], kk, v, self.n_win, base=self.n_ctx, advance=False)
+        after the last layer; kk = v = None: already appended by the fused RoPE kernel) + top-k
+        attention of this rank's heads (libtkv, one call)."""
+        if kk is not None:
+            ops.kv_append(lw["K"], lw["V"], kk, v, self.n_win, base=self.n_ctx, advance=False)
         kl = self.budget[layer]
         idx, scores = self._sel[kl]
         ops.topk_decode_attention(q, lw["K"], lw["V"], self.n_ctx, kl, n_win=self._n_win_next,
@@ -216,6 +232,9 @@ class TopkLlamaDecoder:
         return x
 
     def _step_body(self) -> None:
+        if self.device.type == "cuda":
+            self._step_body_cuda()
+            return
         x = self.embed.index_select(0, self.token)
         self._n_win_next = self.n_win + 1  # the token attends to itself (attention.py:210)
         for layer, lw in enumerate(self.layers):
@@ -223,6 +242,43 @@ class TopkLlamaDecoder:
         logits = rmsnorm(x, self.norm_f, self.shape.eps) @ self.lm_head
         self.logits.copy_(logits)
         self.next_token.copy_(logits.argmax(-1))
+        self.n_win.add_(1)
+        self.pos.add_(1)
+
+    def _step_body_cuda(self) -> None:
+        """One step on the device, ~14 launches per layer: fused residual-add + RMSNorm, the QKV
+        GEMV, fused RoPE + window append, top-k attention (libtkv), O projection (+ the TP
+        all-reduce), fused residual-add + RMSNorm, gate/up GEMV, fused SiLU·up, down GEMV (+ the
+        all-reduce); then the final norm, LM head and a fused logits copy + argmax
+        (csrc/model_glue.cu). Same numerics as the eager path (bf16 storage, fp32 math)."""
+        s, dev = self.shape, self.device
+        st = ops._stream(dev)
+        vp = ops._vp
+        torch.index_select(self.embed, 0, self.token, out=self._x)
+        torch.add(self.n_win, 1, out=self._n_win_next)  # the token attends to itself (attention.py:210)
+        delta = None
+        for layer, lw in enumerate(self.layers):
+            _lib.call("tkv_model_add_rmsnorm", vp(self._x), vp(delta), vp(lw["n1"]), s.eps, vp(self._h),
+                      s.d_model, st)
+            torch.mm(self._h, lw["wqkv"], out=self._qkv)
+            _lib.call("tkv_model_qkv_rope_append", vp(self._qkv), vp(self.cos), vp(self.sin), vp(self.pos),
+                      vp(self._q), vp(lw["K"]), vp(lw["V"]), vp(self.n_ctx), vp(self.n_win), self.rows, self.hq,
+                      self.hkv, s.head_dim, st)
+            attn = self._attend(layer, lw, self._q, None, None)
+            self._a.copy_(attn.view(1, -1))
+            torch.mm(self._a, lw["wo"], out=self._o)
+            delta = self._reduce(self._o)
+            _lib.call("tkv_model_add_rmsnorm", vp(self._x), vp(delta), vp(lw["n2"]), s.eps, vp(self._h),
+                      s.d_model, st)
+            torch.mm(self._h, lw["wgu"], out=self._gu)
+            _lib.call("tkv_model_silu_mul", vp(self._gu), vp(self._act), self.ffn, st)
+            torch.mm(self._act, lw["wd"], out=self._d)
+            delta = self._reduce(self._d)
+        _lib.call("tkv_model_add_rmsnorm", vp(self._x), vp(delta), vp(self.norm_f), s.eps, vp(self._h),
+                  s.d_model, st)
+        torch.mm(self._h, self.lm_head, out=self._lg)
+        _lib.call("tkv_model_logits_argmax", vp(self._lg), s.vocab, vp(self.logits), vp(self.next_token),
+                  vp(self._am), st)
         self.n_win.add_(1)
         self.pos.add_(1)
 
