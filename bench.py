@@ -47,6 +47,8 @@ CONFIGS = {
     "cfg2": dict(B=1, N=131072, k=2048),
     "cfg3": dict(B=1, N=1 << 20, k=16384),
     "cfg5": dict(B=16, N=262144, k=4096),
+    # one rank's shard of cfg3 at 8 GPUs (its local top-k over 131,072 rows): diagnostics only
+    "cfg3_g8": dict(B=1, N=131072, k=16384),
 }
 METRIC = "us_per_layer_decode_step"
 WINDOW_CAP = 256

@@ -395,6 +395,7 @@ AttendParams make_attend(const tkv_problem* p, const void* q, const void* k_cach
   a.part_o = at<float>(ws, L.po);
   a.ticket = at<uint32_t>(ws, L.ticket_g);
   a.nchunks = L.nchunks;
+  a.items_mult = diag_env("TKV_ATT_MULT", 1);  // experiments (TKV_DIAG builds): items per gather CTA
   a.cand = at<uint64_t>(ws, L.cand);
   a.cap = L.cap;
   a.cand_cnt = at<uint32_t>(ws, L.cnt);

@@ -39,7 +39,8 @@ __device__ __forceinline__ void attend_cand_run(const AttendParams& p, AttSmem& 
   __syncthreads();
   uint32_t total_chunks = 0;
   for (int w = 0; w < NW; ++w) total_chunks += sm.wcnt[w];
-  const int S = total_chunks > gridDim.x ? static_cast<int>((total_chunks + gridDim.x - 1) / gridDim.x) : 1;
+  const uint32_t slots = gridDim.x * static_cast<uint32_t>(p.items_mult > 0 ? p.items_mult : 1);
+  const int S = total_chunks > slots ? static_cast<int>((total_chunks + slots - 1) / slots) : 1;
   __syncthreads();
   auto nslots_of = [&](int lh) -> int {
     const int c = chunks_of(lh);

@@ -201,7 +201,10 @@ __device__ void gather_acc(const AttendParams& p, int bh, int nrows, const AttSm
   const int half = lane >> 4, part = lane & 15;
   const __nv_bfloat16* vb =
       p.vc + (static_cast<int64_t>(b) * p.Hkv + kvh) * p.cache_rows * kD + part * 8;
-  constexpr int UNR = 8;
+#ifndef TKV_GATHER_UNR
+#define TKV_GATHER_UNR 8
+#endif
+  constexpr int UNR = TKV_GATHER_UNR;
   for (int r0 = warp * 2 + half; r0 < nrows; r0 += 2 * NW * UNR) {
     uint4 v[UNR];
     float w[UNR];

@@ -213,6 +213,7 @@ struct AttendParams {
   // (l, o[128]) partials read through device pointers, when n_peers > 0
   const float* const* partial_peers;
   int n_peers;
+  int items_mult;  // candidate mode: work items per CTA, about (0 = 1)
 };
 
 // shard_merge_kernel (shard.cu): exact global top-k over every rank's published candidate lists

@@ -85,7 +85,7 @@ struct UnitWalk {
 // (diagnostic builds cap the registers at the release count: the timers would otherwise push
 // the kernel past the register budget that lets threshold / k-th CTAs share its SMs)
 #ifdef TKV_DIAG
-__global__ void __launch_bounds__(kTcScanThreads) __maxnreg__(120) scan_tc_kernel(
+__global__ void __maxnreg__(120) scan_tc_kernel(
 #else
 __global__ void __launch_bounds__(kTcScanThreads, 1) scan_tc_kernel(
 #endif
