@@ -992,3 +992,6 @@ int tkv_shard_finalize(const tkv_problem* p, const void* q, const void* k_cache,
 }
 
 }  // extern "C"
+
+// error reporting for the other translation units' C entry points (model_glue.cu)
+int tkv::api_fail(int code, const char* msg) { return fail(code, "%s", msg); }

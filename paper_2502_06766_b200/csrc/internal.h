@@ -155,6 +155,9 @@ struct SelectParams {
   int fb_scan_smem;
 };
 
+// sets tkv_last_error's message and returns code (api.cu)
+int api_fail(int code, const char* msg);
+
 // host-side preparation of the device-tail-launched fallback kernels (select.cu)
 void prepare_fallback_kernels();
 

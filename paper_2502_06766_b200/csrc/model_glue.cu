@@ -12,6 +12,7 @@
 // Numerics follow the eager code they replace (model.py history): bf16 storage, fp32 math,
 // the same roundings to bf16.
 #include <math.h>
+#include <stdio.h>
 
 #include "common.cuh"
 #include "internal.h"
@@ -134,6 +135,14 @@ __global__ void __launch_bounds__(256) logits_argmax_kernel(const __nv_bfloat16*
 
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+int launched(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) return TKV_OK;
+  char buf[256];
+  snprintf(buf, sizeof(buf), "%s launch: %s", what, cudaGetErrorString(e));
+  return api_fail(TKV_ECUDA, buf);
+}
+
 }  // namespace
 }  // namespace tkv
 
@@ -142,44 +151,47 @@ using namespace tkv;
 extern "C" {
 
 int tkv_model_add_rmsnorm(void* x, const void* delta, const float* w, float eps, void* h, int32_t d, void* stream) {
-  if (!x || !w || !h || d <= 0) return TKV_EBADSHAPE;
+  if (!x || !w || !h || d <= 0) return api_fail(TKV_EBADSHAPE, "tkv_model_add_rmsnorm: null tensor or d <= 0");
   add_rmsnorm_kernel<<<1, kNormThreads, 0, as_stream(stream)>>>(
       static_cast<__nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(delta), w, eps,
       static_cast<__nv_bfloat16*>(h), d);
-  return cudaGetLastError() == cudaSuccess ? TKV_OK : TKV_ECUDA;
+  return launched("tkv_model kernel");
 }
 
 int tkv_model_qkv_rope_append(const void* qkv, const float* cos_t, const float* sin_t, const int64_t* pos,
                               void* q_out, void* k_cache, void* v_cache, const int32_t* n_ctx,
                               const int32_t* n_win, int64_t cache_rows, int32_t n_heads, int32_t n_kv_heads,
                               int32_t head_dim, void* stream) {
-  if (!qkv || !cos_t || !sin_t || !pos || !q_out || !k_cache || !v_cache || !n_ctx || !n_win) return TKV_EBADSHAPE;
-  if (head_dim != kD || n_heads <= 0 || n_kv_heads <= 0 || cache_rows <= 0) return TKV_EBADSHAPE;
+  if (!qkv || !cos_t || !sin_t || !pos || !q_out || !k_cache || !v_cache || !n_ctx || !n_win)
+    return api_fail(TKV_EBADSHAPE, "tkv_model_qkv_rope_append: null tensor");
+  if (head_dim != kD || n_heads <= 0 || n_kv_heads <= 0 || cache_rows <= 0)
+    return api_fail(TKV_EBADSHAPE, "tkv_model_qkv_rope_append: head_dim must be 128, head counts and rows > 0");
   qkv_rope_append_kernel<<<n_heads + 2 * n_kv_heads, 64, 0, as_stream(stream)>>>(
       static_cast<const __nv_bfloat16*>(qkv), cos_t, sin_t, pos, static_cast<__nv_bfloat16*>(q_out),
       static_cast<__nv_bfloat16*>(k_cache), static_cast<__nv_bfloat16*>(v_cache), n_ctx, n_win, cache_rows,
       n_heads, n_kv_heads);
-  return cudaGetLastError() == cudaSuccess ? TKV_OK : TKV_ECUDA;
+  return launched("tkv_model kernel");
 }
 
 int tkv_model_silu_mul(const void* gate_up, void* out, int32_t ffn, void* stream) {
-  if (!gate_up || !out || ffn <= 0) return TKV_EBADSHAPE;
+  if (!gate_up || !out || ffn <= 0) return api_fail(TKV_EBADSHAPE, "tkv_model_silu_mul: null tensor or ffn <= 0");
   int grid = (ffn + 255) / 256;
   grid = grid > 148 * 4 ? 148 * 4 : grid;
   silu_mul_kernel<<<grid, 256, 0, as_stream(stream)>>>(static_cast<const __nv_bfloat16*>(gate_up),
                                                        static_cast<__nv_bfloat16*>(out), ffn);
-  return cudaGetLastError() == cudaSuccess ? TKV_OK : TKV_ECUDA;
+  return launched("tkv_model kernel");
 }
 
 int tkv_model_logits_argmax(const void* logits, int32_t n, float* logits_f32, int64_t* token, uint64_t* scratch,
                             void* stream) {
-  if (!logits || !token || !scratch || n <= 0) return TKV_EBADSHAPE;
+  if (!logits || !token || !scratch || n <= 0)
+    return api_fail(TKV_EBADSHAPE, "tkv_model_logits_argmax: null tensor or n <= 0");
   int grid = (n + 255) / 256;
   grid = grid > 148 * 2 ? 148 * 2 : grid;
   logits_argmax_kernel<<<grid, 256, 0, as_stream(stream)>>>(static_cast<const __nv_bfloat16*>(logits), n,
                                                             logits_f32, token,
                                                             reinterpret_cast<unsigned long long*>(scratch));
-  return cudaGetLastError() == cudaSuccess ? TKV_OK : TKV_ECUDA;
+  return launched("tkv_model kernel");
 }
 
 }  // extern "C"

@@ -96,6 +96,15 @@ def test_compute_entry_rejects_bad_arguments_before_any_launch():
     assert rc == errors.TKV_EBADSHAPE and "q is NULL" in _lib.last_error()
     rc = lib.tkv_kv_append(1, 8, 128, 10, None, None, None, None, None, None, 1, None)
     assert rc == errors.TKV_EBADSHAPE
+    # the decode-step helpers validate before launching, with a message
+    rc = lib.tkv_model_add_rmsnorm(None, None, None, 1e-5, None, 4096, None)
+    assert rc == errors.TKV_EBADSHAPE and "tkv_model_add_rmsnorm" in _lib.last_error()
+    rc = lib.tkv_model_qkv_rope_append(*([None] * 9), 10, 8, 2, 64, None)
+    assert rc == errors.TKV_EBADSHAPE and "qkv_rope_append" in _lib.last_error()
+    rc = lib.tkv_model_silu_mul(None, None, 0, None)
+    assert rc == errors.TKV_EBADSHAPE and "silu_mul" in _lib.last_error()
+    rc = lib.tkv_model_logits_argmax(None, 10, None, None, None, None)
+    assert rc == errors.TKV_EBADSHAPE and "logits_argmax" in _lib.last_error()
 
 
 def test_status_mapping():
