@@ -178,8 +178,8 @@ __device__ __forceinline__ void mark_pinned(const AttendParams& p, int bh, int64
 }
 
 struct AttSmem {
-  float w[kCandChunk];
-  int32_t row[kCandChunk];
+  __align__(16) float w[kCandChunk];
+  __align__(16) int32_t row[kCandChunk];
   float red[NW][kD];
   float l[NW];
   float z[128];
@@ -192,7 +192,10 @@ struct AttSmem {
 
 // Accumulate the V rows listed in sm.row (local rows, -1 = skip) weighted by sm.w into this
 // thread's registers: lane part·8 .. +7 of the 128 dims (16 lanes per 256-byte row, 16-byte
-// loads, 8 rows in flight per half-warp), and the weight sum. Leaves sm.row / sm.w intact.
+// loads), and the weight sum. A half-warp takes 8 consecutive list entries per round — their
+// ids and weights arrive as two broadcast 16-byte shared loads each instead of eight scalar
+// ones (ncu, cfg3: the per-row id load and its bounds test were 11 % of the kernel's
+// instructions) — and keeps their 8 rows in flight. Leaves sm.row / sm.w intact.
 template <class Gp = CtaGrp>
 __device__ void gather_acc(const AttendParams& p, int bh, int nrows, const AttSmem& sm, float (&acc)[8],
                            float& lw) {
@@ -201,22 +204,25 @@ __device__ void gather_acc(const AttendParams& p, int bh, int nrows, const AttSm
   const int half = lane >> 4, part = lane & 15;
   const __nv_bfloat16* vb =
       p.vc + (static_cast<int64_t>(b) * p.Hkv + kvh) * p.cache_rows * kD + part * 8;
-#ifndef TKV_GATHER_UNR
-#define TKV_GATHER_UNR 8
-#endif
-  constexpr int UNR = TKV_GATHER_UNR;
-  for (int r0 = warp * 2 + half; r0 < nrows; r0 += 2 * NW * UNR) {
+  constexpr int UNR = 8;
+  for (int r0 = (warp * 2 + half) * UNR; r0 < nrows; r0 += 2 * NW * UNR) {
+    const int4 ra = *reinterpret_cast<const int4*>(&sm.row[r0]);
+    const int4 rb = *reinterpret_cast<const int4*>(&sm.row[r0 + 4]);
+    const float4 wa = *reinterpret_cast<const float4*>(&sm.w[r0]);
+    const float4 wb = *reinterpret_cast<const float4*>(&sm.w[r0 + 4]);
+    const int rr[UNR] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
+    const float ww[UNR] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
     uint4 v[UNR];
     float w[UNR];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
-      const int r = r0 + 2 * NW * u;
-      const int row = r < nrows ? sm.row[r] : -1;
-      w[u] = r < nrows ? sm.w[r] : 0.f;
-      v[u] = row >= 0 ? ldg_stream(vb + static_cast<int64_t>(row) * kD) : make_uint4(0, 0, 0, 0);
+      const bool ok = r0 + u < nrows && rr[u] >= 0;
+      w[u] = ok ? ww[u] : 0.f;
+      v[u] = ok ? ldg_stream(vb + static_cast<int64_t>(rr[u]) * kD) : make_uint4(0, 0, 0, 0);
     }
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
+      if (part == 0) lw += w[u];
       acc[0] = fmaf(w[u], bf16lo(v[u].x), acc[0]);
       acc[1] = fmaf(w[u], bf16hi(v[u].x), acc[1]);
       acc[2] = fmaf(w[u], bf16lo(v[u].y), acc[2]);
@@ -227,7 +233,6 @@ __device__ void gather_acc(const AttendParams& p, int bh, int nrows, const AttSm
       acc[7] = fmaf(w[u], bf16hi(v[u].w), acc[7]);
     }
   }
-  for (int i = tid; i < nrows; i += NT) lw += sm.w[i];
 }
 
 // Reduce the per-thread (acc, lw) of gather_acc over the block into the head's partial slot
