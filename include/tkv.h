@@ -270,10 +270,11 @@ int tkv_profile_scan_events(void* start, void* stop);
  * (slot e = words 2e, 2e+1) of: 0 sample, 1 threshold, 2 threshold past its dependency wait,
  * 3 key scan, 4 scan epilogue past its dependency wait, 5 k-th (or the small-k head kernel),
  * 6 gather, 7-9 head kernel: threshold found / rows compacted / V gathered; and slots 10-20
- * accumulate (sum of ns, count) of the head kernel's per-CTA phase durations; slots 21-63 more
- * first/last stamps and phase sums of the other kernels (see tools/timeline.py). NULL disables.
+ * accumulate (sum of ns, count) of the head kernel's per-CTA phase durations; slots 21-119 more
+ * first/last stamps and phase sums of the other kernels, words 240-248 SM bitmasks (see
+ * tools/timeline.py; diagnostic builds record most of them). NULL disables.
  */
-#define TKV_TIMELINE_WORDS 128
+#define TKV_TIMELINE_WORDS 256
 int tkv_debug_timeline(void* buf);
 
 

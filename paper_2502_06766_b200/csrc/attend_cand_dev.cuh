@@ -14,6 +14,13 @@ namespace {
 // same pass. s_pref: [heads + 1] words of dynamic shared memory.
 __device__ __forceinline__ void attend_cand_run(const AttendParams& p, AttSmem& sm, uint32_t* s_pref) {
   if (threadIdx.x == 0) tl_start(p.tl, 6);
+#ifdef TKV_DIAG
+  uint64_t t_ph = p.tl ? ptimer() : 0ull;
+#define TKV_ATT_PHASE(e) \
+  if (threadIdx.x == 0) tl_phase(p.tl, e, t_ph)
+#else
+#define TKV_ATT_PHASE(e)
+#endif
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int BH = p.bh_count ? p.bh_count : p.B * p.Hq;  // heads [bh_begin, bh_begin + BH)
   auto chunks_of = [&](int lh) -> int {  // kCandQuant-candidate quanta of a head
@@ -75,6 +82,7 @@ __device__ __forceinline__ void attend_cand_run(const AttendParams& p, AttSmem& 
   }
   const uint32_t total = s_pref[BH];
   const float zs = p.scale * kLog2e;
+  TKV_ATT_PHASE(60);
   for (uint32_t item = blockIdx.x; item < total; item += gridDim.x) {
     int lo = 0, hi = BH;  // largest local head with s_pref[lh] <= item
     while (hi - lo > 1) {
@@ -117,6 +125,7 @@ __device__ __forceinline__ void attend_cand_run(const AttendParams& p, AttSmem& 
         cv[u] = (i < cnt && kb > 0) ? src[i] : 0ull;
         sel[u] = cv[u] != 0ull && cv[u] >= T;
       }
+      TKV_ATT_PHASE(61);
       // block-ordered compaction of the selected candidates
       uint32_t mine = 0;
 #pragma unroll
@@ -149,7 +158,9 @@ __device__ __forceinline__ void attend_cand_run(const AttendParams& p, AttSmem& 
         }
       }
       __syncthreads();
+      TKV_ATT_PHASE(62);
       if (p.gather) gather_acc(p, bh, static_cast<int>(m), sm, acc, lw);
+      TKV_ATT_PHASE(63);
       // selected ids / raw scores (order unspecified); the reservation atomic completed
       // during the gather
       const uint32_t obase = sm.base;
@@ -168,11 +179,14 @@ __device__ __forceinline__ void attend_cand_run(const AttendParams& p, AttSmem& 
         }
       }
     }
+    TKV_ATT_PHASE(64);
     if (p.gather) {
       partial_write(p, bh, slot, sm, acc, lw);
+      TKV_ATT_PHASE(65);
       ticket_finish(p, bh, nslots, sm);
     }
     __syncthreads();
+    TKV_ATT_PHASE(66);
   }
   if (threadIdx.x == 0) tl_end(p.tl, 6);
 }

@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(kThrThreads, 4) threshold_kernel(SampleParams 
   if (threadIdx.x == 0) {
     tl_start(p.tl, 45);  // diagnostics: first / last CTA past its wait
     tl_end(p.tl, 45);
-    tl_smid(p.tl, 119);  // SMs hosting a threshold CTA
+    tl_smid(p.tl, 240);  // SMs hosting a threshold CTA
   }
   uint64_t t_ph = p.tl ? ptimer() : 0ull;
 #define TKV_THR_PHASE(e) \

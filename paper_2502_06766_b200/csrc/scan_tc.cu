@@ -106,8 +106,8 @@ __global__ void __launch_bounds__(kTcScanThreads, 1) scan_tc_kernel(
     tl_end(p.tl, 40);
 #ifdef TKV_DIAG
     // SMs whose scan CTA started > 6 us after the step's first kernel
-    if (p.tl && gtimer() > p.tl[0] + 6000ull) tl_smid(p.tl, 122);
-    tl_smid(p.tl, 125);  // SMs hosting a scan CTA
+    if (p.tl && gtimer() > p.tl[0] + 6000ull) tl_smid(p.tl, 243);
+    tl_smid(p.tl, 246);  // SMs hosting a scan CTA
 #endif
   }
   TcPipe t = tc_setup(smem_raw, s_bar, &s_tmem, p.G, flush_every, n_stages, &kmap, tid == 0, warp == 1,

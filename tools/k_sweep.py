@@ -59,7 +59,7 @@ def main():
 
         us = timed()             # default: 4 overlapped parts at this size (>= 4 GB of keys)
         us_p1 = timed(parts=1)   # one part: the plain kernel sequence, for the split below
-        tl = torch.zeros(128, dtype=torch.int64, device=dev)  # TKV_TIMELINE_WORDS
+        tl = torch.zeros(256, dtype=torch.int64, device=dev)  # TKV_TIMELINE_WORDS
         tl[0:20:2] = -1
         lib.tkv_debug_timeline(ctypes.c_void_p(tl.data_ptr()))
         tkv.topk_decode_attention(q, K, V, nc, k, **kw, parts=1)

@@ -70,7 +70,7 @@ def main():
             import ctypes
             import numpy as np
             from tools.timeline import EXTRA_PHASES
-            buf = torch.zeros(128, dtype=torch.int64, device=dev)
+            buf = torch.zeros(256, dtype=torch.int64, device=dev)
             lib = tkv._lib.load()
             lib.tkv_debug_timeline(ctypes.c_void_p(buf.data_ptr()))
             for _ in range(args.steps):

@@ -26,7 +26,11 @@ EXTRA_PHASES = {42: "scan epilogue: wait for a unit's scores", 43: "scan epilogu
                 47: "merge: start→bounds + narrow count + rule", 48: "→histogram + cluster sums + bucket",
                 49: "→bucket count", 50: "→members + barrier", 51: "→rank select + barrier",
                 52: "→emit (2 passes) + barrier",
-                55: "kth CTA: past wait→state loads", 56: "kth CTA: →hist in smem (then bucket)"}
+                55: "kth CTA: past wait→state loads", 56: "kth CTA: →hist in smem (then bucket)",
+                60: "gather CTA: start→item prefix", 61: "gather: →batch candidates loaded",
+                62: "gather: →compaction (2 barriers)", 63: "gather: →V rows accumulated",
+                64: "gather: →ids written (per item)", 65: "gather: →partial written",
+                66: "gather: →ticket / head finish"}
 
 
 def main():
@@ -53,7 +57,7 @@ def main():
     ph = np.zeros(len(PHASES))
     xe = {e: [0.0, 0.0] for e in EXTRA_EVENTS}
     xp = {e: 0.0 for e in EXTRA_PHASES}
-    buf = torch.zeros(128, dtype=torch.int64, device=dev)  # TKV_TIMELINE_WORDS
+    buf = torch.zeros(256, dtype=torch.int64, device=dev)  # TKV_TIMELINE_WORDS
     init = torch.zeros_like(buf)
     init[0:2 * len(NAMES):2] = -1  # UINT64_MAX (first-start slots); phase sums stay 0
     for e in EXTRA_EVENTS:
@@ -109,7 +113,7 @@ def main():
     def sms(w):  # SM bitmask words (tl_smid) of the last step
         return {64 * i + b for i in range(3) for b in range(64) if (int(raw[w + i]) >> b) & 1}
 
-    thr_sms, late_sms, scan_sms = sms(119), sms(122), sms(125)
+    thr_sms, late_sms, scan_sms = sms(240), sms(243), sms(246)
     if scan_sms:
         print(f"  SMs: scan CTAs on {len(scan_sms)}, threshold CTAs on {len(thr_sms)}, scan CTAs starting "
               f">6 us late on {len(late_sms)} (of which {len(late_sms & thr_sms)} host a threshold CTA)")
