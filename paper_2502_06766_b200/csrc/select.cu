@@ -361,7 +361,13 @@ __global__ void __cluster_dims__(kKthCtas, 1, 1) __launch_bounds__(kKthThreads, 
   const int bh = p.bh_begin + blockIdx.y, part = blockIdx.x, P = gridDim.x;
   const int b = bh / p.Hq, h = bh % p.Hq;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (p.pass == kPassFallback && p.hs.flag_fail[bh] == 0u) return;
+  if (p.pass == kPassFallback) {
+    // The candidate-mode gather that follows the fallback rewrites every head's ids from
+    // position 0: a head the small-k head kernel already finished must not append behind its
+    // first copy (that would overwrite the k > kb pads)
+    if (part == 0 && tid == 0) p.hs.out_cnt[bh] = 0u;
+    if (p.hs.flag_fail[bh] == 0u) return;
+  }
 
   const uint64_t* src = p.src + static_cast<int64_t>(bh) * p.src_stride;
   int64_t n = p.hs.cand_cnt[bh];
