@@ -101,3 +101,61 @@ def test_device_sharded_step_graph_capture(cuda):
             for h in range(a.shape[1]):
                 assert set(a[0, h].tolist()) == set(ref[0, h].tolist())
             assert float((out - out1).abs().max()) < 1e-5
+
+
+# TKV_SHARD_FUZZ="start:count" widens the sweep (default 0:24)
+_F0, _FN = (int(v) for v in __import__("os").environ.get("TKV_SHARD_FUZZ", "0:24").split(":"))
+
+
+@pytest.mark.parametrize("seed", range(_F0, _F0 + _FN))
+def test_device_sharded_step_fuzz(cuda, seed):
+    """Random shard counts (uneven shards included), batch, GQA shapes, k from 1 to beyond a
+    shard's rows and beyond N, windows, skew and exact cross-shard ties (duplicated rows): the
+    emulated device-driven step gives the unsharded call's ids and outputs."""
+    from paper_2502_06766_b200 import topk_decode_attention
+
+    r = np.random.default_rng(seed)
+    G = int(r.choice([2, 3, 4, 8]))
+    B = int(r.integers(1, 3))
+    Hkv = int(r.choice([1, 2, 8]))
+    Hq = Hkv * int(r.choice([1, 4]))
+    N = int(r.choice([3001, 20000, 70000]))
+    k = int(r.choice([1, 50, 700, 4096, N + 5]))
+    W = int(r.choice([0, 3]))
+    skew = bool(r.random() < 0.3)
+    q, K, V, N, k, W, ranks, nw = _setup(cuda, G, skew, N=N, k=k, W=W, B=B, Hq=Hq, Hkv=Hkv, seed=100 + seed)
+    if r.random() < 0.3:  # duplicated rows across shard boundaries: ties resolved by the lower id
+        src = r.integers(0, N, size=4)
+        for b in range(B):
+            for h in range(Hkv):
+                K[b, h, r.integers(0, N, size=N // 5)] = K[b, h, r.choice(src)]
+        q, K, V, N, k, W, ranks, nw = _rebuild(cuda, G, q, K, V, N, k, W, B, Hq, Hkv)
+    qd = _dev(q, cuda)
+    out1, idx1, _ = topk_decode_attention(qd, _dev(K, cuda), _dev(V, cuda), [N] * B, k, n_win=[W] * B)
+    outs, res = _emulated_step(qd, ranks, nw)
+    torch.cuda.synchronize()
+    ref = idx1.cpu().numpy()
+    for (idx, sc), out in zip(res, outs):
+        a = idx.cpu().numpy()
+        for b in range(B):
+            for h in range(Hq):
+                assert set(a[b, h].tolist()) == set(ref[b, h].tolist()), (b, h)
+        assert float((out - out1).abs().max()) < 2e-5
+
+
+def _rebuild(cuda, G, q, K, V, N, k, W, B, Hq, Hkv):
+    """_setup's per-rank state for given arrays (after the data was modified)."""
+    from paper_2502_06766_b200 import CudaStages, DeviceShardedStep, LocalExchange, narrow_k, shard_range
+
+    kk = narrow_k(k, G)
+    exch = LocalExchange(G, B, Hq, k, kk, cuda)
+    ranks = []
+    for g in range(G):
+        lo, hi = shard_range(N, G, g)
+        ks = np.concatenate([K[:, :, lo:hi], K[:, :, N:N + W]], axis=2)
+        vs = np.concatenate([V[:, :, lo:hi], V[:, :, N:N + W]], axis=2)
+        st = CudaStages(B, Hq, Hkv, ks.shape[2], hi - lo, k, row_offset=lo, device=cuda)
+        nc = torch.tensor([hi - lo] * B, dtype=torch.int32, device=cuda)
+        ranks.append((DeviceShardedStep(st, exch, g, kk), _dev(ks, cuda), _dev(vs, cuda), nc))
+    nw = torch.tensor([W] * B, dtype=torch.int32, device=cuda)
+    return q, K, V, N, k, W, ranks, nw
