@@ -71,6 +71,9 @@ extern "C" {
                               workspace, so a host-I/O step needs no H2D copy of its inputs      */
 #define TKV_F_HEAD 32u     /* k-th + V gather by the per-head kernel (head_topk_kernel) at any k   */
 #define TKV_F_NO_HEAD 64u  /* never the per-head kernel (automatic: k <= 1024, one part)          */
+#define TKV_F_CLUSTER 4096u /* k-th + V gather + finish by one 4-CTA thread-block cluster per head  \
+                               (clus_topk_kernel; automatic at moderate k, one part)              */
+#define TKV_F_NO_CLUSTER 8192u /* never the cluster kernel                                      */
 #define TKV_F_SCAN_HMMA 8u /* key scan on register-staged mma.sync (scan.cu) instead of the TMA +  
                               tcgen05 pipeline (scan_tc.cu, the default)                         */
 

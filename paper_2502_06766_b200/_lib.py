@@ -59,6 +59,8 @@ F_GATHER_LIST = 16
 F_HEAD = 32
 F_NO_HEAD = 64
 F_HOST_Q = 128
+F_CLUSTER = 4096
+F_NO_CLUSTER = 8192
 
 
 class Problem(ctypes.Structure):

@@ -451,6 +451,17 @@ int run_emit(const tkv_problem* p, const void* q, const void* k_cache, const voi
 // per SM (~25 GB/s), half of what attend_cand's four CTAs per SM sustain. TKV_HEAD_TOPK=0/1
 // forces either (any k: the selected rows stream through a kHeadCap-row buffer); the
 // TKV_F_HEAD / TKV_F_NO_HEAD flags force it per call.
+// Moderate k: one 4-CTA cluster per head does the k-th selection, the V gather and the finish
+// (clus_topk_kernel) — no k-th → gather launch gap, no global tickets. TKV_CLUS=0/1 (TKV_DIAG
+// builds) forces either; TKV_F_CLUSTER / TKV_F_NO_CLUSTER per call.
+bool use_clus_topk(const tkv_problem* p) {
+  const int env = diag_env("TKV_CLUS", -1);
+  if (p->flags & TKV_F_CLUSTER) return true;
+  if ((p->flags & (TKV_F_GATHER_LIST | TKV_F_NO_CLUSTER | TKV_F_HEAD)) || env == 0) return false;
+  if (env > 0) return true;
+  return false;
+}
+
 bool use_head_topk(const tkv_problem* p, int gather) {
   const int env = diag_env("TKV_HEAD_TOPK", -1);
   if (p->flags & TKV_F_HEAD) return true;
@@ -462,7 +473,7 @@ bool use_head_topk(const tkv_problem* p, int gather) {
 
 int run_head(const tkv_problem* p, const void* q, const void* k_cache, const void* v_cache, const int32_t* n_ctx,
              const int32_t* n_win, int32_t* idx, float* scores, uint64_t* packed, float* out, int gather, void* ws,
-             const Layout& L, cudaStream_t st, ScanParams cp, SelectParams sl, int nbh, bool pdl) {
+             const Layout& L, cudaStream_t st, ScanParams cp, SelectParams sl, int nbh, bool pdl, bool clus = false) {
   HeadParams hp{};
   cp.seg_begin = 0;
   cp.seg_count = static_cast<int64_t>(p->batch) * p->n_kv_heads;
@@ -494,7 +505,10 @@ int run_head(const tkv_problem* p, const void* q, const void* k_cache, const voi
   if (C > 8) C = 8;
   if (C > L.nchunks) C = L.nchunks;
   hp.ctas_per_head = C < 1 ? 1 : C;
-  TKV_LAUNCH(launch_head_topk(hp, st));
+  if (clus)
+    TKV_LAUNCH(launch_clus_topk(hp, st));
+  else
+    TKV_LAUNCH(launch_head_topk(hp, st));
   if (p->flags & TKV_F_SORTED) {
     SortParams so{idx, scores, at<int32_t>(ws, L.mkb), p->k, 0, at<uint64_t>(ws, L.sortb)};
     TKV_SORT(so, nbh, st);
@@ -556,6 +570,9 @@ int run_layer_dev(const tkv_problem* p, const void* q, const void* k_cache, cons
       // between two kernels would hide the overlap anyway)
       TRY(run_scan_part(p, cp, 0, nseg, st, pdl_enabled() && !prof));
       if (prof) cudaEventRecord(g_scan_stop, st);
+      if (use_clus_topk(p))
+        return run_head(p, q, k_cache, v_cache, n_ctx, n_win, idx, scores, packed, out, gather, ws, L, st, cp, sl,
+                        static_cast<int>(nseg * G), pdl_enabled() && !prof, true);
       if (use_head_topk(p, gather))
         return run_head(p, q, k_cache, v_cache, n_ctx, n_win, idx, scores, packed, out, gather, ws, L, st, cp, sl,
                         static_cast<int>(nseg * G), pdl_enabled() && !prof);

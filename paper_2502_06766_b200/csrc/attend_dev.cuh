@@ -196,22 +196,25 @@ struct AttSmem {
 // ids and weights arrive as two broadcast 16-byte shared loads each instead of eight scalar
 // ones (ncu, cfg3: the per-row id load and its bounds test were 11 % of the kernel's
 // instructions) — and keeps their 8 rows in flight. Leaves sm.row / sm.w intact.
-template <class Gp = CtaGrp>
+template <class Gp = CtaGrp, int UNR = 8>
 __device__ void gather_acc(const AttendParams& p, int bh, int nrows, const AttSmem& sm, float (&acc)[8],
                            float& lw) {
+  static_assert(UNR % 4 == 0, "list entries come in 16-byte groups of four");
   const int b = bh / p.Hq, h = bh % p.Hq, kvh = h / p.G;
   const int tid = Gp::tid(), lane = tid & 31, warp = tid >> 5;
   const int half = lane >> 4, part = lane & 15;
   const __nv_bfloat16* vb =
       p.vc + (static_cast<int64_t>(b) * p.Hkv + kvh) * p.cache_rows * kD + part * 8;
-  constexpr int UNR = 8;
   for (int r0 = (warp * 2 + half) * UNR; r0 < nrows; r0 += 2 * NW * UNR) {
-    const int4 ra = *reinterpret_cast<const int4*>(&sm.row[r0]);
-    const int4 rb = *reinterpret_cast<const int4*>(&sm.row[r0 + 4]);
-    const float4 wa = *reinterpret_cast<const float4*>(&sm.w[r0]);
-    const float4 wb = *reinterpret_cast<const float4*>(&sm.w[r0 + 4]);
-    const int rr[UNR] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
-    const float ww[UNR] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+    int rr[UNR];
+    float ww[UNR];
+#pragma unroll
+    for (int g = 0; g < UNR / 4; ++g) {
+      const int4 ra = *reinterpret_cast<const int4*>(&sm.row[r0 + 4 * g]);
+      const float4 wa = *reinterpret_cast<const float4*>(&sm.w[r0 + 4 * g]);
+      rr[4 * g] = ra.x, rr[4 * g + 1] = ra.y, rr[4 * g + 2] = ra.z, rr[4 * g + 3] = ra.w;
+      ww[4 * g] = wa.x, ww[4 * g + 1] = wa.y, ww[4 * g + 2] = wa.z, ww[4 * g + 3] = wa.w;
+    }
     uint4 v[UNR];
     float w[UNR];
 #pragma unroll

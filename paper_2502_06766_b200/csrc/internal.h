@@ -303,6 +303,7 @@ cudaError_t launch_narrow_check(const uint64_t* gathered, int n_shards, int list
                                 int32_t* ok, cudaStream_t s);
 cudaError_t launch_kth(const SelectParams& p, cudaStream_t s);
 cudaError_t launch_head_topk(const HeadParams& p, cudaStream_t s);
+cudaError_t launch_clus_topk(const HeadParams& p, cudaStream_t s);
 cudaError_t launch_attend_cand(const AttendParams& p, cudaStream_t s);
 cudaError_t launch_attend_list(const AttendParams& p, cudaStream_t s);
 cudaError_t launch_sort(const SortParams& p, int nbh, cudaStream_t s, int* launches);

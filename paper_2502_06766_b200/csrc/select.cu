@@ -918,6 +918,367 @@ cudaError_t launch_head_topk(const HeadParams& p, cudaStream_t s) {
                     q);
 }
 
+// ---------------------------------------------------------------- k-th + gather + finish per cluster
+// clus_topk_kernel: grid (kKthCtas, heads), one kKthCtas-CTA thread-block cluster per head,
+// 256 threads per CTA (NT). Replaces kth_kernel + attend_cand_kernel (or head_topk_kernel) at
+// moderate k, where the post-scan chain (k-th kernel, a launch gap, a gather kernel that
+// re-derives its work split and finishes heads through global tickets) is latency-bound:
+//   1. every CTA loads its 1/kKthCtas slice of the head's candidates into registers while it
+//      reads the scan's histogram and finds the bucket d* of the kb-th largest;
+//   2. slice scan: maximum + members of d* into shared memory; one cluster barrier;
+//   3. every CTA pulls the other CTAs' members and maxima through distributed shared memory and
+//      derives the same exact T itself (rank counting over 64-bit composites: lower-id ties,
+//      ann.py:162-166) — no second barrier, no global hand-off;
+//   4. the selected rows of its slice (c >= T; still in registers) are compacted into shared
+//      memory, the output reservation atomic issued, their V rows gathered (16 lanes per
+//      256-byte row, 8 rows in flight per half-warp) and weighted against the head max
+//      (attention.py:158-167), ids / raw scores written;
+//   5. the (l, o[128]) partial of each CTA goes to its shared memory; cluster rank 0 sums the
+//      four in rank order (deterministic) over DSMEM and finishes the head: unselected pinned
+//      rows, the window, normalisation (attention.py:107-122, 152-154).
+// The CTAs fit beside a tcgen05 scan CTA (33 KB of shared memory, <= 85 registers), so under
+// programmatic dependent launch they are resident before the scan ends. A head whose sampled
+// threshold let fewer than kb rows through takes head_topk_kernel's exactness fallback.
+#ifndef TKV_CLUS_PAD
+#define TKV_CLUS_PAD 0  // experiments: extra dynamic shared memory (CTAs per SM)
+#endif
+constexpr int kClusSmem = kHistBins * 4 + kKthSmemBucket * 8 + kCandChunk * 4 + TKV_CLUS_PAD;  // + raw scores of a batch
+static_assert(sizeof(AttSmem) <= kHistBins * 4, "AttSmem aliases the histogram");
+static_assert(kCandChunk == NT * 4, "one compaction batch = the registers of one slice batch");
+#ifndef TKV_CLUS_CL
+#define TKV_CLUS_CL 4  // CTAs per head (cluster size)
+#endif
+#ifndef TKV_CLUS_MINB
+#define TKV_CLUS_MINB 3  // <= 85 registers: a CTA fits beside a tcgen05 scan CTA
+#endif
+#ifndef TKV_CLUS_GU
+#define TKV_CLUS_GU 8  // V rows in flight per half-warp in the cluster kernel's gather
+#endif
+
+__global__ void __cluster_dims__(TKV_CLUS_CL, 1, 1) __launch_bounds__(NT, TKV_CLUS_MINB) clus_topk_kernel(HeadParams hp) {
+  constexpr int CL = TKV_CLUS_CL, UNR = kCandChunk / NT;
+  const SelectParams& p = hp.s;
+  const AttendParams& a = hp.a;
+  extern __shared__ __align__(16) uint8_t s_dyn[];
+  uint32_t* s_hist = reinterpret_cast<uint32_t*>(s_dyn);                 // before T
+  AttSmem& sm = *reinterpret_cast<AttSmem*>(s_dyn);                      // after T (aliases s_hist)
+  uint64_t* s_bkt = reinterpret_cast<uint64_t*>(s_dyn + kHistBins * 4);  // read by peers until the last barrier
+  float* s_sc = reinterpret_cast<float*>(s_dyn + kHistBins * 4 + kKthSmemBucket * 8);  // a batch's raw scores
+  __shared__ uint32_t s_scr[32], s_out[2], s_nb;
+  __shared__ uint64_t s_rmax[NW], s_vmax, s_res;
+  __shared__ __align__(16) float s_part[kD + 4];
+
+  pdl_wait();  // candidates and histograms of the scan
+  if (threadIdx.x == 0) tl_start(p.tl, 5);
+#ifdef TKV_DIAG
+  if (threadIdx.x == 0) tl_smid(p.tl, 249);  // SMs hosting a cluster CTA
+  uint64_t t_ph = p.tl ? ptimer() : 0ull;
+#define TKV_CL_PHASE(e) \
+  if (threadIdx.x == 0) tl_phase(p.tl, e, t_ph)
+#else
+#define TKV_CL_PHASE(e)
+#endif
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = static_cast<int>(cluster.block_rank());
+  const int bh = p.bh_begin + static_cast<int>(blockIdx.y);
+  const int b = bh / p.Hq, h = bh % p.Hq;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t* src = p.src + static_cast<int64_t>(bh) * p.src_stride;
+  int64_t n = p.hs.cand_cnt[bh];
+  if (n > p.src_stride) n = p.src_stride;
+  const int64_t N = p.n_ctx[b];
+  const int64_t kb = N < p.k ? N : p.k;
+
+  if (n < kb) {  // cluster-uniform: the whole cluster leaves without a barrier
+    if (rank == 0) {
+      uint32_t* gh = p.hs.hist + static_cast<int64_t>(bh) * kHistBins;
+      for (int i = tid; i < kHistBins; i += NT) gh[i] = 0u;
+      if (tid == 0) {
+        p.hs.flag_fail[bh] = 1u;
+        atomicAdd(p.hs.fb_heads, 1u);
+        p.hs.group_fail[b * p.Hkv + h / p.G] = 1u;
+        p.hs.cand_cnt[bh] = 0u;
+        p.hs.thr[bh] = 0u;
+        p.hs.hshift[bh] = kNoFilterShift;
+        __threadfence();
+#ifndef TKV_NO_CDP
+        // exact chain over ALL heads (the good heads are rewritten identically up to fp32
+        // summation order; the fallback k-th pass resets every head's output counter)
+        if (atomicExch(p.hs.fb_launched, 1u) == 0u) {
+          fb_scan_kernel<<<p.fb_scan_grid, kScanWarps * 32, p.fb_scan_smem, cudaStreamTailLaunch>>>(p.fb_scan);
+          SelectParams f = p;
+          f.pass = kPassFallback;
+          f.pdl = 0;
+          const int nbh = p.bh_count ? p.bh_count : p.B * p.Hq;
+          kth_kernel<<<dim3(kKthCtas, nbh), kKthThreads, kKthSmem, cudaStreamTailLaunch>>>(f);
+          attend_cand_fb_kernel<<<hp.att_grid, NT, (nbh + 1) * sizeof(uint32_t), cudaStreamTailLaunch>>>(a);
+        }
+#endif
+      }
+    }
+    return;
+  }
+
+  TKV_CL_PHASE(67);
+  // ---- 1. slice registers + histogram bucket
+  const int64_t lo = n * rank / CL, hi = n * (rank + 1) / CL;
+  uint64_t cv0[UNR];
+#pragma unroll
+  for (int u = 0; u < UNR; ++u) {
+    const int64_t i = lo + u * NT + tid;
+    cv0[u] = i < hi ? src[i] : 0ull;
+  }
+  const uint32_t thr = p.hs.thr[bh], shift = p.hs.hshift[bh];
+  const bool all = kb >= n;  // includes kb == 0 (then n == 0)
+  uint32_t dstar = 0, need = 0, bcnt = 0;
+  bool whole = true;
+  if (!all) {
+    copy_g2s_u32<NT, kHistBins>(s_hist, p.hs.hist + static_cast<int64_t>(bh) * kHistBins, kHistBins);
+    __syncthreads();
+    find_bucket<NT, kHistBins>(s_hist, static_cast<uint32_t>(kb), s_out, s_scr);
+    dstar = s_out[0];
+    need = static_cast<uint32_t>(kb) - s_out[1];
+    bcnt = s_hist[dstar];
+    whole = bcnt == need;
+  }
+  const bool refine = !all && !whole;
+  bool big = refine && bcnt > static_cast<uint32_t>(kKthSmemBucket);
+  TKV_CL_PHASE(68);
+
+  // ---- 2. slice scan: maximum + members of bucket d*
+  if (tid == 0) s_nb = 0u;
+  __syncthreads();
+  uint64_t vmax = 0ull;
+  for (int64_t start = lo; start < hi; start += kCandChunk) {
+    uint64_t cv[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int64_t i = start + u * NT + tid;
+      cv[u] = start == lo ? cv0[u] : (i < hi ? src[i] : 0ull);
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const uint64_t cc = cv[u];
+      vmax = cc > vmax ? cc : vmax;
+      const bool inb = refine && !big && cc != 0ull && hist_digit(comp_key(cc), thr, shift) == dstar;
+      const unsigned bb = __ballot_sync(kFull, inb);
+      if (bb) {
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(&s_nb, __popc(bb));
+        base = __shfl_sync(kFull, base, 0);
+        const uint32_t pos = base + __popc(bb & lanemask_lt());
+        if (inb && pos < static_cast<uint32_t>(kKthSmemBucket)) s_bkt[pos] = cc;
+      }
+    }
+  }
+  vmax = warp_max_u64(vmax);
+  if (lane == 0) s_rmax[warp] = vmax;
+  __syncthreads();
+  if (tid == 0) {
+    uint64_t m = 0ull;
+    for (int w = 0; w < NW; ++w) m = s_rmax[w] > m ? s_rmax[w] : m;
+    s_vmax = m;
+  }
+  TKV_CL_PHASE(69);
+  cluster.sync();  // every CTA's s_nb / s_bkt / s_vmax final
+  TKV_CL_PHASE(70);
+
+  // ---- 3. every CTA: the other CTAs' members appended behind its own (peers read only
+  // [0, their own count) of this buffer), the head maximum, and the exact T
+  const uint32_t own = s_nb;
+  uint32_t nb = own;
+  vmax = s_vmax;
+  for (int r = 0; r < CL; ++r) {
+    if (r == rank) continue;
+    const uint32_t nr = *cluster.map_shared_rank(&s_nb, r);
+    const uint64_t mr = *cluster.map_shared_rank(&s_vmax, r);
+    vmax = mr > vmax ? mr : vmax;
+    if (refine && !big && nb + nr <= static_cast<uint32_t>(kKthSmemBucket)) {
+      const uint64_t* rb = cluster.map_shared_rank(s_bkt, r);
+      for (uint32_t i = tid; i < nr; i += NT) s_bkt[nb + i] = rb[i];
+    }
+    nb += nr;
+  }
+  if (nb > static_cast<uint32_t>(kKthSmemBucket) || own > static_cast<uint32_t>(kKthSmemBucket))
+    big = refine;  // histogram / list mismatch guard
+  __syncthreads();
+  uint64_t T;
+  if (all) {
+    T = 1ull;  // every valid (non-zero) candidate
+  } else if (whole) {
+    T = static_cast<uint64_t>(thr + (dstar << shift)) << 32;  // lower bound of bucket d*
+  } else if (!big) {
+    T = block_rank_select_par<NT>(s_bkt, static_cast<int>(nb), static_cast<int>(need), &s_res);
+  } else {
+    int cs = 64;
+    uint64_t cp = 0;
+    auto ld = [&](int64_t i, uint64_t& cc) {
+      cc = __ldcg(&src[i]);
+      return cc != 0ull && hist_digit(comp_key(cc), thr, shift) == dstar;
+    };
+    radix_select_u64<NT>(ld, n, need, s_hist, s_scr, s_out, cs, cp);
+    T = cp << cs;
+  }
+  if (tid == 0) tl_end(p.tl, 7);
+  TKV_CL_PHASE(71);
+  const float zs = a.scale * kLog2e;
+  const float mscore = key_score(comp_key(vmax));
+  const float zref = kb > 0 ? mscore * zs : 0.f;
+  int32_t* idx_o = a.idx_out + static_cast<int64_t>(bh) * p.k;
+  float* sc_o = a.scores_out + static_cast<int64_t>(bh) * p.k;
+  uint64_t* pk_o = a.packed_out ? a.packed_out + static_cast<int64_t>(bh) * p.k : nullptr;
+  if (rank == 0) {
+    if (tid == 0) {
+      p.meta_kth[bh] = kb > 0 ? T : ~0ull;
+      p.meta_kb[bh] = static_cast<int32_t>(kb);
+      p.meta_max[bh] = kb > 0 ? mscore : -INFINITY;
+    }
+    for (int i = static_cast<int>(kb) + tid; i < p.k; i += NT) {  // pads (attention.py:147-149)
+      idx_o[i] = -1;
+      sc_o[i] = -INFINITY;
+      if (pk_o) pk_o[i] = 0ull;
+    }
+  }
+
+  // ---- 4. this slice's selected rows: compaction, reservation, V gather, ids / scores
+  float acc[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+  float lw = 0.f;
+  for (int64_t start = lo; start < hi && kb > 0; start += kCandChunk) {
+    uint64_t cv[UNR];
+    bool sel[UNR];
+    uint32_t mine = 0;
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int64_t i = start + u * NT + tid;
+      cv[u] = start == lo ? cv0[u] : (i < hi ? src[i] : 0ull);
+      sel[u] = cv[u] != 0ull && cv[u] >= T;
+      mine += sel[u] ? 1u : 0u;
+    }
+    uint32_t incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += t;
+    }
+    __syncthreads();  // the previous batch's gather no longer reads sm.row / sm.w (and s_hist is dead)
+    if (lane == 31) sm.wcnt[warp] = incl;
+    __syncthreads();
+    uint32_t woff = 0, m = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      woff += w < warp ? sm.wcnt[w] : 0u;
+      m += sm.wcnt[w];
+    }
+    if (tid == 0) sm.base = m ? atomicAdd(&a.out_cnt[bh], m) : 0u;
+    uint32_t pos = woff + incl - mine;
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      if (sel[u]) {
+        const int64_t local = static_cast<int64_t>(comp_gid(cv[u])) - a.row_offset;
+        mark_pinned(a, bh, local);
+        const float sc = key_score(comp_key(cv[u]));
+        sm.row[pos] = static_cast<int32_t>(local);
+        sm.w[pos] = exp2f(fmaf(sc, zs, -zref));
+        s_sc[pos] = sc;
+        ++pos;
+      }
+    }
+    __syncthreads();
+    // (the candidates leave registers here: nothing but the V rows is live across the gather,
+    // so every row load of a round is issued before the first use)
+    if (a.gather) gather_acc<CtaGrp, TKV_CLUS_GU>(a, bh, static_cast<int>(m), sm, acc, lw);
+    const uint32_t obase = sm.base;
+    for (uint32_t i = tid; i < m; i += NT) {  // ids / raw scores (order unspecified)
+      const uint32_t o = obase + i;
+      if (o < static_cast<uint32_t>(kb)) {
+        const uint32_t gid = static_cast<uint32_t>(static_cast<int64_t>(sm.row[i]) + a.row_offset);
+        idx_o[o] = static_cast<int32_t>(gid);
+        sc_o[o] = s_sc[i];
+        if (pk_o) pk_o[o] = make_comp(score_key(s_sc[i]), gid);  // the composite, rebuilt exactly
+      }
+    }
+  }
+
+  TKV_CL_PHASE(72);
+  // ---- 5. partials: (l, o) of this CTA into shared memory; rank 0 sums them and finishes
+  if (a.gather) {
+    const int half = lane >> 4, part = lane & 15;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] += __shfl_xor_sync(kFull, acc[j], 16);
+    __syncthreads();  // sm.row / sm.w readers done
+    if (half == 0) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) sm.red[warp][part * 8 + j] = acc[j];
+    }
+    lw = warp_sum(lw);
+    if (lane == 0) sm.l[warp] = lw;
+    __syncthreads();
+    if (tid < kD) {
+      float o = 0.f;
+#pragma unroll
+      for (int w2 = 0; w2 < NW; ++w2) o += sm.red[w2][tid];
+      s_part[1 + tid] = o;
+    }
+    if (tid == 0) {
+      float l = 0.f;
+#pragma unroll
+      for (int w2 = 0; w2 < NW; ++w2) l += sm.l[w2];
+      s_part[0] = l;
+    }
+  }
+  __threadfence();  // pinned-prefix marks before the finishing CTA reads them
+  cluster.sync();   // partials final; every peer read of s_bkt done
+  float o_c = 0.f, l_c = 0.f;
+  if (a.gather && rank == 0) {
+    for (int r = 0; r < CL; ++r) {  // rank order: deterministic
+      const float* pr = cluster.map_shared_rank(s_part, r);
+      if (tid < kD) o_c += pr[1 + tid];
+      l_c += pr[0];
+    }
+  }
+  cluster.sync();  // rank 0's reads done: the other CTAs may exit
+  TKV_CL_PHASE(73);
+  if (!a.gather || rank != 0) {
+    if (tid == 0) tl_end(p.tl, 5);
+    return;
+  }
+  const int kvh = h / p.G;
+  const int64_t nctx = a.n_ctx[b];
+  __syncthreads();
+  add_pinned(a, b, h, kvh, nctx, static_cast<int>(kb), zref, l_c, o_c, sm.z, sm.scr, &sm.red[0][0]);
+  if (a.partial_only) {
+    sm.o[tid] = o_c;
+    __syncthreads();
+    float* dst = a.partial_out + static_cast<int64_t>(bh) * (kD + 1);
+    if (tid == 0) dst[0] = l_c;
+    if (tid < kD) dst[1 + tid] = sm.o[tid] + sm.o[tid + kD];
+  } else {
+    finalize_head(a, b, h, kvh, nctx, zref, l_c, o_c, sm.z, sm.scr, sm.o, &sm.red[0][0]);
+  }
+  TKV_CL_PHASE(74);
+  if (tid == 0) tl_end(p.tl, 5);
+#undef TKV_CL_PHASE
+}
+
+cudaError_t launch_clus_topk(const HeadParams& p, cudaStream_t s) {
+  prepare_fallback_kernels();
+  const int att_grid = per_device(reinterpret_cast<const void*>(clus_topk_kernel), 0, [] {
+    int per = 0;
+#ifndef TKV_NO_CDP
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, attend_cand_fb_kernel, NT, 8192);
+#endif
+    cudaFuncSetAttribute(clus_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kClusSmem);
+    const int g = device_sm_count() * (per > 0 ? per : 1);
+    return g < kMaxGatherGrid ? g : kMaxGatherGrid;
+  });
+  HeadParams q = p;
+  q.att_grid = att_grid;
+  const int nbh = p.s.bh_count ? p.s.bh_count : p.s.B * p.s.Hq;
+  return launch_pdl(clus_topk_kernel, dim3(TKV_CLUS_CL, nbh), dim3(NT), kClusSmem, s, p.s.pdl != 0, q);
+}
+
 // ---------------------------------------------------------------- optional sorted output
 // Bitonic sort (descending composite = score desc, id asc: TopKResult order, ann.py:166)
 // of the kb selected rows in shared memory.

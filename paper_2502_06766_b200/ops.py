@@ -45,7 +45,7 @@ def make_problem(B: int, Hq: int, Hkv: int, cache_rows: int, max_ctx: int, k: in
                  sorted: bool = False, no_filter: bool = False, row_offset: int = 0,
                  head_dim: int = HEAD_DIM,
                  tc_scan: bool | None = None, parts: int = 0, list_gather: bool = False,
-                 head: bool | None = None, host_q: bool = False) -> _lib.Problem:
+                 head: bool | str | None = None, host_q: bool = False) -> _lib.Problem:
     p = _lib.Problem()
     p.batch, p.n_q_heads, p.n_kv_heads, p.head_dim = B, Hq, Hkv, head_dim
     p.cache_rows, p.max_ctx, p.k = cache_rows, max_ctx, k
@@ -62,8 +62,12 @@ def make_problem(B: int, Hq: int, Hkv: int, cache_rows: int, max_ctx: int, k: in
     p.flags |= parts << _lib.F_PARTS_SHIFT
     if list_gather:
         p.flags |= _lib.F_GATHER_LIST
-    if head is not None:  # per-head k-th + gather kernel forced on / off (None: automatic, k <= 1024)
-        p.flags |= _lib.F_HEAD if head else _lib.F_NO_HEAD
+    # k-th + gather kernel: True = per-head CTAs (head_topk_kernel), "cluster" = one 4-CTA cluster
+    # per head (clus_topk_kernel), False = k-th kernel + candidate gather; None: automatic
+    if head == "cluster":
+        p.flags |= _lib.F_CLUSTER
+    elif head is not None:
+        p.flags |= (_lib.F_HEAD | _lib.F_NO_CLUSTER) if head else (_lib.F_NO_HEAD | _lib.F_NO_CLUSTER)
     if host_q:  # q in pinned host memory, staged on device inside the call
         p.flags |= _lib.F_HOST_Q
     p.row_offset = row_offset
@@ -170,7 +174,7 @@ def topk_decode_attention(q, k_cache, v_cache, n_ctx, k: int, *, n_win=None, sca
                           max_ctx: int | None = None, no_filter: bool = False, row_offset: int = 0,
                           out=None, idx=None, scores=None, workspace: Workspace | None = None,
                           tc_scan: bool | None = None, parts: int = 0,
-                          list_gather: bool = False, head: bool | None = None):
+                          list_gather: bool = False, head: bool | str | None = None):
     """Exact top-k decode attention for every (batch, q head) of one layer.
 
     q [B, Hq, 128] bf16; k_cache/v_cache [B, Hkv, rows, 128] bf16 with the context in rows
@@ -205,7 +209,7 @@ def topk_decode_step(q, k_new, v_new, k_cache, v_cache, n_ctx, n_win, k: int, *,
                      combine: str = "joint", pinned_prefix: int = 0, sorted: bool = False,
                      max_ctx: int | None = None, out=None, idx=None, scores=None,
                      workspace: Workspace | None = None, tc_scan: bool | None = None,
-                     parts: int = 0, list_gather: bool = False, head: bool | None = None):
+                     parts: int = 0, list_gather: bool = False, head: bool | str | None = None):
     """One decode step of one layer (decode_step, attention.py:203-230): append this token's
     k_new/v_new [B, Hkv, 128] to the window (GenWindow.append, attention.py:210; n_win is a
     device int32 counter advanced in place) and attend over context + window, in one call."""
@@ -237,7 +241,7 @@ def topk_decode_step(q, k_new, v_new, k_cache, v_cache, n_ctx, n_win, k: int, *,
 
 def topk_search(q, k_cache, n_ctx, k: int, *, sorted: bool = True, max_ctx: int | None = None,
                 no_filter: bool = False, row_offset: int = 0, workspace: Workspace | None = None,
-                tc_scan: bool | None = None, parts: int = 0, head: bool | None = None):
+                tc_scan: bool | None = None, parts: int = 0, head: bool | str | None = None):
     """Exact top-k rows per (batch, q head) without attention (knn_search flat, ann.py:203-218).
 
     Returns (idx [B, Hq, k] int32, scores [B, Hq, k] f32), TopKResult-ordered when sorted.

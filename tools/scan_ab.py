@@ -13,6 +13,11 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--scan", choices=["tc", "hmma"], default="tc")
     ap.add_argument("--label", default="")
+    ap.add_argument("--no-filter", action="store_true", help="no sampled threshold: every score is a candidate")
+    ap.add_argument("--n", type=int, default=0, help="override the context length")
+    ap.add_argument("--k", type=int, default=0, help="override k")
+    ap.add_argument("--head", default="auto", choices=["auto", "cluster", "head", "kth"],
+                    help="k-th + gather kernels: automatic, cluster, per-head CTAs, k-th + candidate gather")
     args = ap.parse_args()
     args.tc = args.scan == "tc"
     import torch
@@ -21,7 +26,11 @@ def main():
     import paper_2502_06766_b200 as tkv
     from paper_2502_06766_b200 import _lib
 
-    cfg = bench.CONFIGS[args.config]
+    cfg = dict(bench.CONFIGS[args.config])
+    if args.n:
+        cfg["N"] = args.n
+    if args.k:
+        cfg["k"] = args.k
     dev = torch.device("cuda", 0)
     q, K, V, n = bench.make_inputs(cfg, cfg["N"] + 8, 0, dev)
     B, k = cfg["B"], cfg["k"]
@@ -29,9 +38,12 @@ def main():
     out = torch.empty((B, 32, 128), dtype=torch.float32, device=dev)
     idx = torch.empty((B, 32, k), dtype=torch.int32, device=dev)
     sc = torch.empty((B, 32, k), dtype=torch.float32, device=dev)
-    prob = tkv.ops.make_problem(B, 32, 8, K.shape[2], n, k, tc_scan=args.tc)
+    head = {"auto": None, "cluster": "cluster", "head": True, "kth": False}[args.head]
+    prob = tkv.ops.make_problem(B, 32, 8, K.shape[2], n, k, tc_scan=args.tc, head=head,
+                                no_filter=args.no_filter)
     ws = tkv.Workspace(prob, dev)
-    kw = dict(max_ctx=n, out=out, idx=idx, scores=sc, workspace=ws, tc_scan=args.tc)
+    kw = dict(max_ctx=n, out=out, idx=idx, scores=sc, workspace=ws, tc_scan=args.tc, head=head,
+              no_filter=args.no_filter)
     for _ in range(5):
         tkv.topk_decode_attention(q, K, V, nc, k, **kw)
     torch.cuda.synchronize()
@@ -73,7 +85,7 @@ def main():
     lib.tkv_profile_scan_events(None, None)
     scan = sum(a.elapsed_time(b) for a, b in ev) / args.steps * 1e3
     kbytes = B * 8 * n * 128 * 2
-    print(f"{args.config} tc={int(args.tc)} {args.label}: step {step:.1f} us (graph replay {step_graph:.1f} us), scan {scan:.1f} us "
+    print(f"{args.config} N={n} k={k} tc={int(args.tc)} head={args.head} nf={int(args.no_filter)} {args.label}: step {step:.1f} us (graph replay {step_graph:.1f} us), scan {scan:.1f} us "
           f"({kbytes / scan / 1e3:.0f} GB/s)", flush=True)
 
 

@@ -30,7 +30,10 @@ EXTRA_PHASES = {42: "scan epilogue: wait for a unit's scores", 43: "scan epilogu
                 60: "gather CTA: start→item prefix", 61: "gather: →batch candidates loaded",
                 62: "gather: →compaction (2 barriers)", 63: "gather: →V rows accumulated",
                 64: "gather: →ids written (per item)", 65: "gather: →partial written",
-                66: "gather: →ticket / head finish"}
+                66: "gather: →ticket / head finish",
+                67: "cluster CTA: past wait→params", 68: "→hist + bucket", 69: "→slice scan + max",
+                70: "→cluster barrier 1", 71: "→peer members + T", 72: "→compaction + V gather",
+                73: "→partials + 2 cluster barriers", 74: "→finish (rank 0)"}
 
 
 def main():
@@ -117,6 +120,9 @@ def main():
     if scan_sms:
         print(f"  SMs: scan CTAs on {len(scan_sms)}, threshold CTAs on {len(thr_sms)}, scan CTAs starting "
               f">6 us late on {len(late_sms)} (of which {len(late_sms & thr_sms)} host a threshold CTA)")
+    clus_sms = sms(249)
+    if clus_sms:
+        print(f"  SMs hosting a cluster k-th + gather CTA: {len(clus_sms)}")
     for e, nm in enumerate(NAMES):
         print(f"  {nm:26s} start {acc[e, 0]:8.1f}  end {acc[e, 1]:8.1f} us")
     for j, nm in enumerate(PHASES):
