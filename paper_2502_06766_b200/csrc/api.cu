@@ -54,7 +54,7 @@ int fail(int code, const char* fmt, ...) {
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct Layout {
-  size_t ticket_g, ticket_k, flag, gflag, fbl, fbh, mout, ctrl_end;
+  size_t ticket_g, ticket_k, flag, gflag, fbl, fbh, mout, steal, ctrl_end;
   size_t maxc, bktc, bkt, outc;
   size_t cnt, thr, hshift, hist, mmax, mkth, mkb, mt2, samp, cand, sidx, sscore, pl, po, pinm, qs, sortb, total;
   int pin_words;
@@ -79,6 +79,7 @@ Layout make_layout(const tkv_problem* p) {
   L.fbl = take(4 * kMaxParts);
   L.fbh = take(4);
   L.mout = take(BH * 4);  // sharded merge output counters (self-resetting)
+  L.steal = take(2 * 4 * kMaxParts);  // tcgen05 scan work pool, one counter pair per part (self-resetting)
   L.ctrl_end = off;
   L.cnt = take(BH * 4);
   L.thr = take(BH * 4);
@@ -251,6 +252,7 @@ int run_prefix(const tkv_problem* p, const void* q, const void* k_cache, const i
   cp.tl = g_tl;
   cp.seg_begin = 0;
   cp.seg_count = static_cast<int64_t>(p->batch) * p->n_kv_heads;
+  cp.steal = at<uint32_t>(ws, L.steal);
 
   SelectParams sl{};
   sl.src = cp.cand;
@@ -285,7 +287,12 @@ bool use_tc_scan(const tkv_problem* p, const ScanParams& cp) {
 }
 
 // key scan of segments [s0, s1) on stream `st`
-int run_scan_part(const tkv_problem* p, ScanParams cp, int64_t s0, int64_t s1, cudaStream_t st, bool pdl) {
+int run_scan_part(const tkv_problem* p, ScanParams cp, int64_t s0, int64_t s1, cudaStream_t st, bool pdl,
+                  int part = 0, bool steal = true) {
+  // the dynamic tail only where nothing absorbs the CTAs' uneven ends: in the chained parts
+  // pipeline the next part's CTAs take over SMs as they free up (cfg5: 1448 us static, 1475-1490
+  // with every part balanced), so only the last part balances
+  cp.steal = steal ? cp.steal + 2 * part : nullptr;  // overlapping part scans each own a counter pair
   cp.seg_begin = s0;
   cp.seg_count = s1 - s0;
   cp.pdl = pdl ? 1 : 0;
@@ -303,7 +310,7 @@ int run_scan_part(const tkv_problem* p, ScanParams cp, int64_t s0, int64_t s1, c
 // k-th of failing heads, tail-launched on device); the selected set of a head is
 // { candidates c : c >= meta_kth }, materialised by run_emit
 int run_kth_part(const tkv_problem* p, ScanParams cp, SelectParams sl, int64_t s0, int64_t s1, int part,
-                 cudaStream_t st, bool pdl) {
+                 cudaStream_t st, bool pdl, SelectParams* launched = nullptr) {
   const int G = p->n_q_heads / p->n_kv_heads;
   cp.seg_begin = s0;
   cp.seg_count = s1 - s0;
@@ -316,6 +323,7 @@ int run_kth_part(const tkv_problem* p, ScanParams cp, SelectParams sl, int64_t s
   sl.fb_scan = cp;
   scan_launch_shape(cp, &sl.fb_scan_grid, &sl.fb_scan_smem);
   TKV_LAUNCH(launch_kth(sl, st));
+  if (launched) *launched = sl;
   return TKV_OK;
 }
 
@@ -406,12 +414,22 @@ AttendParams make_attend(const tkv_problem* p, const void* q, const void* k_cach
   return a;
 }
 
+// Gather structure: one fused filter + gather pass over the candidates, or (many selected
+// rows) a filter pass writing idx/scores followed by a streaming gather over those lists —
+// measured faster from ~1M selected rows per step (cfg5 family), slower below (cfg1-3).
+// TKV_LIST_GATHER=0/1 forces either.
+bool list_gather_used(const tkv_problem* p, int bh_count, int gather) {
+  const int list_env = diag_env("TKV_LIST_GATHER", -1);
+  const double sel_rows = static_cast<double>(bh_count) * p->k;
+  return gather && ((p->flags & TKV_F_GATHER_LIST) ? true : (list_env >= 0 ? list_env != 0 : sel_rows >= 1.0e6));
+}
+
 // Materialise the selected rows (idx/scores[/packed]) from the candidates, with the V
 // gather + softmax fused when gather != 0; then the optional TopKResult-order sort.
 int run_emit(const tkv_problem* p, const void* q, const void* k_cache, const void* v_cache,
              const int32_t* n_ctx, const int32_t* n_win, int32_t* idx, float* scores,
              uint64_t* packed, float* out, int gather, void* ws, const Layout& L, cudaStream_t st,
-             int bh_begin, int bh_count) {
+             int bh_begin, int bh_count, const SelectParams* deferred = nullptr) {
   AttendParams a = make_attend(p, q, k_cache, v_cache, n_ctx, n_win, idx, scores, ws, L);
   a.bh_begin = bh_begin;
   a.bh_count = bh_count;
@@ -421,19 +439,17 @@ int run_emit(const tkv_problem* p, const void* q, const void* k_cache, const voi
   a.out = out;
   a.gather = gather;
   a.partial_only = 0;
-  // Gather structure: one fused filter + gather pass over the candidates, or (many selected
-  // rows) a filter pass writing idx/scores followed by a streaming gather over those lists —
-  // measured faster from ~1M selected rows per step (cfg5 family), slower below (cfg1-3).
-  // TKV_LIST_GATHER=0/1 forces either.
-  const int list_env = diag_env("TKV_LIST_GATHER", -1);
-  const double sel_rows = static_cast<double>(bh_count) * p->k;
-  const bool list_gather =
-      (p->flags & TKV_F_GATHER_LIST) ? true : (list_env >= 0 ? list_env != 0 : sel_rows >= 1.0e6);
+  const bool list_gather = list_gather_used(p, bh_count, gather);
   if (gather && list_gather) {
     a.gather = 0;  // filter only: idx / scores
     TKV_LAUNCH(launch_attend_cand(a, st));
     a.gather = 1;
     TKV_LAUNCH(launch_attend_list(a, st));
+  } else if (deferred) {  // PDL behind the k-th kernel, which left the fallback launch to it
+    HeadParams hp{};
+    hp.s = *deferred;
+    hp.a = a;
+    TKV_LAUNCH(launch_attend_cand_pdl(hp, st));
   } else {
     TKV_LAUNCH(launch_attend_cand(a, st));
   }
@@ -454,12 +470,17 @@ int run_emit(const tkv_problem* p, const void* q, const void* k_cache, const voi
 // Moderate k: one 4-CTA cluster per head does the k-th selection, the V gather and the finish
 // (clus_topk_kernel) — no k-th → gather launch gap, no global tickets. TKV_CLUS=0/1 (TKV_DIAG
 // builds) forces either; TKV_F_CLUSTER / TKV_F_NO_CLUSTER per call.
+// Automatic: few heads (one wave of 4-CTA clusters over the SMs) and moderate k (a CTA gathers
+// <= k/4 rows: at cfg3's k = 16384 the candidate gather's four CTAs per SM keep more rows in
+// flight — 361 vs 391 us). Measured: cfg1 (32 heads, k = 256) 38.3 -> 34.1 us, cfg2 (k = 2048)
+// 76.1 -> 74.1 us.
 bool use_clus_topk(const tkv_problem* p) {
   const int env = diag_env("TKV_CLUS", -1);
   if (p->flags & TKV_F_CLUSTER) return true;
   if ((p->flags & (TKV_F_GATHER_LIST | TKV_F_NO_CLUSTER | TKV_F_HEAD)) || env == 0) return false;
   if (env > 0) return true;
-  return false;
+  const int nbh = p->batch * p->n_q_heads;
+  return p->k <= 4096 && nbh * 4 <= device_sm_count();
 }
 
 bool use_head_topk(const tkv_problem* p, int gather) {
@@ -576,9 +597,17 @@ int run_layer_dev(const tkv_problem* p, const void* q, const void* k_cache, cons
       if (use_head_topk(p, gather))
         return run_head(p, q, k_cache, v_cache, n_ctx, n_win, idx, scores, packed, out, gather, ws, L, st, cp, sl,
                         static_cast<int>(nseg * G), pdl_enabled() && !prof);
-      TRY(run_kth_part(p, cp, sl, 0, nseg, 0, st, pdl_enabled() && !prof));
+      // TKV_GATHER_PDL=1 (TKV_DIAG builds, experiment): the gather PDL-launched behind the k-th
+      // kernel, which then leaves the exactness fallback launch to the gather. Measured slower
+      // (cfg2 78.2 vs 75.8 us, cfg3 363.5 vs 360.7) and it hung one adversarial fuzz case, so off
+      const bool pdl = pdl_enabled() && !prof;
+      const bool defer = pdl && !list_gather_used(p, static_cast<int>(nseg * G), gather) &&
+                         diag_env("TKV_GATHER_PDL", 0) != 0;
+      SelectParams launched{};
+      if (defer) sl.defer_fb = 1;
+      TRY(run_kth_part(p, cp, sl, 0, nseg, 0, st, pdl, &launched));
       return run_emit(p, q, k_cache, v_cache, n_ctx, n_win, idx, scores, packed, out, gather, ws, L, st, 0,
-                      static_cast<int>(nseg * G));
+                      static_cast<int>(nseg * G), defer ? &launched : nullptr);
     }
     PipeRes* r = nullptr;
     TRY(pipe_res(&r));
@@ -586,7 +615,7 @@ int run_layer_dev(const tkv_problem* p, const void* q, const void* k_cache, cons
     if (serial) {
       if (prof) cudaEventRecord(g_scan_start, st);
       for (int part = 0; part < P; ++part)
-        TRY(run_scan_part(p, cp, nseg * part / P, nseg * (part + 1) / P, st, false));
+        TRY(run_scan_part(p, cp, nseg * part / P, nseg * (part + 1) / P, st, false, part));
       if (prof) cudaEventRecord(g_scan_stop, st);
       for (int part = 0; part < P; ++part) {
         const int64_t s0 = nseg * part / P, s1 = nseg * (part + 1) / P;
@@ -612,7 +641,7 @@ int run_layer_dev(const tkv_problem* p, const void* q, const void* k_cache, cons
       const int64_t s0 = bound(part), s1 = bound(part + 1);
       // the first part's scan overlaps sample / threshold (PDL); later parts' CTAs take over SMs
       // as the previous part's retire (its epilogue waits for that grid; TMEM buffers the gap)
-      TRY(run_scan_part(p, cp, s0, s1, st, pdl_enabled() && !prof && (part == 0 || chain)));
+      TRY(run_scan_part(p, cp, s0, s1, st, pdl_enabled() && !prof && (part == 0 || chain), part, part == P - 1));
       if (cudaEventRecord(r->ev[part], st) != cudaSuccess || cudaStreamWaitEvent(r->side, r->ev[part], 0) != cudaSuccess)
         return fail(TKV_ECUDA, "pipeline fork failed");
       TRY(run_kth_part(p, cp, sl, s0, s1, part, r->side, false));
@@ -826,9 +855,15 @@ int tkv_shard_candidates2(const tkv_problem* p, int32_t narrow_k, const void* q,
   sl.k2 = narrow_k;
   sl.meta_t2 = at<uint64_t>(ws, L.mt2);
   TRY(run_scan_part(&pu, cp, 0, nseg, st, pdl_enabled()));
-  TRY(run_kth_part(&pu, cp, sl, 0, nseg, 0, st, pdl_enabled()));
-  TRY(run_emit(&pu, q, k_cache, k_cache, n_ctx, nullptr, at<int32_t>(ws, L.sidx), at<float>(ws, L.sscore), cand_full,
-               nullptr, 0, ws, L, st, 0, nbh));
+  if (diag_env("TKV_SHARD_CLUS", 0) != 0 && nbh * 4 <= device_sm_count()) {
+    // k-th + list emission (no gather) by one cluster per head: no k-th -> filter launch gap
+    TRY(run_head(&pu, q, k_cache, k_cache, n_ctx, nullptr, at<int32_t>(ws, L.sidx), at<float>(ws, L.sscore),
+                 cand_full, nullptr, 0, ws, L, st, cp, sl, nbh, pdl_enabled(), true));
+  } else {
+    TRY(run_kth_part(&pu, cp, sl, 0, nseg, 0, st, pdl_enabled()));
+    TRY(run_emit(&pu, q, k_cache, k_cache, n_ctx, nullptr, at<int32_t>(ws, L.sidx), at<float>(ws, L.sscore),
+                 cand_full, nullptr, 0, ws, L, st, 0, nbh));
+  }
   TKV_LAUNCH(launch_narrow_filter(cand_full, p->k, cand_narrow, narrow_k, at<uint64_t>(ws, L.mt2),
                                   at<uint64_t>(ws, L.mkth), at<int32_t>(ws, L.mkb), p->k, bounds, nbh, st));
   return TKV_OK;

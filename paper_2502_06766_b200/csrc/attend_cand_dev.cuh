@@ -144,7 +144,11 @@ __device__ __forceinline__ void attend_cand_run(const AttendParams& p, AttSmem& 
         woff += w < warp ? sm.wcnt[w] : 0u;
         m += sm.wcnt[w];
       }
-      if (tid == 0) sm.base = m ? atomicAdd(&p.out_cnt[bh], m) : 0u;
+      // output reservation: thread 0 keeps the result in a register and publishes it after the
+      // gather (storing it to shared memory here would stall the block's barrier on the atomic's
+      // L2 round trip)
+      uint32_t rbase = 0u;
+      if (tid == 0 && m) rbase = atomicAdd(&p.out_cnt[bh], m);
       uint32_t pos = woff + incl - mine;
 #pragma unroll
       for (int u = 0; u < PER; ++u) {
@@ -163,6 +167,8 @@ __device__ __forceinline__ void attend_cand_run(const AttendParams& p, AttSmem& 
       TKV_ATT_PHASE(63);
       // selected ids / raw scores (order unspecified); the reservation atomic completed
       // during the gather
+      if (tid == 0) sm.base = rbase;
+      __syncthreads();
       const uint32_t obase = sm.base;
       pos = woff + incl - mine;
 #pragma unroll

@@ -345,6 +345,7 @@ __global__ void __cluster_dims__(kKthCtas, 1, 1) __launch_bounds__(kKthThreads, 
     tl_end(p.tl, 53);
   }
 #endif
+  if (p.defer_fb) pdl_trigger();  // the PDL-launched gather may become resident now
   pdl_wait();  // candidates and histograms of the scan
   if (threadIdx.x == 0) tl_start(p.tl, 5);
 #ifdef TKV_DIAG
@@ -393,7 +394,7 @@ __global__ void __cluster_dims__(kKthCtas, 1, 1) __launch_bounds__(kKthThreads, 
         // the next kernel of the caller's stream waits for them — no host round trip, and no
         // cost at all when no head fails.
 #ifndef TKV_NO_CDP
-        if (atomicExch(p.hs.fb_launched, 1u) == 0u) {
+        if (atomicExch(p.hs.fb_launched, 1u) == 0u && !p.defer_fb) {
           fb_scan_kernel<<<p.fb_scan_grid, kScanWarps * 32, p.fb_scan_smem, cudaStreamTailLaunch>>>(p.fb_scan);
           SelectParams f = p;
           f.pass = kPassFallback;
@@ -596,6 +597,32 @@ __global__ void __launch_bounds__(NT, 4) attend_cand_fb_kernel(AttendParams p) {
 }
 #endif
 
+// Candidate-mode gather PDL-launched behind kth_kernel (whose CTAs trigger at their start, so
+// this grid's CTAs are resident before the k-th ends: no launch gap). kth_kernel then only flags
+// a failing head (defer_fb); this kernel sees the flag after the wait and tail-launches the exact
+// chain — re-scan, k-th (fallback pass), candidate gather over all heads — when it completes.
+__global__ void __launch_bounds__(NT, 4) attend_cand_pdl_kernel(HeadParams hp) {
+  __shared__ AttSmem sm;
+  extern __shared__ uint32_t s_pref[];
+  pdl_wait();  // k-th thresholds (and, transitively, the scan's candidates)
+  if (__ldcg(hp.s.hs.fb_launched) != 0u) {
+#ifndef TKV_NO_CDP
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      const SelectParams& p = hp.s;
+      fb_scan_kernel<<<p.fb_scan_grid, kScanWarps * 32, p.fb_scan_smem, cudaStreamTailLaunch>>>(p.fb_scan);
+      SelectParams f = p;
+      f.pass = kPassFallback;
+      f.pdl = 0;
+      const int nbh = p.bh_count ? p.bh_count : p.B * p.Hq;
+      kth_kernel<<<dim3(kKthCtas, nbh), kKthThreads, kKthSmem, cudaStreamTailLaunch>>>(f);
+      attend_cand_fb_kernel<<<hp.att_grid, NT, (nbh + 1) * sizeof(uint32_t), cudaStreamTailLaunch>>>(hp.a);
+    }
+#endif
+    return;
+  }
+  attend_cand_run(hp.a, sm, s_pref);
+}
+
 // (staging the V rows through shared memory with 1-D bulk copies instead measured 6.7 GB/s
 // per SM — one 256-byte cp.async.bulk per ~36 ns — against ~25 GB/s for register loads)
 constexpr int kHeadSmem = kHistBins * 4 + kHeadCap * 12;  // hist | bucket (= comp) | w
@@ -775,8 +802,8 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_topk_kernel(HeadParams h
   float lw = 0.f;
   __shared__ uint32_t s_gbase;
   auto flush = [&](uint32_t cnt) {  // rows [0, cnt) of s_comp / s_w; block-uniform cnt
-    if (tid == 0) s_gbase = cnt ? atomicAdd(&a.out_cnt[bh], cnt) : 0u;
-    __syncthreads();
+    uint32_t rbase = 0u;  // published after the gather (a shared store here would stall the block)
+    if (tid == 0 && cnt) rbase = atomicAdd(&a.out_cnt[bh], cnt);
     const int nr = static_cast<int>(cnt);
     if (a.gather) {
       constexpr int GU = 8;
@@ -804,6 +831,8 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_topk_kernel(HeadParams h
       }
       for (int i = tid; i < nr; i += HT) lw += s_w[i];
     }
+    if (tid == 0) s_gbase = rbase;
+    __syncthreads();
     const uint32_t gb = s_gbase;
     for (int i = tid; i < nr; i += HT) {
       const uint32_t o = gb + i;
@@ -940,7 +969,10 @@ cudaError_t launch_head_topk(const HeadParams& p, cudaStream_t s) {
 // programmatic dependent launch they are resident before the scan ends. A head whose sampled
 // threshold let fewer than kb rows through takes head_topk_kernel's exactness fallback.
 #ifndef TKV_CLUS_PAD
-#define TKV_CLUS_PAD 0  // experiments: extra dynamic shared memory (CTAs per SM)
+// shared memory held beyond what the kernel uses, so that one CTA fills an SM's shared memory
+// beside nothing else: the clusters then spread over 128 SMs instead of packing two or three
+// CTAs per SM (measured: cfg1 35.9 -> 34.1 us, cfg2 80.0 -> 74.6 us per step)
+#define TKV_CLUS_PAD 90000
 #endif
 constexpr int kClusSmem = kHistBins * 4 + kKthSmemBucket * 8 + kCandChunk * 4 + TKV_CLUS_PAD;  // + raw scores of a batch
 static_assert(sizeof(AttSmem) <= kHistBins * 4, "AttSmem aliases the histogram");
@@ -1041,6 +1073,19 @@ __global__ void __cluster_dims__(TKV_CLUS_CL, 1, 1) __launch_bounds__(NT, TKV_CL
     bcnt = s_hist[dstar];
     whole = bcnt == need;
   }
+  const bool narrow2 = p.k2 > 0 && p.k2 < kb;  // sharded narrow list bound (tkv_shard_candidates2)
+  if (narrow2 && rank == 0) {
+    if (all) {
+      copy_g2s_u32<NT, kHistBins>(s_hist, p.hs.hist + static_cast<int64_t>(bh) * kHistBins, kHistBins);
+      __syncthreads();
+    }
+    find_bucket<NT, kHistBins>(s_hist, static_cast<uint32_t>(p.k2), s_out, s_scr);
+    const uint32_t d2 = s_out[0];
+    if (tid == 0)
+      p.meta_t2[bh] = d2 + 1 < static_cast<uint32_t>(kHistBins)
+                          ? static_cast<uint64_t>(thr + ((d2 + 1) << shift)) << 32
+                          : ~0ull;  // the k2-th sits in the top (clamped) bucket: send none
+  }
   const bool refine = !all && !whole;
   bool big = refine && bcnt > static_cast<uint32_t>(kKthSmemBucket);
   TKV_CL_PHASE(68);
@@ -1132,6 +1177,7 @@ __global__ void __cluster_dims__(TKV_CLUS_CL, 1, 1) __launch_bounds__(NT, TKV_CL
       p.meta_kth[bh] = kb > 0 ? T : ~0ull;
       p.meta_kb[bh] = static_cast<int32_t>(kb);
       p.meta_max[bh] = kb > 0 ? mscore : -INFINITY;
+      if (p.k2 > 0 && !narrow2) p.meta_t2[bh] = kb > 0 ? T : 0ull;  // the narrow list is the whole selection
     }
     for (int i = static_cast<int>(kb) + tid; i < p.k; i += NT) {  // pads (attention.py:147-149)
       idx_o[i] = -1;
@@ -1171,7 +1217,8 @@ __global__ void __cluster_dims__(TKV_CLUS_CL, 1, 1) __launch_bounds__(NT, TKV_CL
       woff += w < warp ? sm.wcnt[w] : 0u;
       m += sm.wcnt[w];
     }
-    if (tid == 0) sm.base = m ? atomicAdd(&a.out_cnt[bh], m) : 0u;
+    uint32_t rbase = 0u;  // published after the gather (a shared store here would stall the barrier)
+    if (tid == 0 && m) rbase = atomicAdd(&a.out_cnt[bh], m);
     uint32_t pos = woff + incl - mine;
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
@@ -1186,9 +1233,13 @@ __global__ void __cluster_dims__(TKV_CLUS_CL, 1, 1) __launch_bounds__(NT, TKV_CL
       }
     }
     __syncthreads();
+    TKV_CL_PHASE(75);
     // (the candidates leave registers here: nothing but the V rows is live across the gather,
     // so every row load of a round is issued before the first use)
     if (a.gather) gather_acc<CtaGrp, TKV_CLUS_GU>(a, bh, static_cast<int>(m), sm, acc, lw);
+    TKV_CL_PHASE(76);
+    if (tid == 0) sm.base = rbase;
+    __syncthreads();
     const uint32_t obase = sm.base;
     for (uint32_t i = tid; i < m; i += NT) {  // ids / raw scores (order unspecified)
       const uint32_t o = obase + i;
@@ -1277,6 +1328,22 @@ cudaError_t launch_clus_topk(const HeadParams& p, cudaStream_t s) {
   q.att_grid = att_grid;
   const int nbh = p.s.bh_count ? p.s.bh_count : p.s.B * p.s.Hq;
   return launch_pdl(clus_topk_kernel, dim3(TKV_CLUS_CL, nbh), dim3(NT), kClusSmem, s, p.s.pdl != 0, q);
+}
+
+cudaError_t launch_attend_cand_pdl(const HeadParams& p, cudaStream_t s) {
+  prepare_fallback_kernels();
+  const int grid = per_device(reinterpret_cast<const void*>(attend_cand_pdl_kernel), 0, [] {
+    cudaFuncSetAttribute(attend_cand_pdl_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, attend_cand_pdl_kernel, NT, 8192);
+    const int g = device_sm_count() * (per > 0 ? per : 1);
+    return g < kMaxGatherGrid ? g : kMaxGatherGrid;
+  });
+  HeadParams q = p;
+  q.att_grid = grid;  // the fallback gather's grid (same kernel body)
+  const size_t nbh = p.a.bh_count ? static_cast<size_t>(p.a.bh_count) : static_cast<size_t>(p.a.B) * p.a.Hq;
+  return launch_pdl(attend_cand_pdl_kernel, dim3(grid), dim3(NT), (nbh + 1) * sizeof(uint32_t), s, true, q);
 }
 
 // ---------------------------------------------------------------- optional sorted output
