@@ -291,7 +291,7 @@ int run_scan_part(const tkv_problem* p, ScanParams cp, int64_t s0, int64_t s1, c
                   int part = 0, bool steal = true) {
   // the dynamic tail only where nothing absorbs the CTAs' uneven ends: in the chained parts
   // pipeline the next part's CTAs take over SMs as they free up (cfg5: 1448 us static, 1475-1490
-  // with every part balanced), so only the last part balances
+  // with every part balanced, 1459 with the last part balanced), so the parts stay static
   cp.steal = steal ? cp.steal + 2 * part : nullptr;  // overlapping part scans each own a counter pair
   cp.seg_begin = s0;
   cp.seg_count = s1 - s0;
@@ -641,7 +641,7 @@ int run_layer_dev(const tkv_problem* p, const void* q, const void* k_cache, cons
       const int64_t s0 = bound(part), s1 = bound(part + 1);
       // the first part's scan overlaps sample / threshold (PDL); later parts' CTAs take over SMs
       // as the previous part's retire (its epilogue waits for that grid; TMEM buffers the gap)
-      TRY(run_scan_part(p, cp, s0, s1, st, pdl_enabled() && !prof && (part == 0 || chain), part, part == P - 1));
+      TRY(run_scan_part(p, cp, s0, s1, st, pdl_enabled() && !prof && (part == 0 || chain), part, false));
       if (cudaEventRecord(r->ev[part], st) != cudaSuccess || cudaStreamWaitEvent(r->side, r->ev[part], 0) != cudaSuccess)
         return fail(TKV_ECUDA, "pipeline fork failed");
       TRY(run_kth_part(p, cp, sl, s0, s1, part, r->side, false));

@@ -981,7 +981,7 @@ static_assert(kCandChunk == NT * 4, "one compaction batch = the registers of one
 #define TKV_CLUS_CL 4  // CTAs per head (cluster size)
 #endif
 #ifndef TKV_CLUS_MINB
-#define TKV_CLUS_MINB 3  // <= 85 registers: a CTA fits beside a tcgen05 scan CTA
+#define TKV_CLUS_MINB 2  // <= 128 registers: one CTA per SM anyway (TKV_CLUS_PAD)
 #endif
 #ifndef TKV_CLUS_GU
 #define TKV_CLUS_GU 8  // V rows in flight per half-warp in the cluster kernel's gather
@@ -998,7 +998,11 @@ __global__ void __cluster_dims__(TKV_CLUS_CL, 1, 1) __launch_bounds__(NT, TKV_CL
   float* s_sc = reinterpret_cast<float*>(s_dyn + kHistBins * 4 + kKthSmemBucket * 8);  // a batch's raw scores
   __shared__ uint32_t s_scr[32], s_out[2], s_nb;
   __shared__ uint64_t s_rmax[NW], s_vmax, s_res;
-  __shared__ __align__(16) float s_part[kD + 4];
+  // rank 0 receives every CTA's (l, o[128]) partial here (DSMEM stores by the peers)
+  __shared__ __align__(16) float s_part[TKV_CLUS_CL][kD + 4];
+  // s_pulled: the peers finished reading this CTA's bucket members (it may exit after it);
+  // s_parts (rank 0): the peers' partials have landed
+  __shared__ __align__(8) uint64_t s_pulled, s_parts;
 
   pdl_wait();  // candidates and histograms of the scan
   if (threadIdx.x == 0) tl_start(p.tl, 5);
@@ -1012,6 +1016,11 @@ __global__ void __cluster_dims__(TKV_CLUS_CL, 1, 1) __launch_bounds__(NT, TKV_CL
 #endif
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = static_cast<int>(cluster.block_rank());
+  if (threadIdx.x == 0) {
+    mbar_init(smem_u32(&s_pulled), CL - 1);
+    mbar_init(smem_u32(&s_parts), CL - 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   const int bh = p.bh_begin + static_cast<int>(blockIdx.y);
   const int b = bh / p.Hq, h = bh % p.Hq;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1147,6 +1156,7 @@ __global__ void __cluster_dims__(TKV_CLUS_CL, 1, 1) __launch_bounds__(NT, TKV_CL
   if (nb > static_cast<uint32_t>(kKthSmemBucket) || own > static_cast<uint32_t>(kKthSmemBucket))
     big = refine;  // histogram / list mismatch guard
   __syncthreads();
+  if (tid < CL && tid != rank) mbar_arrive_remote(mapa_shared(smem_u32(&s_pulled), tid));  // peers' reads done
   uint64_t T;
   if (all) {
     T = 1ull;  // every valid (non-zero) candidate
@@ -1266,34 +1276,41 @@ __global__ void __cluster_dims__(TKV_CLUS_CL, 1, 1) __launch_bounds__(NT, TKV_CL
     lw = warp_sum(lw);
     if (lane == 0) sm.l[warp] = lw;
     __syncthreads();
+    // this CTA's partial → slot [rank] of rank 0's shared memory (DSMEM stores)
+    float* dst = cluster.map_shared_rank(&s_part[rank][0], 0);
     if (tid < kD) {
       float o = 0.f;
 #pragma unroll
       for (int w2 = 0; w2 < NW; ++w2) o += sm.red[w2][tid];
-      s_part[1 + tid] = o;
+      dst[1 + tid] = o;
     }
     if (tid == 0) {
       float l = 0.f;
 #pragma unroll
       for (int w2 = 0; w2 < NW; ++w2) l += sm.l[w2];
-      s_part[0] = l;
+      dst[0] = l;
     }
   }
   __threadfence();  // pinned-prefix marks before the finishing CTA reads them
-  cluster.sync();   // partials final; every peer read of s_bkt done
-  float o_c = 0.f, l_c = 0.f;
-  if (a.gather && rank == 0) {
-    for (int r = 0; r < CL; ++r) {  // rank order: deterministic
-      const float* pr = cluster.map_shared_rank(s_part, r);
-      if (tid < kD) o_c += pr[1 + tid];
-      l_c += pr[0];
-    }
-  }
-  cluster.sync();  // rank 0's reads done: the other CTAs may exit
-  TKV_CL_PHASE(73);
-  if (!a.gather || rank != 0) {
+  __syncthreads();  // the partial stores of the whole CTA precede thread 0's release
+  if (rank != 0) {
+    if (tid == 0) mbar_arrive_remote(mapa_shared(smem_u32(&s_parts), 0));
+    mbar_wait_cluster(smem_u32(&s_pulled), 0);  // no peer still reads this CTA's members
+    TKV_CL_PHASE(73);
     if (tid == 0) tl_end(p.tl, 5);
     return;
+  }
+  mbar_wait_cluster(smem_u32(&s_parts), 0);  // (also: every peer is past its reads of s_bkt)
+  mbar_wait_cluster(smem_u32(&s_pulled), 0);
+  TKV_CL_PHASE(73);
+  if (!a.gather) {
+    if (tid == 0) tl_end(p.tl, 5);
+    return;
+  }
+  float o_c = 0.f, l_c = 0.f;
+  for (int r = 0; r < CL; ++r) {  // rank order: deterministic
+    if (tid < kD) o_c += s_part[r][1 + tid];
+    l_c += s_part[r][0];
   }
   const int kvh = h / p.G;
   const int64_t nctx = a.n_ctx[b];

@@ -134,3 +134,16 @@ def test_product_package_does_not_import_oracle():
     for f in pkg.rglob("*.py"):
         src = f.read_text()
         assert "import oracle" not in src and "from oracle" not in src, f"{f} imports the oracle"
+
+
+def test_python_flag_constants_match_header():
+    """The drop-in's flag constants (_lib.F_*) are the header's TKV_F_* values."""
+    import re
+
+    from paper_2502_06766_b200 import _lib
+
+    hdr = (Path(__file__).resolve().parents[1] / "include" / "tkv.h").read_text()
+    defs = {m.group(1): int(m.group(2)) for m in re.finditer(r"#define TKV_F_(\w+) (\d+)u", hdr)}
+    for name in ("SORTED", "NO_FILTER", "GATHER_LIST", "HEAD", "NO_HEAD", "HOST_Q", "SCAN_HMMA", "CLUSTER",
+                 "NO_CLUSTER"):
+        assert getattr(_lib, "F_" + name) == defs[name], name
