@@ -441,7 +441,7 @@ def main():
                "d2h_bytes_per_step": B * HQ * D * 4 + B * HQ * k * 4, "steps": e2e_steps,
                "path": "TopkDecoder.step(q, k_new, v_new) -> (out, idx) with pinned host tensors: CUDA-graph "
                        "replay (a staging kernel reads q/k/v in place from pinned host memory, KV append, "
-                       "top-k attention writing out into pinned host memory, D2H copy of the selected ids) "
+                       "top-k attention writing out and the selected ids straight into pinned host memory) "
                        "-> host sync, every step",
                "out_only": {"value": round(e2e_out_us, 2), "d2h_bytes_per_step": B * HQ * D * 4,
                             "path": "the same step with return_idx=False (ids stay on the device)"}}

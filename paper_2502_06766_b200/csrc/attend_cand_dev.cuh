@@ -156,8 +156,10 @@ __device__ __forceinline__ void attend_cand_run(const AttendParams& p, AttSmem& 
           const uint64_t c = cv[u];
           const int64_t local = static_cast<int64_t>(comp_gid(c)) - p.row_offset;
           mark_pinned(p, bh, local);
+          const float sc = key_score(comp_key(c));
           sm.row[pos] = static_cast<int32_t>(local);
-          sm.w[pos] = exp2f(fmaf(key_score(comp_key(c)), zs, -zref));
+          sm.w[pos] = exp2f(fmaf(sc, zs, -zref));
+          sm.sc[pos] = sc;
           ++pos;
         }
       }
@@ -165,23 +167,19 @@ __device__ __forceinline__ void attend_cand_run(const AttendParams& p, AttSmem& 
       TKV_ATT_PHASE(62);
       if (p.gather) gather_acc(p, bh, static_cast<int>(m), sm, acc, lw);
       TKV_ATT_PHASE(63);
-      // selected ids / raw scores (order unspecified); the reservation atomic completed
-      // during the gather
+      // the reservation atomic completed during the gather
       if (tid == 0) sm.base = rbase;
       __syncthreads();
+      // ids / raw scores in list order from shared memory: consecutive threads, consecutive
+      // slots (coalesced — the ids may live in pinned host memory, written over PCIe)
       const uint32_t obase = sm.base;
-      pos = woff + incl - mine;
-#pragma unroll
-      for (int u = 0; u < PER; ++u) {
-        if (sel[u]) {
-          const uint64_t c = cv[u];
-          const uint32_t o = obase + pos;
-          if (o < static_cast<uint32_t>(p.k)) {
-            idx_o[o] = static_cast<int32_t>(comp_gid(c));
-            sc_o[o] = key_score(comp_key(c));
-            if (p.packed_out) p.packed_out[static_cast<int64_t>(bh) * p.k + o] = c;
-          }
-          ++pos;
+      for (uint32_t i = tid; i < m; i += NT) {
+        const uint32_t o = obase + i;
+        if (o < static_cast<uint32_t>(p.k)) {
+          const uint32_t gid = static_cast<uint32_t>(static_cast<int64_t>(sm.row[i]) + p.row_offset);
+          idx_o[o] = static_cast<int32_t>(gid);
+          sc_o[o] = sm.sc[i];
+          if (p.packed_out) p.packed_out[static_cast<int64_t>(bh) * p.k + o] = make_comp(score_key(sm.sc[i]), gid);
         }
       }
     }

@@ -180,6 +180,7 @@ __device__ __forceinline__ void mark_pinned(const AttendParams& p, int bh, int64
 struct AttSmem {
   __align__(16) float w[kCandChunk];
   __align__(16) int32_t row[kCandChunk];
+  float sc[kCandChunk];  // candidate mode: raw scores of the batch's selected rows (coalesced id writes)
   float red[NW][kD];
   float l[NW];
   float z[128];

@@ -974,8 +974,9 @@ cudaError_t launch_head_topk(const HeadParams& p, cudaStream_t s) {
 // CTAs per SM (measured: cfg1 35.9 -> 34.1 us, cfg2 80.0 -> 74.6 us per step)
 #define TKV_CLUS_PAD 90000
 #endif
-constexpr int kClusSmem = kHistBins * 4 + kKthSmemBucket * 8 + kCandChunk * 4 + TKV_CLUS_PAD;  // + raw scores of a batch
-static_assert(sizeof(AttSmem) <= kHistBins * 4, "AttSmem aliases the histogram");
+constexpr int kClusFront = (static_cast<int>(sizeof(AttSmem)) > kHistBins * 4 ? static_cast<int>(sizeof(AttSmem))
+                                                                                 : kHistBins * 4 + 15) / 16 * 16;
+constexpr int kClusSmem = kClusFront + kKthSmemBucket * 8 + TKV_CLUS_PAD;  // [hist | AttSmem] [bucket members]
 static_assert(kCandChunk == NT * 4, "one compaction batch = the registers of one slice batch");
 #ifndef TKV_CLUS_CL
 #define TKV_CLUS_CL 4  // CTAs per head (cluster size)
@@ -994,8 +995,8 @@ __global__ void __cluster_dims__(TKV_CLUS_CL, 1, 1) __launch_bounds__(NT, TKV_CL
   extern __shared__ __align__(16) uint8_t s_dyn[];
   uint32_t* s_hist = reinterpret_cast<uint32_t*>(s_dyn);                 // before T
   AttSmem& sm = *reinterpret_cast<AttSmem*>(s_dyn);                      // after T (aliases s_hist)
-  uint64_t* s_bkt = reinterpret_cast<uint64_t*>(s_dyn + kHistBins * 4);  // read by peers until the last barrier
-  float* s_sc = reinterpret_cast<float*>(s_dyn + kHistBins * 4 + kKthSmemBucket * 8);  // a batch's raw scores
+  uint64_t* s_bkt = reinterpret_cast<uint64_t*>(s_dyn + kClusFront);  // read by peers until s_pulled completes
+  float* s_sc = sm.sc;  // a batch's raw scores
   __shared__ uint32_t s_scr[32], s_out[2], s_nb;
   __shared__ uint64_t s_rmax[NW], s_vmax, s_res;
   // rank 0 receives every CTA's (l, o[128]) partial here (DSMEM stores by the peers)

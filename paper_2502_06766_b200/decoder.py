@@ -135,15 +135,21 @@ class TopkDecoder:
             q_in = b["q"]
         else:
             q_in = q_h
+        # the selected ids likewise go straight into pinned host memory, written by the gather
+        # as it finds them (coalesced 128-byte PCIe writes overlapping the gather) instead of a
+        # device->host copy of the whole list after it — unless the ids are sorted afterwards
+        # (the sort kernel would then work over PCIe)
+        direct_idx = with_idx and not self.kw["sorted"]
+        idx_buf = b["idx_h"] if direct_idx else b["idx"]
         if with_kv and self.fold_append:  # window append folded into the attention call
             ops.topk_decode_step(q_in, k_h, v_h, self.k_cache, self.v_cache, self.n_ctx,
-                                 self.n_win, self.k, out=b["out_h"], idx=b["idx"], scores=b["scores"],
+                                 self.n_win, self.k, out=b["out_h"], idx=idx_buf, scores=b["scores"],
                                  workspace=self.ws, **self.kw)
         else:
             ops.topk_decode_attention(q_in, self.k_cache, self.v_cache, self.n_ctx, self.k,
-                                      n_win=self.n_win, out=b["out_h"], idx=b["idx"], scores=b["scores"],
+                                      n_win=self.n_win, out=b["out_h"], idx=idx_buf, scores=b["scores"],
                                       workspace=self.ws, **self.kw)
-        if with_idx:
+        if with_idx and not direct_idx:
             b["idx_h"].copy_(b["idx"], non_blocking=True)
 
     # ------------------------------------------------------------------ user API
