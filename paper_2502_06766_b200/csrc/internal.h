@@ -30,7 +30,7 @@ constexpr int kKthSmem = kKthSmemBucket * 8;  // kth_kernel dynamic shared memor
 constexpr int kAttendThreads = 256;
 constexpr int kAttendChunk = 512;    // selected rows per gather CTA (list mode)
 #ifndef TKV_CAND_CHUNK
-#define TKV_CAND_CHUNK 1024
+#define TKV_CAND_CHUNK 2048
 #endif
 constexpr int kCandChunk = TKV_CAND_CHUNK;  // candidates per compaction + gather batch (candidate mode)
 constexpr int kCandQuant = 256;             // candidate-mode work items are multiples of this
@@ -315,6 +315,7 @@ cudaError_t launch_attend_cand(const AttendParams& p, cudaStream_t s);
 cudaError_t launch_attend_list(const AttendParams& p, cudaStream_t s);
 cudaError_t launch_sort(const SortParams& p, int nbh, cudaStream_t s, int* launches);
 cudaError_t launch_attend(const AttendParams& p, cudaStream_t s);
+cudaError_t launch_attend_owned(const AttendParams& p, cudaStream_t s);
 cudaError_t launch_finalize(const AttendParams& p, cudaStream_t s);
 cudaError_t launch_append(const AppendParams& p, cudaStream_t s);
 

@@ -977,7 +977,7 @@ cudaError_t launch_head_topk(const HeadParams& p, cudaStream_t s) {
 constexpr int kClusFront = (static_cast<int>(sizeof(AttSmem)) > kHistBins * 4 ? static_cast<int>(sizeof(AttSmem))
                                                                                  : kHistBins * 4 + 15) / 16 * 16;
 constexpr int kClusSmem = kClusFront + kKthSmemBucket * 8 + TKV_CLUS_PAD;  // [hist | AttSmem] [bucket members]
-static_assert(kCandChunk == NT * 4, "one compaction batch = the registers of one slice batch");
+static_assert(kCandChunk % NT == 0, "one compaction batch = the registers of one slice batch");
 #ifndef TKV_CLUS_CL
 #define TKV_CLUS_CL 4  // CTAs per head (cluster size)
 #endif

@@ -21,4 +21,5 @@ ncu --set full --clock-control none --import-source on -k regex:scan_tc -s 3 -c 
 ncu --set full --clock-control none --import-source on -k regex:clus_topk -s 3 -c 1 -o $O/clus_cfg2 \
     python tools/scan_ab.py --config cfg2 --steps 3 > $O/ncu_clus.log 2>&1
 python tools/k_sweep.py --out $O/ksweep.json > $O/ksweep.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -x -q > $O/tests.txt 2>&1
 ls $O
