@@ -315,7 +315,6 @@ cudaError_t launch_attend_cand(const AttendParams& p, cudaStream_t s);
 cudaError_t launch_attend_list(const AttendParams& p, cudaStream_t s);
 cudaError_t launch_sort(const SortParams& p, int nbh, cudaStream_t s, int* launches);
 cudaError_t launch_attend(const AttendParams& p, cudaStream_t s);
-cudaError_t launch_attend_owned(const AttendParams& p, cudaStream_t s);
 cudaError_t launch_finalize(const AttendParams& p, cudaStream_t s);
 cudaError_t launch_append(const AppendParams& p, cudaStream_t s);
 
