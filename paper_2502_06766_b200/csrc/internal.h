@@ -10,7 +10,10 @@
 
 namespace tkv {
 
-constexpr int kSamples = 4096;       // sampled rows per (b, kv head) for the threshold estimate
+#ifndef TKV_SAMPLES
+#define TKV_SAMPLES 4096
+#endif
+constexpr int kSamples = TKV_SAMPLES;  // sampled rows per (b, kv head) for the threshold estimate
 constexpr int kSampleThreads = 256;  // sample-scoring CTA
 #ifndef TKV_THR_THREADS
 #define TKV_THR_THREADS 512
