@@ -27,7 +27,11 @@ constexpr int kScanStage = kScanRows * kScanFlushEvery;  // staged candidates pe
 constexpr int kSelectThreads = 1024;
 constexpr int kSelectBucketCap = 8192;  // threshold-bucket candidates refined in shared memory
 constexpr int kKthThreads = 512;        // kth_kernel CTA
-constexpr int kKthCtas = 4;             // kth_kernel CTAs per (b, q head)
+#ifndef TKV_KTH_CTAS
+#define TKV_KTH_CTAS 4
+#endif
+constexpr int kKthCtas = TKV_KTH_CTAS;  // kth_kernel CTAs per (b, q head) (one cluster)
+constexpr int kKthManyHeads = 128;      // from this many heads per call: 2-CTA clusters
 constexpr int kKthSmemBucket = 2048;    // threshold-bucket members rank-selected in shared memory
 constexpr int kKthSmem = kKthSmemBucket * 8;  // kth_kernel dynamic shared memory (fits beside the scan)
 constexpr int kAttendThreads = 256;

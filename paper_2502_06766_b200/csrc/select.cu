@@ -329,7 +329,11 @@ __global__ void __launch_bounds__(kScanWarps * 32, 2) fb_scan_kernel(ScanParams 
 // <= 32 registers (4 CTAs per SM): a kth CTA's 16 warps then fit beside a 320-thread scan CTA in
 // every SM sub-partition's 16K-register file (the scan puts 3 warps x 3840 registers on some),
 // so the k-th of one part runs while the next part is scanned
-__global__ void __cluster_dims__(kKthCtas, 1, 1) __launch_bounds__(kKthThreads, 4) kth_kernel(SelectParams p) {
+// CL: CTAs per head (the cluster); the body slices by gridDim.x, so any CL works. 4 by default;
+// 2 when many heads share the call (their k-th then fits beside the next part's scan: cfg5
+// 1454 -> 1419 us), 8 measured slower (cfg3 365 vs 358 us).
+template <int CL>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kKthThreads, 4) kth_kernel(SelectParams p) {
   constexpr int KT = kKthThreads, KW = KT / 32;
   extern __shared__ uint64_t s_bkt[];  // [kKthSmemBucket]
   __shared__ __align__(16) uint32_t s_hist[kHistBins];
@@ -398,7 +402,7 @@ __global__ void __cluster_dims__(kKthCtas, 1, 1) __launch_bounds__(kKthThreads, 
           fb_scan_kernel<<<p.fb_scan_grid, kScanWarps * 32, p.fb_scan_smem, cudaStreamTailLaunch>>>(p.fb_scan);
           SelectParams f = p;
           f.pass = kPassFallback;
-          kth_kernel<<<dim3(kKthCtas, p.bh_count ? p.bh_count : p.B * p.Hq), kKthThreads, kKthSmem,
+          kth_kernel<kKthCtas><<<dim3(kKthCtas, p.bh_count ? p.bh_count : p.B * p.Hq), kKthThreads, kKthSmem,
                        cudaStreamTailLaunch>>>(f);
         }
 #endif
@@ -566,13 +570,18 @@ void prepare_fallback_kernels() {
 
 cudaError_t launch_kth(const SelectParams& p, cudaStream_t s) {
   prepare_fallback_kernels();
-  per_device(reinterpret_cast<const void*>(kth_kernel), 0, [] {
+  per_device(reinterpret_cast<const void*>(kth_kernel<kKthCtas>), 0, [] {
     // same shared-memory carveout as the scan, so both can share an SM (parts pipeline)
-    cudaFuncSetAttribute(kth_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(kth_kernel<kKthCtas>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(kth_kernel<2>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     return 1;
   });
-  return launch_pdl(kth_kernel, dim3(kKthCtas, p.bh_count ? p.bh_count : p.B * p.Hq), dim3(kKthThreads), kKthSmem, s,
-                    p.pdl && p.pass == kPassMain, p);
+  const int nbh = p.bh_count ? p.bh_count : p.B * p.Hq;
+  const bool pdl = p.pdl && p.pass == kPassMain;
+  if (nbh >= kKthManyHeads)
+    return launch_pdl(kth_kernel<2>, dim3(2, nbh), dim3(kKthThreads), kKthSmem, s, pdl, p);
+  return launch_pdl(kth_kernel<kKthCtas>, dim3(kKthCtas, nbh), dim3(kKthThreads), kKthSmem, s, pdl, p);
 }
 
 // ---------------------------------------------------------------- small k: a few CTAs per head
@@ -614,7 +623,7 @@ __global__ void __launch_bounds__(NT, 4) attend_cand_pdl_kernel(HeadParams hp) {
       f.pass = kPassFallback;
       f.pdl = 0;
       const int nbh = p.bh_count ? p.bh_count : p.B * p.Hq;
-      kth_kernel<<<dim3(kKthCtas, nbh), kKthThreads, kKthSmem, cudaStreamTailLaunch>>>(f);
+      kth_kernel<kKthCtas><<<dim3(kKthCtas, nbh), kKthThreads, kKthSmem, cudaStreamTailLaunch>>>(f);
       attend_cand_fb_kernel<<<hp.att_grid, NT, (nbh + 1) * sizeof(uint32_t), cudaStreamTailLaunch>>>(hp.a);
     }
 #endif
@@ -680,7 +689,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_topk_kernel(HeadParams h
           f.pass = kPassFallback;
           f.pdl = 0;
           const int nbh = p.bh_count ? p.bh_count : p.B * p.Hq;
-          kth_kernel<<<dim3(kKthCtas, nbh), kKthThreads, kKthSmem, cudaStreamTailLaunch>>>(f);
+          kth_kernel<kKthCtas><<<dim3(kKthCtas, nbh), kKthThreads, kKthSmem, cudaStreamTailLaunch>>>(f);
           attend_cand_fb_kernel<<<hp.att_grid, NT, (nbh + 1) * sizeof(uint32_t), cudaStreamTailLaunch>>>(a);
         }
 #endif
@@ -1052,7 +1061,7 @@ __global__ void __cluster_dims__(TKV_CLUS_CL, 1, 1) __launch_bounds__(NT, TKV_CL
           f.pass = kPassFallback;
           f.pdl = 0;
           const int nbh = p.bh_count ? p.bh_count : p.B * p.Hq;
-          kth_kernel<<<dim3(kKthCtas, nbh), kKthThreads, kKthSmem, cudaStreamTailLaunch>>>(f);
+          kth_kernel<kKthCtas><<<dim3(kKthCtas, nbh), kKthThreads, kKthSmem, cudaStreamTailLaunch>>>(f);
           attend_cand_fb_kernel<<<hp.att_grid, NT, (nbh + 1) * sizeof(uint32_t), cudaStreamTailLaunch>>>(a);
         }
 #endif
