@@ -310,7 +310,7 @@ int run_scan_part(const tkv_problem* p, ScanParams cp, int64_t s0, int64_t s1, c
 // k-th of failing heads, tail-launched on device); the selected set of a head is
 // { candidates c : c >= meta_kth }, materialised by run_emit
 int run_kth_part(const tkv_problem* p, ScanParams cp, SelectParams sl, int64_t s0, int64_t s1, int part,
-                 cudaStream_t st, bool pdl, SelectParams* launched = nullptr) {
+                 cudaStream_t st, bool pdl) {
   const int G = p->n_q_heads / p->n_kv_heads;
   cp.seg_begin = s0;
   cp.seg_count = s1 - s0;
@@ -323,7 +323,6 @@ int run_kth_part(const tkv_problem* p, ScanParams cp, SelectParams sl, int64_t s
   sl.fb_scan = cp;
   scan_launch_shape(cp, &sl.fb_scan_grid, &sl.fb_scan_smem);
   TKV_LAUNCH(launch_kth(sl, st));
-  if (launched) *launched = sl;
   return TKV_OK;
 }
 
@@ -429,7 +428,7 @@ bool list_gather_used(const tkv_problem* p, int bh_count, int gather) {
 int run_emit(const tkv_problem* p, const void* q, const void* k_cache, const void* v_cache,
              const int32_t* n_ctx, const int32_t* n_win, int32_t* idx, float* scores,
              uint64_t* packed, float* out, int gather, void* ws, const Layout& L, cudaStream_t st,
-             int bh_begin, int bh_count, const SelectParams* deferred = nullptr) {
+             int bh_begin, int bh_count) {
   AttendParams a = make_attend(p, q, k_cache, v_cache, n_ctx, n_win, idx, scores, ws, L);
   a.bh_begin = bh_begin;
   a.bh_count = bh_count;
@@ -445,11 +444,6 @@ int run_emit(const tkv_problem* p, const void* q, const void* k_cache, const voi
     TKV_LAUNCH(launch_attend_cand(a, st));
     a.gather = 1;
     TKV_LAUNCH(launch_attend_list(a, st));
-  } else if (deferred) {  // PDL behind the k-th kernel, which left the fallback launch to it
-    HeadParams hp{};
-    hp.s = *deferred;
-    hp.a = a;
-    TKV_LAUNCH(launch_attend_cand_pdl(hp, st));
   } else {
     TKV_LAUNCH(launch_attend_cand(a, st));
   }
@@ -597,17 +591,9 @@ int run_layer_dev(const tkv_problem* p, const void* q, const void* k_cache, cons
       if (use_head_topk(p, gather))
         return run_head(p, q, k_cache, v_cache, n_ctx, n_win, idx, scores, packed, out, gather, ws, L, st, cp, sl,
                         static_cast<int>(nseg * G), pdl_enabled() && !prof);
-      // TKV_GATHER_PDL=1 (TKV_DIAG builds, experiment): the gather PDL-launched behind the k-th
-      // kernel, which then leaves the exactness fallback launch to the gather. Measured slower
-      // (cfg2 78.2 vs 75.8 us, cfg3 363.5 vs 360.7) and it hung one adversarial fuzz case, so off
-      const bool pdl = pdl_enabled() && !prof;
-      const bool defer = pdl && !list_gather_used(p, static_cast<int>(nseg * G), gather) &&
-                         diag_env("TKV_GATHER_PDL", 0) != 0;
-      SelectParams launched{};
-      if (defer) sl.defer_fb = 1;
-      TRY(run_kth_part(p, cp, sl, 0, nseg, 0, st, pdl, &launched));
+      TRY(run_kth_part(p, cp, sl, 0, nseg, 0, st, pdl_enabled() && !prof));
       return run_emit(p, q, k_cache, v_cache, n_ctx, n_win, idx, scores, packed, out, gather, ws, L, st, 0,
-                      static_cast<int>(nseg * G), defer ? &launched : nullptr);
+                      static_cast<int>(nseg * G));
     }
     PipeRes* r = nullptr;
     TRY(pipe_res(&r));
@@ -855,15 +841,9 @@ int tkv_shard_candidates2(const tkv_problem* p, int32_t narrow_k, const void* q,
   sl.k2 = narrow_k;
   sl.meta_t2 = at<uint64_t>(ws, L.mt2);
   TRY(run_scan_part(&pu, cp, 0, nseg, st, pdl_enabled()));
-  if (diag_env("TKV_SHARD_CLUS", 0) != 0 && nbh * 4 <= device_sm_count()) {
-    // k-th + list emission (no gather) by one cluster per head: no k-th -> filter launch gap
-    TRY(run_head(&pu, q, k_cache, k_cache, n_ctx, nullptr, at<int32_t>(ws, L.sidx), at<float>(ws, L.sscore),
-                 cand_full, nullptr, 0, ws, L, st, cp, sl, nbh, pdl_enabled(), true));
-  } else {
-    TRY(run_kth_part(&pu, cp, sl, 0, nseg, 0, st, pdl_enabled()));
-    TRY(run_emit(&pu, q, k_cache, k_cache, n_ctx, nullptr, at<int32_t>(ws, L.sidx), at<float>(ws, L.sscore),
-                 cand_full, nullptr, 0, ws, L, st, 0, nbh));
-  }
+  TRY(run_kth_part(&pu, cp, sl, 0, nseg, 0, st, pdl_enabled()));
+  TRY(run_emit(&pu, q, k_cache, k_cache, n_ctx, nullptr, at<int32_t>(ws, L.sidx), at<float>(ws, L.sscore), cand_full,
+               nullptr, 0, ws, L, st, 0, nbh));
   TKV_LAUNCH(launch_narrow_filter(cand_full, p->k, cand_narrow, narrow_k, at<uint64_t>(ws, L.mt2),
                                   at<uint64_t>(ws, L.mkth), at<int32_t>(ws, L.mkb), p->k, bounds, nbh, st));
   return TKV_OK;

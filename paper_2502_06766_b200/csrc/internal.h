@@ -157,11 +157,7 @@ struct SelectParams {
   // above the one holding the k2-th largest; T itself when every candidate is selected)
   int k2;
   uint64_t* meta_t2;
-  // exactness fallback, tail-launched by kth_kernel (main pass) when a head failed — or, with
-  // defer_fb, only flagged in *hs.fb_launched and tail-launched by the candidate gather that is
-  // PDL-launched behind the k-th kernel (attend_cand_pdl_kernel: its CTAs wait on the k-th grid,
-  // so a launch from the k-th kernel could find no SM room for the re-scan)
-  int defer_fb;
+  // exactness fallback, tail-launched by kth_kernel (main pass) when a head failed
   ScanParams fb_scan;
   int fb_scan_grid;
   int fb_scan_smem;
@@ -316,8 +312,6 @@ cudaError_t launch_narrow_check(const uint64_t* gathered, int n_shards, int list
 cudaError_t launch_kth(const SelectParams& p, cudaStream_t s);
 cudaError_t launch_head_topk(const HeadParams& p, cudaStream_t s);
 cudaError_t launch_clus_topk(const HeadParams& p, cudaStream_t s);
-// candidate-mode gather PDL-launched behind kth_kernel (defer_fb): tail-launches the flagged fallback
-cudaError_t launch_attend_cand_pdl(const HeadParams& p, cudaStream_t s);
 cudaError_t launch_attend_cand(const AttendParams& p, cudaStream_t s);
 cudaError_t launch_attend_list(const AttendParams& p, cudaStream_t s);
 cudaError_t launch_sort(const SortParams& p, int nbh, cudaStream_t s, int* launches);

@@ -349,7 +349,6 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kKthThreads, 4) kth
     tl_end(p.tl, 53);
   }
 #endif
-  if (p.defer_fb) pdl_trigger();  // the PDL-launched gather may become resident now
   pdl_wait();  // candidates and histograms of the scan
   if (threadIdx.x == 0) tl_start(p.tl, 5);
 #ifdef TKV_DIAG
@@ -398,7 +397,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kKthThreads, 4) kth
         // the next kernel of the caller's stream waits for them — no host round trip, and no
         // cost at all when no head fails.
 #ifndef TKV_NO_CDP
-        if (atomicExch(p.hs.fb_launched, 1u) == 0u && !p.defer_fb) {
+        if (atomicExch(p.hs.fb_launched, 1u) == 0u) {
           fb_scan_kernel<<<p.fb_scan_grid, kScanWarps * 32, p.fb_scan_smem, cudaStreamTailLaunch>>>(p.fb_scan);
           SelectParams f = p;
           f.pass = kPassFallback;
@@ -605,32 +604,6 @@ __global__ void __launch_bounds__(NT, 4) attend_cand_fb_kernel(AttendParams p) {
   attend_cand_run(p, sm, s_pref);
 }
 #endif
-
-// Candidate-mode gather PDL-launched behind kth_kernel (whose CTAs trigger at their start, so
-// this grid's CTAs are resident before the k-th ends: no launch gap). kth_kernel then only flags
-// a failing head (defer_fb); this kernel sees the flag after the wait and tail-launches the exact
-// chain — re-scan, k-th (fallback pass), candidate gather over all heads — when it completes.
-__global__ void __launch_bounds__(NT, 4) attend_cand_pdl_kernel(HeadParams hp) {
-  __shared__ AttSmem sm;
-  extern __shared__ uint32_t s_pref[];
-  pdl_wait();  // k-th thresholds (and, transitively, the scan's candidates)
-  if (__ldcg(hp.s.hs.fb_launched) != 0u) {
-#ifndef TKV_NO_CDP
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      const SelectParams& p = hp.s;
-      fb_scan_kernel<<<p.fb_scan_grid, kScanWarps * 32, p.fb_scan_smem, cudaStreamTailLaunch>>>(p.fb_scan);
-      SelectParams f = p;
-      f.pass = kPassFallback;
-      f.pdl = 0;
-      const int nbh = p.bh_count ? p.bh_count : p.B * p.Hq;
-      kth_kernel<kKthCtas><<<dim3(kKthCtas, nbh), kKthThreads, kKthSmem, cudaStreamTailLaunch>>>(f);
-      attend_cand_fb_kernel<<<hp.att_grid, NT, (nbh + 1) * sizeof(uint32_t), cudaStreamTailLaunch>>>(hp.a);
-    }
-#endif
-    return;
-  }
-  attend_cand_run(hp.a, sm, s_pref);
-}
 
 // (staging the V rows through shared memory with 1-D bulk copies instead measured 6.7 GB/s
 // per SM — one 256-byte cp.async.bulk per ~36 ns — against ~25 GB/s for register loads)
@@ -1092,19 +1065,6 @@ __global__ void __cluster_dims__(TKV_CLUS_CL, 1, 1) __launch_bounds__(NT, TKV_CL
     bcnt = s_hist[dstar];
     whole = bcnt == need;
   }
-  const bool narrow2 = p.k2 > 0 && p.k2 < kb;  // sharded narrow list bound (tkv_shard_candidates2)
-  if (narrow2 && rank == 0) {
-    if (all) {
-      copy_g2s_u32<NT, kHistBins>(s_hist, p.hs.hist + static_cast<int64_t>(bh) * kHistBins, kHistBins);
-      __syncthreads();
-    }
-    find_bucket<NT, kHistBins>(s_hist, static_cast<uint32_t>(p.k2), s_out, s_scr);
-    const uint32_t d2 = s_out[0];
-    if (tid == 0)
-      p.meta_t2[bh] = d2 + 1 < static_cast<uint32_t>(kHistBins)
-                          ? static_cast<uint64_t>(thr + ((d2 + 1) << shift)) << 32
-                          : ~0ull;  // the k2-th sits in the top (clamped) bucket: send none
-  }
   const bool refine = !all && !whole;
   bool big = refine && bcnt > static_cast<uint32_t>(kKthSmemBucket);
   TKV_CL_PHASE(68);
@@ -1197,7 +1157,6 @@ __global__ void __cluster_dims__(TKV_CLUS_CL, 1, 1) __launch_bounds__(NT, TKV_CL
       p.meta_kth[bh] = kb > 0 ? T : ~0ull;
       p.meta_kb[bh] = static_cast<int32_t>(kb);
       p.meta_max[bh] = kb > 0 ? mscore : -INFINITY;
-      if (p.k2 > 0 && !narrow2) p.meta_t2[bh] = kb > 0 ? T : 0ull;  // the narrow list is the whole selection
     }
     for (int i = static_cast<int>(kb) + tid; i < p.k; i += NT) {  // pads (attention.py:147-149)
       idx_o[i] = -1;
@@ -1355,22 +1314,6 @@ cudaError_t launch_clus_topk(const HeadParams& p, cudaStream_t s) {
   q.att_grid = att_grid;
   const int nbh = p.s.bh_count ? p.s.bh_count : p.s.B * p.s.Hq;
   return launch_pdl(clus_topk_kernel, dim3(TKV_CLUS_CL, nbh), dim3(NT), kClusSmem, s, p.s.pdl != 0, q);
-}
-
-cudaError_t launch_attend_cand_pdl(const HeadParams& p, cudaStream_t s) {
-  prepare_fallback_kernels();
-  const int grid = per_device(reinterpret_cast<const void*>(attend_cand_pdl_kernel), 0, [] {
-    cudaFuncSetAttribute(attend_cand_pdl_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         cudaSharedmemCarveoutMaxShared);
-    int per = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, attend_cand_pdl_kernel, NT, 8192);
-    const int g = device_sm_count() * (per > 0 ? per : 1);
-    return g < kMaxGatherGrid ? g : kMaxGatherGrid;
-  });
-  HeadParams q = p;
-  q.att_grid = grid;  // the fallback gather's grid (same kernel body)
-  const size_t nbh = p.a.bh_count ? static_cast<size_t>(p.a.bh_count) : static_cast<size_t>(p.a.B) * p.a.Hq;
-  return launch_pdl(attend_cand_pdl_kernel, dim3(grid), dim3(NT), (nbh + 1) * sizeof(uint32_t), s, true, q);
 }
 
 // ---------------------------------------------------------------- optional sorted output

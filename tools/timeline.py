@@ -33,7 +33,7 @@ EXTRA_PHASES = {42: "scan epilogue: wait for a unit's scores", 43: "scan epilogu
                 66: "gather: →ticket / head finish",
                 67: "cluster CTA: past wait→params", 68: "→hist + bucket", 69: "→slice scan + max",
                 70: "→cluster barrier 1", 71: "→peer members + T", 72: "→compaction + V gather",
-                73: "→partials + 2 cluster barriers", 74: "→finish (rank 0)",
+                73: "→partial hand-off (remote mbarrier arrivals)", 74: "→finish (rank 0)",
                 75: "  (per batch: →compaction)", 76: "  (per batch: →V gather)"}
 
 
