@@ -35,11 +35,15 @@ constexpr int kKthManyHeads = 128;      // from this many heads per call: 2-CTA 
 constexpr int kKthSmemBucket = 2048;    // threshold-bucket members rank-selected in shared memory
 constexpr int kKthSmem = kKthSmemBucket * 8;  // kth_kernel dynamic shared memory (fits beside the scan)
 constexpr int kAttendThreads = 256;
-constexpr int kAttendChunk = 512;    // selected rows per gather CTA (list mode)
+#ifndef TKV_ATTEND_CHUNK
+#define TKV_ATTEND_CHUNK 512
+#endif
+constexpr int kAttendChunk = TKV_ATTEND_CHUNK;  // selected rows per gather CTA (list mode)
 #ifndef TKV_CAND_CHUNK
 #define TKV_CAND_CHUNK 2048
 #endif
 constexpr int kCandChunk = TKV_CAND_CHUNK;  // candidates per compaction + gather batch (candidate mode)
+static_assert(kAttendChunk <= kCandChunk, "a list chunk fits the gather's row buffer");
 constexpr int kCandQuant = 256;             // candidate-mode work items are multiples of this
 constexpr int kMaxGatherGrid = 1023;        // candidate-mode gather CTAs (bounds the partial slots)
 constexpr int kFlatMinRows = 256;           // flat list gather: rows per CTA range, at least

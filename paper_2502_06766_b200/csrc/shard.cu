@@ -110,6 +110,7 @@ cudaError_t launch_narrow_filter(const uint64_t* full, int full_len, uint64_t* n
 namespace {
 constexpr int MT = 512, MW = MT / 32, CL = 4;
 constexpr int kMergeBkt = 2048;  // bucket members rank-selected in shared memory
+constexpr int kMergeCache = 12288;  // this CTA's narrow-list entries kept in shared memory (96 KB)
 
 struct MergeSmem {
   uint32_t hist[kHistBins];
@@ -126,8 +127,12 @@ struct MergeSmem {
 // slots and past the end), each thread loading UNR entries before using any: one memory round
 // trip per batch instead of one per entry. Every lane makes the same number of calls, so fn may
 // use warp ballots.
+// cmode 1: also keep every loaded entry in `cache` (shared memory); cmode 2: read the entries
+// from `cache` instead of the lists (peer memory over NVLink, or L2) — the merge sweeps the same
+// narrow lists up to five times.
 template <int UNR = 8, class Fn>
-__device__ __forceinline__ void sweep(const uint64_t* const* lists, int G, int len, int bh, int cta, Fn&& fn) {
+__device__ __forceinline__ void sweep(const uint64_t* const* lists, int G, int len, int bh, int cta, Fn&& fn,
+                                      uint64_t* cache = nullptr, int cmode = 0) {
   const int nr = (G - cta + CL - 1) / CL;  // ranks this CTA reads
   const int total = nr * len;
   for (int base = 0; base < total; base += MT * UNR) {
@@ -136,7 +141,12 @@ __device__ __forceinline__ void sweep(const uint64_t* const* lists, int G, int l
     for (int u = 0; u < UNR; ++u) {
       const int i = base + u * MT + static_cast<int>(threadIdx.x);
       const int r = i / len;
-      cv[u] = i < total ? lists[cta + r * CL][static_cast<int64_t>(bh) * len + (i - r * len)] : 0ull;
+      if (cmode == 2) {
+        cv[u] = i < total ? cache[i] : 0ull;
+      } else {
+        cv[u] = i < total ? lists[cta + r * CL][static_cast<int64_t>(bh) * len + (i - r * len)] : 0ull;
+        if (cmode == 1 && i < total) cache[i] = cv[u];
+      }
     }
 #pragma unroll
     for (int u = 0; u < UNR; ++u) fn(cv[u]);
@@ -195,8 +205,11 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(MT, 1) shard_merge_
     M = warp_max_u64(mx);
   }
   // narrow candidates >= T* (this CTA: ranks cta, cta + CL, ...)
+  uint64_t* cache = reinterpret_cast<uint64_t*>(dyn + ((sizeof(MergeSmem) + 15) / 16) * 16);
+  const bool cacheable = ((G - cta + CL - 1) / CL) * p.narrow_len <= kMergeCache;
   uint32_t ge = 0;
-  sweep(p.narrow, G, p.narrow_len, bh, cta, [&](uint64_t c) { ge += c != 0ull && c >= Tstar; });
+  sweep(p.narrow, G, p.narrow_len, bh, cta, [&](uint64_t c) { ge += c != 0ull && c >= Tstar; }, cache,
+        cacheable ? 1 : 0);
   uint32_t ge_cta;
   block_excl(ge, s.wsum, &ge_cta);
   if (tid == 0) s.cnt = ge_cta;
@@ -210,6 +223,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(MT, 1) shard_merge_
   // ---- 2. source lists and the lower bound every global top-k row clears
   const uint64_t* const* lists = exact ? p.narrow : p.full;
   const int len = exact ? p.narrow_len : p.full_len;
+  const int cm = exact && cacheable ? 2 : 0;  // later sweeps of the narrow lists: from shared memory
   const uint64_t lo = exact ? Tstar : Tfull;
   const uint32_t klo = comp_key(lo), khi = comp_key(M);
   const uint32_t range = khi > klo ? khi - klo : 0u;
@@ -221,7 +235,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(MT, 1) shard_merge_
   __syncthreads();
   sweep(lists, G, len, bh, cta, [&](uint64_t c) {
     if (c != 0ull && c >= lo) atomicAdd(&s.hist[hist_digit(comp_key(c), klo, shift)], 1u);
-  });
+  }, cache, cm);
   __syncthreads();
   cluster.sync();
   constexpr int SB = kHistBins / CL;
@@ -326,7 +340,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(MT, 1) shard_merge_
         const uint32_t slot = wb + __popc(bm & lanemask_lt());
         if (inb && slot < static_cast<uint32_t>(kMergeBkt)) s.bkt[slot] = c;  // total <= kMergeBkt
       }
-    });
+    }, cache, cm);
   }
   cluster.sync();  // members complete; every remote read of hist / tot / slsum done
   MERGE_PHASE(50);
@@ -397,7 +411,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(MT, 1) shard_merge_
   // memory (rare) has no per-CTA member counts: those CTAs count and reserve globally.
   if (big) {
     uint32_t mine = 0;
-    sweep(lists, G, len, bh, cta, [&](uint64_t c) { mine += c != 0ull && c >= T; });
+    sweep(lists, G, len, bh, cta, [&](uint64_t c) { mine += c != 0ull && c >= T; }, cache, cm);
     uint32_t cta_total;
     block_excl(mine, s.wsum, &cta_total);
     if (tid == 0) s.obase = cta_total ? atomicAdd(&p.out_cnt[bh], cta_total) : 0u;
@@ -419,7 +433,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(MT, 1) shard_merge_
         sc_o[o] = key_score(comp_key(c));
       }
     }
-  });
+  }, cache, cm);
   cluster.sync();  // every CTA's (rare) global reservation is done: rank 0 re-arms the counter
   MERGE_PHASE(52);
   if (cta == 0) {
@@ -438,7 +452,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(MT, 1) shard_merge_
 }
 
 cudaError_t launch_shard_merge(const ShardMergeParams& p, int nbh, cudaStream_t s) {
-  const int smem = static_cast<int>(sizeof(MergeSmem));
+  const int smem = static_cast<int>((sizeof(MergeSmem) + 15) / 16 * 16 + kMergeCache * sizeof(uint64_t));
   const int attr = per_device(reinterpret_cast<const void*>(shard_merge_kernel), 0, [smem] {
     return static_cast<int>(cudaFuncSetAttribute(shard_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   });
