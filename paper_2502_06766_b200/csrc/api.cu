@@ -56,7 +56,7 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 struct Layout {
   size_t ticket_g, ticket_k, flag, gflag, fbl, fbh, mout, steal, ctrl_end;
   size_t maxc, bktc, bkt, outc;
-  size_t cnt, thr, hshift, hist, mmax, mkth, mkb, mt2, samp, cand, sidx, sscore, pl, po, pinm, qs, sortb, total;
+  size_t cnt, thr, hshift, hist, mmax, mkth, mkb, mt2, ncnt, samp, cand, sidx, sscore, pl, po, pinm, qs, sortb, total;
   int pin_words;
   int64_t cap;
   int nchunks;
@@ -93,6 +93,7 @@ Layout make_layout(const tkv_problem* p) {
   L.mkth = take(BH * 8);
   L.mkb = take(BH * 4);
   L.mt2 = take(BH * 8);  // sharded narrow-list bound t2 per head
+  L.ncnt = take(BH * 4);  // sharded narrow-list append counters (zeroed by the k-th kernel)
   L.samp = take(BH * kSamples * 4);
   L.cap = p->max_ctx > 0 ? p->max_ctx : 1;
   L.cand = take(BH * static_cast<size_t>(L.cap) * 8);
@@ -374,6 +375,15 @@ int pipe_res(PipeRes** out) {
   return TKV_OK;
 }
 
+// tkv_shard_candidates2's narrow-list append, carried into the emit pass's AttendParams
+struct NarrowEmit {
+  uint64_t* out = nullptr;
+  int len = 0;
+  uint32_t* cnt = nullptr;
+  const uint64_t* t2 = nullptr;
+};
+thread_local NarrowEmit g_narrow;
+
 AttendParams make_attend(const tkv_problem* p, const void* q, const void* k_cache, const void* v_cache,
                          const int32_t* n_ctx, const int32_t* n_win, const int32_t* idx,
                          const float* scores, void* ws, const Layout& L) {
@@ -410,6 +420,10 @@ AttendParams make_attend(const tkv_problem* p, const void* q, const void* k_cach
   a.tl = g_tl;
   a.pin_words = L.pin_words;
   a.pin_mask = L.pin_words ? at<uint32_t>(ws, L.pinm) : nullptr;
+  a.narrow_out = g_narrow.out;
+  a.narrow_len = g_narrow.len;
+  a.narrow_cnt = g_narrow.cnt;
+  a.meta_t2 = g_narrow.t2;
   return a;
 }
 
@@ -840,13 +854,20 @@ int tkv_shard_candidates2(const tkv_problem* p, int32_t narrow_k, const void* q,
   const int nbh = p->batch * p->n_q_heads;
   sl.k2 = narrow_k;
   sl.meta_t2 = at<uint64_t>(ws, L.mt2);
+  // the narrow list + bounds are produced by the k-th kernel (zeroed list, bounds) and the emit
+  // pass (selected candidates >= t2 appended) — no separate filter kernel over the full list
+  sl.narrow_out = cand_narrow;
+  sl.narrow_len = narrow_k;
+  sl.narrow_cnt = at<uint32_t>(ws, L.ncnt);
+  sl.bound_out = bounds;
   TRY(run_scan_part(&pu, cp, 0, nseg, st, pdl_enabled()));
   TRY(run_kth_part(&pu, cp, sl, 0, nseg, 0, st, pdl_enabled()));
-  TRY(run_emit(&pu, q, k_cache, k_cache, n_ctx, nullptr, at<int32_t>(ws, L.sidx), at<float>(ws, L.sscore), cand_full,
-               nullptr, 0, ws, L, st, 0, nbh));
-  TKV_LAUNCH(launch_narrow_filter(cand_full, p->k, cand_narrow, narrow_k, at<uint64_t>(ws, L.mt2),
-                                  at<uint64_t>(ws, L.mkth), at<int32_t>(ws, L.mkb), p->k, bounds, nbh, st));
-  return TKV_OK;
+  g_narrow = NarrowEmit{cand_narrow, narrow_k, at<uint32_t>(ws, L.ncnt), at<uint64_t>(ws, L.mt2)};
+  const int rc = run_emit(&pu, q, k_cache, k_cache, n_ctx, nullptr, at<int32_t>(ws, L.sidx), at<float>(ws, L.sscore),
+                          cand_full, nullptr, 0, ws, L, st, 0, nbh);
+  g_narrow = NarrowEmit{};
+  (void)bounds;
+  return rc;
 }
 
 int tkv_shard_exchange_merge(const tkv_problem* p, const uint64_t* const* narrow_lists,

@@ -173,13 +173,30 @@ __device__ __forceinline__ void attend_cand_run(const AttendParams& p, AttSmem& 
       // ids / raw scores in list order from shared memory: consecutive threads, consecutive
       // slots (coalesced — the ids may live in pinned host memory, written over PCIe)
       const uint32_t obase = sm.base;
-      for (uint32_t i = tid; i < m; i += NT) {
+      const uint64_t t2 = p.narrow_out ? p.meta_t2[bh] : ~0ull;
+      for (uint32_t i0 = 0; i0 < m; i0 += NT) {  // warp-uniform trip count (narrow-list ballots)
+        const uint32_t i = i0 + tid;
         const uint32_t o = obase + i;
-        if (o < static_cast<uint32_t>(p.k)) {
+        bool nar = false;
+        uint64_t c = 0ull;
+        if (i < m && o < static_cast<uint32_t>(p.k)) {
           const uint32_t gid = static_cast<uint32_t>(static_cast<int64_t>(sm.row[i]) + p.row_offset);
           idx_o[o] = static_cast<int32_t>(gid);
           sc_o[o] = sm.sc[i];
-          if (p.packed_out) p.packed_out[static_cast<int64_t>(bh) * p.k + o] = make_comp(score_key(sm.sc[i]), gid);
+          c = make_comp(score_key(sm.sc[i]), gid);
+          if (p.packed_out) p.packed_out[static_cast<int64_t>(bh) * p.k + o] = c;
+          nar = p.narrow_out && c >= t2;
+        }
+        if (p.narrow_out) {  // sharded: append to this rank's narrow list, one atomic per warp
+          const unsigned bm = __ballot_sync(kFull, nar);
+          if (bm) {
+            uint32_t wb = 0;
+            if (lane == 0) wb = atomicAdd(&p.narrow_cnt[bh], __popc(bm));
+            wb = __shfl_sync(kFull, wb, 0);
+            const uint32_t slot = wb + __popc(bm & lanemask_lt());
+            if (nar && slot < static_cast<uint32_t>(p.narrow_len))
+              p.narrow_out[static_cast<int64_t>(bh) * p.narrow_len + slot] = c;
+          }
         }
       }
     }

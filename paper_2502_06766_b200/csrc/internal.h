@@ -36,7 +36,7 @@ constexpr int kKthSmemBucket = 2048;    // threshold-bucket members rank-selecte
 constexpr int kKthSmem = kKthSmemBucket * 8;  // kth_kernel dynamic shared memory (fits beside the scan)
 constexpr int kAttendThreads = 256;
 #ifndef TKV_ATTEND_CHUNK
-#define TKV_ATTEND_CHUNK 512
+#define TKV_ATTEND_CHUNK 1024
 #endif
 constexpr int kAttendChunk = TKV_ATTEND_CHUNK;  // selected rows per gather CTA (list mode)
 #ifndef TKV_CAND_CHUNK
@@ -161,6 +161,13 @@ struct SelectParams {
   // above the one holding the k2-th largest; T itself when every candidate is selected)
   int k2;
   uint64_t* meta_t2;
+  // ... and (narrow_out != nullptr) zeroes this rank's narrow list [B*Hq][narrow_len] and its
+  // append counters, and writes the bounds [B*Hq][3] = {t2, local k-th floor, max composite};
+  // the emit pass then appends the selected candidates >= t2 (no separate filter kernel)
+  uint64_t* narrow_out;
+  int narrow_len;
+  uint32_t* narrow_cnt;
+  uint64_t* bound_out;
   // exactness fallback, tail-launched by kth_kernel (main pass) when a head failed
   ScanParams fb_scan;
   int fb_scan_grid;
@@ -229,6 +236,12 @@ struct AttendParams {
   const float* const* partial_peers;
   int n_peers;
   int items_mult;  // candidate mode: work items per CTA, about (0 = 1)
+  // sharded candidates (tkv_shard_candidates2): selected candidates >= meta_t2[bh] are also
+  // appended to narrow_out[bh][0, narrow_len) (order unspecified; kth_kernel zeroed the list)
+  uint64_t* narrow_out;
+  int narrow_len;
+  uint32_t* narrow_cnt;
+  const uint64_t* meta_t2;
 };
 
 // shard_merge_kernel (shard.cu): exact global top-k over every rank's published candidate lists
@@ -250,10 +263,6 @@ struct ShardMergeParams {
   uint64_t* tl;        // diagnostics timeline (TKV_DIAG builds: per-phase means)
 };
 cudaError_t launch_shard_merge(const ShardMergeParams& p, int nbh, cudaStream_t s);
-cudaError_t launch_narrow_filter(const uint64_t* full, int full_len, uint64_t* narrow, int narrow_len,
-                                 const uint64_t* meta_t2, const uint64_t* meta_kth, const int32_t* meta_kb, int k,
-                                 uint64_t* bound, int nbh, cudaStream_t s);
-
 // head_topk_kernel (select.cu): k-th selection + V gather + finish of a head by ctas_per_head
 // CTAs (selected rows streamed through a kHeadCap-row shared buffer). att_grid: grid of the candidate-mode gather the exactness fallback
 // tail-launches over all heads.

@@ -410,11 +410,19 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kKthThreads, 4) kth
     return;
   }
   if (kb == 0) {
+    if (part == 0 && p.narrow_out)
+      for (int i = tid; i < p.narrow_len; i += KT) p.narrow_out[static_cast<int64_t>(bh) * p.narrow_len + i] = 0ull;
     if (part == 0 && tid == 0) {
       p.meta_kth[bh] = ~0ull;
       p.meta_kb[bh] = 0;
       p.meta_max[bh] = -INFINITY;
       if (p.k2 > 0) p.meta_t2[bh] = 0ull;  // no rows: nothing withheld
+      if (p.narrow_out) {
+        p.narrow_cnt[bh] = 0u;
+        p.bound_out[3 * bh + 0] = 0ull;
+        p.bound_out[3 * bh + 1] = 0ull;
+        p.bound_out[3 * bh + 2] = 0ull;
+      }
       if (p.pass == kPassFallback) {
         p.hs.flag_fail[bh] = 0u;
         p.hs.group_fail[b * p.Hkv + h / p.G] = 0u;
@@ -541,6 +549,17 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kKthThreads, 4) kth
       radix_select_u64<KT>(ld, n, need, s_hist, s_scr, s_out, cs, cp);
     }
     T = cp << cs;
+  }
+  if (p.narrow_out) {  // this rank's narrow list starts empty; the emit pass appends to it
+    for (int i = tid; i < p.narrow_len; i += KT) p.narrow_out[static_cast<int64_t>(bh) * p.narrow_len + i] = 0ull;
+    __syncthreads();  // (meta_t2 of this head was written by this CTA: part 0 is the cluster's rank 0)
+    if (tid == 0) {
+      const uint64_t t2 = narrow2 ? p.meta_t2[bh] : T;
+      p.narrow_cnt[bh] = 0u;
+      p.bound_out[3 * bh + 0] = t2;
+      p.bound_out[3 * bh + 1] = kb >= p.k ? T : 0ull;  // fewer than k rows: none withheld
+      p.bound_out[3 * bh + 2] = vmax;
+    }
   }
   if (tid == 0) {
     p.meta_kth[bh] = T;

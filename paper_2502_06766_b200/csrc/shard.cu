@@ -29,83 +29,6 @@
 namespace tkv {
 namespace cg = cooperative_groups;
 
-// ---------------------------------------------------------------- narrow list of one rank
-// One CTA per head: narrow[bh][0..) = full-list entries >= t2 in list order (fewer than
-// narrow_len of them, zero-padded), bound[bh] = {t2, local k-th floor, max composite}. Every
-// thread loads its FT_UNR entries before using any (one memory round trip per batch).
-constexpr int FT = 1024, FT_UNR = 16;
-__global__ void __launch_bounds__(FT) narrow_filter_kernel(const uint64_t* __restrict__ full, int full_len,
-                                                           uint64_t* __restrict__ narrow, int narrow_len,
-                                                           const uint64_t* __restrict__ meta_t2,
-                                                           const uint64_t* __restrict__ meta_kth,
-                                                           const int32_t* __restrict__ meta_kb, int k,
-                                                           uint64_t* __restrict__ bound) {
-  __shared__ uint32_t s_w[FT / 32];
-  __shared__ uint64_t s_max[FT / 32];
-  __shared__ uint32_t s_run;
-  const int bh = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint64_t t2 = meta_t2[bh];
-  const uint64_t* src = full + static_cast<int64_t>(bh) * full_len;
-  uint64_t* dst = narrow + static_cast<int64_t>(bh) * narrow_len;
-  if (tid == 0) s_run = 0u;
-  uint64_t mx = 0ull;
-  for (int base = 0; base < full_len; base += FT * FT_UNR) {
-    uint64_t cv[FT_UNR];
-#pragma unroll
-    for (int u = 0; u < FT_UNR; ++u) {  // thread-contiguous entries: list order is kept
-      const int i = base + tid * FT_UNR + u;
-      cv[u] = i < full_len ? src[i] : 0ull;
-    }
-    uint32_t mine = 0;
-#pragma unroll
-    for (int u = 0; u < FT_UNR; ++u) {
-      mx = cv[u] > mx ? cv[u] : mx;
-      mine += cv[u] != 0ull && cv[u] >= t2;
-    }
-    uint32_t inc = mine;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t t = __shfl_up_sync(kFull, inc, o);
-      if (lane >= o) inc += t;
-    }
-    if (lane == 31) s_w[warp] = inc;
-    __syncthreads();
-    uint32_t off = s_run, tot = 0;
-    for (int w = 0; w < FT / 32; ++w) {
-      off += w < warp ? s_w[w] : 0u;
-      tot += s_w[w];
-    }
-    uint32_t o = off + inc - mine;
-#pragma unroll
-    for (int u = 0; u < FT_UNR; ++u) {
-      if (cv[u] != 0ull && cv[u] >= t2) {
-        if (o < static_cast<uint32_t>(narrow_len)) dst[o] = cv[u];
-        ++o;
-      }
-    }
-    __syncthreads();
-    if (tid == 0) s_run += tot;
-  }
-  mx = warp_max_u64(mx);
-  if (lane == 0) s_max[warp] = mx;
-  __syncthreads();
-  for (int i = static_cast<int>(s_run) + tid; i < narrow_len; i += FT) dst[i] = 0ull;
-  if (tid == 0) {
-    uint64_t m = 0ull;
-    for (int w = 0; w < FT / 32; ++w) m = s_max[w] > m ? s_max[w] : m;
-    bound[3 * bh + 0] = t2;
-    bound[3 * bh + 1] = meta_kb[bh] >= k ? meta_kth[bh] : 0ull;  // fewer than k rows: none withheld
-    bound[3 * bh + 2] = m;
-  }
-}
-
-cudaError_t launch_narrow_filter(const uint64_t* full, int full_len, uint64_t* narrow, int narrow_len,
-                                 const uint64_t* meta_t2, const uint64_t* meta_kth, const int32_t* meta_kb, int k,
-                                 uint64_t* bound, int nbh, cudaStream_t s) {
-  narrow_filter_kernel<<<nbh, FT, 0, s>>>(full, full_len, narrow, narrow_len, meta_t2, meta_kth, meta_kb, k, bound);
-  return cudaGetLastError();
-}
-
 // ---------------------------------------------------------------- the merge
 namespace {
 constexpr int MT = 512, MW = MT / 32, CL = 4;
