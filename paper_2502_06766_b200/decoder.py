@@ -52,6 +52,7 @@ class TopkDecoder:
         self._bufs = None
         self.ws = None
         self._graphs: dict[tuple, torch.cuda.CUDAGraph] = {}
+        self._last_direct = None  # (q, k_new, v_new, data pointers) of the last validated direct step
 
     def _ensure(self, Hq: int) -> None:
         if self.Hq == Hq:
@@ -91,6 +92,7 @@ class TopkDecoder:
             idx_h=torch.empty((self.B, Hq, self.k), dtype=i32, pin_memory=True),
         )
         self._graphs.clear()
+        self._last_direct = None
 
     # ------------------------------------------------------------------ device-side pieces
     def _reserve_row(self) -> None:
@@ -169,10 +171,20 @@ class TopkDecoder:
             self._reserve_row()
         Hq = q.shape[1]
         # pinned bf16 inputs of the right shape are read in place by the call (no host copy);
-        # the step's graph is then keyed by their addresses (a few cached)
-        direct = ((self.fold_append or not with_kv) and self._pinned_ok(q, (self.B, Hq, ops.HEAD_DIM))
-                  and (not with_kv or (self._pinned_ok(k_new, (self.B, self.Hkv, ops.HEAD_DIM))
-                                       and self._pinned_ok(v_new, (self.B, self.Hkv, ops.HEAD_DIM)))))
+        # the step's graph is then keyed by their addresses (a few cached). The same live tensor
+        # objects as the previous step skip the checks (Tensor.is_pinned() queries the driver: a
+        # few µs per tensor on the end-to-end path)
+        last = self._last_direct
+        if (last is not None and q is last[0] and k_new is last[1] and v_new is last[2]
+                and last[3] == (q.data_ptr(), k_new.data_ptr() if with_kv else 0,
+                                v_new.data_ptr() if with_kv else 0) and last[4] == q.shape):
+            direct = True
+        else:
+            direct = ((self.fold_append or not with_kv) and self._pinned_ok(q, (self.B, Hq, ops.HEAD_DIM))
+                      and (not with_kv or (self._pinned_ok(k_new, (self.B, self.Hkv, ops.HEAD_DIM))
+                                           and self._pinned_ok(v_new, (self.B, self.Hkv, ops.HEAD_DIM)))))
+            self._last_direct = (q, k_new, v_new, (q.data_ptr(), k_new.data_ptr() if with_kv else 0,
+                                                   v_new.data_ptr() if with_kv else 0), q.shape) if direct else None
         if direct:
             src = (q, k_new, v_new)
             key = (with_kv, return_idx, q.data_ptr(), k_new.data_ptr() if with_kv else 0,

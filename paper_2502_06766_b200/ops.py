@@ -140,6 +140,12 @@ def _as_counts(name: str, v, B: int, device) -> torch.Tensor:
     return torch.tensor(vals, dtype=torch.int32, device=device)
 
 
+def _host_max(v) -> int:
+    """Largest context length of a host-side n_ctx (int or sequence): no device reduction and
+    no device→host read on the call path."""
+    return int(v) if isinstance(v, int) else max(int(x) for x in v)
+
+
 @dataclass
 class Shapes:
     B: int
@@ -189,7 +195,7 @@ def topk_decode_attention(q, k_cache, v_cache, n_ctx, k: int, *, n_win=None, sca
     n_ctx_t = _as_counts("n_ctx", n_ctx, s.B, dev)
     n_win_t = None if n_win is None else _as_counts("n_win", n_win, s.B, dev)
     if max_ctx is None:
-        max_ctx = s.cache_rows if isinstance(n_ctx, torch.Tensor) else int(n_ctx_t.max().item())
+        max_ctx = s.cache_rows if isinstance(n_ctx, torch.Tensor) else _host_max(n_ctx)
     prob = make_problem(s.B, s.Hq, s.Hkv, s.cache_rows, max_ctx, k, pinned_prefix=pinned_prefix,
                         scale=scale, combine=combine, sorted=sorted, no_filter=no_filter,
                         row_offset=row_offset, tc_scan=tc_scan, parts=parts,
@@ -225,7 +231,7 @@ def topk_decode_step(q, k_new, v_new, k_cache, v_cache, n_ctx, n_win, k: int, *,
         if tuple(t.shape) != (s.B, s.Hkv, HEAD_DIM):
             raise ShapeError(f"{name} must be [B, Hkv, {HEAD_DIM}]")
     if max_ctx is None:
-        max_ctx = s.cache_rows if isinstance(n_ctx, torch.Tensor) else int(n_ctx_t.max().item())
+        max_ctx = s.cache_rows if isinstance(n_ctx, torch.Tensor) else _host_max(n_ctx)
     prob = make_problem(s.B, s.Hq, s.Hkv, s.cache_rows, max_ctx, k, pinned_prefix=pinned_prefix,
                         scale=scale, combine=combine, sorted=sorted, tc_scan=tc_scan,
                         parts=parts, list_gather=list_gather, head=head,
@@ -252,7 +258,7 @@ def topk_search(q, k_cache, n_ctx, k: int, *, sorted: bool = True, max_ctx: int 
     dev = k_cache.device
     n_ctx_t = _as_counts("n_ctx", n_ctx, s.B, dev)
     if max_ctx is None:
-        max_ctx = s.cache_rows if isinstance(n_ctx, torch.Tensor) else int(n_ctx_t.max().item())
+        max_ctx = s.cache_rows if isinstance(n_ctx, torch.Tensor) else _host_max(n_ctx)
     prob = make_problem(s.B, s.Hq, s.Hkv, s.cache_rows, max_ctx, k, sorted=sorted,
                         no_filter=no_filter, row_offset=row_offset, tc_scan=tc_scan,
                         parts=parts, head=head, host_q=not q.is_cuda)
