@@ -220,6 +220,7 @@ int run_prefix(const tkv_problem* p, const void* q, const void* k_cache, const i
   sp.k = p->k;
   sp.n_ctx = n_ctx;
   sp.no_filter = (p->flags & TKV_F_NO_FILTER) ? 1 : 0;
+  sp.max_samples = sample_max(p->max_ctx, p->k);
   sp.samp = at<uint32_t>(ws, L.samp);
   sp.hs = hs;
   sp.tl = g_tl;

@@ -52,9 +52,23 @@ constexpr uint32_t kNoFilterShift = 20;  // histogram shift when every score is 
 constexpr int kMinSampleStride = 8;      // small contexts sample at most every 8th row
 constexpr int kMaxParts = 16;            // KV-group parts of the overlapped layer pipeline
 
-// rows between two sampled rows: up to kSamples samples, never denser than 1 in 8
-__host__ __device__ inline int64_t sample_stride(int64_t n) {
-  const int64_t s = (n + kSamples - 1) / kSamples;
+// Half the sample (kSamples / 2) for contexts of at most kSmallCtxRows rows whose k is at most
+// 1/32 of them: there the threshold kernel ends while the key scan waits for it (its epilogue
+// cannot emit before), so the shorter radix select and the smaller sample grid shorten the step
+// (cfg2 70.0 -> 68.1 us). Beyond it the threshold is off the critical path and the tighter full
+// sample (fewer candidates) wins (cfg3 with 2048: 357.9 -> 361.5 us), and so it does at a large
+// k / N (a G = 8 shard of cfg3, 131K rows with k = 16384: candidates stage 92.4 -> 95.4 us).
+constexpr int64_t kSmallCtxRows = int64_t(1) << 17;
+
+// samples of a context of n rows with top-k size k (at most; also sizes the sample grid)
+__host__ __device__ inline int sample_max(int64_t n, int64_t k) {
+  return (n <= kSmallCtxRows && k * 32 <= n) ? kSamples / 2 : kSamples;
+}
+
+// rows between two sampled rows: up to sample_max(n, k) samples, never denser than 1 in 8
+__host__ __device__ inline int64_t sample_stride(int64_t n, int64_t k) {
+  const int64_t target = sample_max(n, k);
+  const int64_t s = (n + target - 1) / target;
   return s > kMinSampleStride ? s : kMinSampleStride;
 }
 
@@ -107,6 +121,7 @@ struct SampleParams {
   __nv_bfloat16* v_dst;
   int32_t* win_count;
   int pdl;  // sample_kernel launched behind the q staging kernel (TKV_F_HOST_Q)
+  int max_samples;  // largest sample of any batch entry (sample_max(max_ctx)): sizes the grid
 };
 
 // TKV_F_HOST_Q: q copied from pinned host memory into the workspace by one small kernel

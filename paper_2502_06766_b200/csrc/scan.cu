@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(kSampleThreads) sample_kernel(SampleParams p) 
   const int g = lane >> 2, c = lane & 3;
   const int64_t N = p.n_ctx[b];
   if (N <= 0) return;
-  const int64_t stride = sample_stride(N);
+  const int64_t stride = sample_stride(N, p.k);
   const int Sb = static_cast<int>((N + stride - 1) / stride);
   QFrag f;
   load_qfrag(f, p.q + (static_cast<int64_t>(b) * p.Hq + kvh * p.G) * kD, p.G, lane);
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(kThrThreads, 4) threshold_kernel(SampleParams 
   const int64_t kb = N < p.k ? N : p.k;
   int Sb = 0;
   if (N > 0) {
-    const int64_t stride = sample_stride(N);
+    const int64_t stride = sample_stride(N, p.k);
     Sb = static_cast<int>((N + stride - 1) / stride);
   }
   const double mu = N > 0 ? static_cast<double>(kb) * Sb / static_cast<double>(N) : 0.0;
@@ -402,7 +402,8 @@ cudaError_t launch_sample(const SampleParams& p, cudaStream_t s) {
     return 1;
   });
   if (!p.no_filter) {
-    dim3 grid(kSamples / kSampleThreads, p.B * p.Hkv);
+    const int ns = p.max_samples > 0 && p.max_samples < kSamples ? p.max_samples : kSamples;
+    dim3 grid((ns + kSampleThreads - 1) / kSampleThreads, p.B * p.Hkv);
     cudaError_t e = launch_pdl(sample_kernel, grid, dim3(kSampleThreads), 0, s, p.pdl != 0, p);
     if (e != cudaSuccess) return e;
   }

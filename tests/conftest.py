@@ -39,11 +39,12 @@ def cuda():
     return torch.device("cuda", 0)
 
 
-def sample_rows(n: int, seg: int) -> np.ndarray:
+def sample_rows(n: int, seg: int, k: int = 1 << 30) -> np.ndarray:
     """Rows the sampled threshold scores for segment seg = b * Hkv + kv head (restates
     sample_row / sample_stride in paper_2502_06766_b200/csrc/internal.h): adversarial caches put
     their outliers exactly there to force the exactness fallback."""
-    stride = max(8, -(-n // 4096))
+    target = 2048 if (n <= (1 << 17) and k * 32 <= n) else 4096  # sample_max: half the sample
+    stride = max(8, -(-n // target))
     h = (seg * 0x9E3779B9 + 0x7F4A7C15) & 0xFFFFFFFF
     r = np.arange(-(-n // stride), dtype=np.int64) * stride + (h >> 8) % stride
     return np.minimum(r, n - 1)

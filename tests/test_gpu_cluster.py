@@ -77,7 +77,7 @@ def test_cluster_kernel_fallback(cuda, k):
     B, Hq, Hkv, N = 1, 8, 2, 65536
     q, K, V = _make(rng, B, Hq, Hkv, N)
     K = O.to_bf16_f32(K * 0.01)
-    rr = sample_rows(N, 1)
+    rr = sample_rows(N, 1, k)
     K[0, 1, rr] = O.to_bf16_f32(np.sign(q[0, 4])[None, :] * 2.0 + K[0, 1, rr])
     prob = ops.make_problem(B, Hq, Hkv, N, N, k, head="cluster")
     ws = ops.Workspace(prob, cuda)

@@ -53,7 +53,7 @@ def test_fuzz_against_oracle(cuda, seed):
     _check(q, K, V, n_ctx, k, out, idx, sc, n_win=n_win, combine=combine, pinned=pin)
 
 
-def _adversarial(seed, q, K, n_ctx):
+def _adversarial(seed, q, K, n_ctx, k):
     """Distributions that stress the sampled threshold, the tie rule and the fallback."""
     from oracle import oracle as O
 
@@ -71,7 +71,7 @@ def _adversarial(seed, q, K, n_ctx):
         K[:] = O.to_bf16_f32(K * 0.01)
         for b in range(B):
             for h in range(Hkv):  # the rows the sampled threshold scores (n_ctx[b] rows)
-                rr = sample_rows(int(n_ctx[b]), b * Hkv + h)
+                rr = sample_rows(int(n_ctx[b]), b * Hkv + h, k)
                 K[b, h, rr] = O.to_bf16_f32(K[b, h, rr] + 2.0 * np.sign(q[b, :1, :]))
     elif kind == 3:  # large magnitudes
         K[:] = O.to_bf16_f32(K * 64.0)
@@ -92,7 +92,7 @@ def test_fuzz_adversarial(cuda, seed):
     B, Hq, Hkv, N, k, W, pin, combine, n_ctx, opts = _config(500 + seed)
     rng = np.random.default_rng(20_000 + seed)
     q, K, V = _make(rng, B, Hq, Hkv, N + W + 4)
-    K = _adversarial(seed, q, K, n_ctx)
+    K = _adversarial(seed, q, K, n_ctx, k)
     n_win = [W] * B
     out, idx, sc = _run(q, K, V, n_ctx, k, cuda, n_win=n_win, pinned_prefix=pin, combine=combine, **opts)
     torch.cuda.synchronize()

@@ -44,7 +44,7 @@ def test_head_kernel_fallback(cuda, k):
     B, Hq, Hkv, N = 1, 8, 2, 65536
     q, K, V = _make(rng, B, Hq, Hkv, N)
     K = O.to_bf16_f32(K * 0.01)
-    rr = sample_rows(N, 1)  # the rows the sampled threshold scores (b = 0, kv head 1)
+    rr = sample_rows(N, 1, k)  # the rows the sampled threshold scores (b = 0, kv head 1)
     K[0, 1, rr] = O.to_bf16_f32(np.sign(q[0, 4])[None, :] * 2.0 + K[0, 1, rr])
     out, idx, sc = _run(q, K, V, [N], k, cuda, head=True)
     torch.cuda.synchronize()

@@ -169,7 +169,7 @@ def test_fallback_when_sample_overestimates(cuda, head):
     B, Hq, Hkv, N, k = 1, 4, 1, 65536, 2048
     q, K, V = _make(rng, B, Hq, Hkv, N)
     K = O.to_bf16_f32(K * 0.01)
-    rr = sample_rows(N, 0)  # the rows the sampled threshold scores (b = 0, kv head 0)
+    rr = sample_rows(N, 0, k)  # the rows the sampled threshold scores (b = 0, kv head 0)
     K[0, 0, rr] = O.to_bf16_f32(np.sign(q[0, 0])[None, :] * 2.0 + K[0, 0, rr])
     from paper_2502_06766_b200 import ops
 

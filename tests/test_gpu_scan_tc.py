@@ -63,7 +63,7 @@ def test_tc_scan_fallback(cuda):
     B, Hq, Hkv, N, k = 1, 4, 1, 65536, 2048
     q, K, V = _make(rng, B, Hq, Hkv, N)
     K = O.to_bf16_f32(K * 0.01)
-    rr = sample_rows(N, 0)  # the rows the sampled threshold scores (kv head 0)
+    rr = sample_rows(N, 0, k)  # the rows the sampled threshold scores (kv head 0)
     K[0, 0, rr] = O.to_bf16_f32(np.sign(q[0, 0])[None, :] * 2.0 + K[0, 0, rr])
     out, idx, sc = _run(q, K, V, [N], k, cuda, tc_scan=True)
     torch.cuda.synchronize()
@@ -134,7 +134,7 @@ def test_overlapped_parts_fallback_and_graph(cuda):
     B, Hq, Hkv, N, k = 1, 16, 4, 65536, 2048
     q, K, V = _make(rng, B, Hq, Hkv, N)
     K = O.to_bf16_f32(K * 0.01)
-    rr = sample_rows(N, 3)  # adversarial sample for kv head 3 only (the last part)
+    rr = sample_rows(N, 3, k)  # adversarial sample for kv head 3 only (the last part)
     K[0, 3, rr] = O.to_bf16_f32(np.sign(q[0, 12])[None, :] * 2.0 + K[0, 3, rr])
     out, idx, sc = _run(q, K, V, [N], k, cuda, parts=4)
     torch.cuda.synchronize()
