@@ -58,7 +58,10 @@ constexpr int kMaxParts = 16;            // KV-group parts of the overlapped lay
 // (cfg2 70.0 -> 68.1 us). Beyond it the threshold is off the critical path and the tighter full
 // sample (fewer candidates) wins (cfg3 with 2048: 357.9 -> 361.5 us), and so it does at a large
 // k / N (a G = 8 shard of cfg3, 131K rows with k = 16384: candidates stage 92.4 -> 95.4 us).
-constexpr int64_t kSmallCtxRows = int64_t(1) << 17;
+#ifndef TKV_SMALL_CTX_LOG2
+#define TKV_SMALL_CTX_LOG2 17
+#endif
+constexpr int64_t kSmallCtxRows = int64_t(1) << TKV_SMALL_CTX_LOG2;
 
 // samples of a context of n rows with top-k size k (at most; also sizes the sample grid)
 __host__ __device__ inline int sample_max(int64_t n, int64_t k) {
